@@ -1,0 +1,170 @@
+// Common plumbing for the trisolve_b200 CUDA library (sm_100a).
+//
+// Error handling, device helpers (streaming loads, deterministic warp/block
+// reductions, last-block arrival), and the per-solve reduction workspace.
+// Every reduction in the library has a FIXED combination order that depends
+// only on the problem shape and the launch plan, never on timing: results are
+// bitwise reproducible run to run on the same GPU model (no fp64 atomics).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/trisolve_b200.h"
+
+namespace ts {
+
+// ---------------------------------------------------------------- errors ----
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+struct Err {
+  int code = 0;
+};
+
+#define TS_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::ts::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e),      \
+                      __FILE__, __LINE__);                                         \
+      return TS_ECUDA;                                                             \
+    }                                                                              \
+  } while (0)
+
+#define TS_CHECK(rc)          \
+  do {                        \
+    int _rc = (rc);           \
+    if (_rc != 0) return _rc; \
+  } while (0)
+
+#define TS_INVAL(...)             \
+  do {                            \
+    ::ts::set_error(__VA_ARGS__); \
+    return TS_EINVAL;             \
+  } while (0)
+
+// ------------------------------------------------------------- constants ----
+constexpr int kNT = 256;          // threads per block for every pass kernel
+constexpr int kWarps = kNT / 32;  // warps per block
+constexpr int kKMax = 8;          // max reduction slots per pass
+constexpr int kCW = 2 * kNT;      // dense A^T tile width (columns): 2 per thread
+constexpr int kTMax = 8;          // max CTA order supported on device
+
+enum RedOp : int { RED_SUM = 0, RED_MIN = 1 };
+
+// ------------------------------------------------------- device helpers ----
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_stream_i(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double red_combine(int op, double a, double b) {
+  return op == RED_MIN ? (b < a ? b : a) : a + b;  // fixed operand order
+}
+__device__ __forceinline__ double red_identity(int op) {
+  return op == RED_MIN ? INFINITY : 0.0;
+}
+
+// xor-butterfly warp reduction: fixed pattern, every lane ends with the value
+__device__ __forceinline__ double warp_reduce(double v, int op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block reduction of K slots; result valid in thread 0.  `sm` >= kWarps*K.
+template <int K, class Ops>
+__device__ __forceinline__ void block_reduce(double (&v)[K], double* sm, const Ops& ops) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_reduce(v[k], ops.op(k));
+  __syncthreads();  // protect sm reuse
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) sm[w * K + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = sm[k];
+      for (int j = 1; j < kWarps; ++j) s = red_combine(ops.op(k), s, sm[j * K + k]);
+      v[k] = s;
+    }
+  }
+}
+
+// Per-solve reduction workspace (device pointers).
+struct Work {
+  double* bacc;     // [pmax * kKMax] per-block partials
+  double* facc;     // [pmax * kKMax] split-row / split-tile epilogue partials
+  double* bpart;    // [pmax * 2] block boundary row-piece sums (first, last)
+  double* tpart;    // [pmax * 2 * kCW] block boundary tile pieces
+  unsigned* cnt;    // [pmax] split counters (self-resetting)
+  unsigned* done;   // [4] completion counters (self-resetting)
+  int pmax;
+};
+
+// All threads: returns true in every thread of the last block to arrive.
+__device__ __forceinline__ bool arrive_last(unsigned* counter, unsigned total, int* sflag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    int last = (prev == total - 1);
+    if (last) *counter = 0u;  // reset for the next launch (all others arrived)
+    *sflag = last;
+  }
+  __syncthreads();
+  bool last = *sflag != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// Final fixed-order reduction of per-block partials (+ fix partials), done by
+// the whole last block; result in thread 0.
+template <int K, class Ops>
+__device__ __forceinline__ void reduce_partials(const double* bacc, const double* facc, int nb,
+                                                double (&out)[K], double* sm, const Ops& ops) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = red_identity(ops.op(k));
+  for (int b = threadIdx.x; b < nb; b += kNT) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double v = __ldcg(bacc + (size_t)b * kKMax + k);
+      if (facc) v = red_combine(ops.op(k), v, __ldcg(facc + (size_t)b * kKMax + k));
+      out[k] = red_combine(ops.op(k), out[k], v);
+    }
+  }
+  block_reduce<K>(out, sm, ops);
+}
+
+inline int ceil_div_i(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace ts

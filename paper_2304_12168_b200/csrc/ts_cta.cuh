@@ -1,0 +1,381 @@
+// CTA (centering family) device pieces: moments epilogues, the equilibrated
+// min-norm Hankel solve, the monotone-retry candidate pass and the fused
+// residual / solution update (centering.py:67-213, driver 263-358).
+#pragma once
+
+#include "ts_state.cuh"
+
+namespace ts {
+
+// ---- equilibrated min-norm Hankel solve (centering.py:87-110) -------------
+// numpy: hankel[i,j] = phi[i+j+1]; rhs = phi[:t]; s = sqrt|diag| (0 -> 1);
+// beta = lstsq(hankel / outer(s,s), rhs / s, rcond) ; alpha = beta / s.
+// lstsq (LAPACK gelsd) is the SVD pseudo-inverse with singular values
+// <= rcond * s_max dropped.  The balanced matrix is exactly symmetric, so its
+// SVD is |eigen-decomposition|: cyclic Jacobi in fp64 gives the eigenpairs.
+// Returns false on non-finite input (numpy raises LinAlgError there).
+__device__ inline bool hankel_min_norm(const double* phi, int order, double rcond, double* alpha) {
+  double B[kTMax][kTMax], V[kTMax][kTMax], s[kTMax], c[kTMax];
+  const int t = order;
+  for (int i = 0; i < t; ++i) {
+    const double d = fabs(phi[2 * i + 1]);
+    s[i] = sqrt(d);
+    if (s[i] == 0.0) s[i] = 1.0;
+  }
+  bool finite = true;
+  for (int i = 0; i < t; ++i) {
+    for (int j = 0; j < t; ++j) {
+      B[i][j] = phi[i + j + 1] / (s[i] * s[j]);
+      V[i][j] = (i == j) ? 1.0 : 0.0;
+      finite = finite && isfinite(B[i][j]);
+    }
+    c[i] = phi[i] / s[i];
+    finite = finite && isfinite(c[i]);
+  }
+  if (!finite) return false;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < t; ++i)
+      for (int j = 0; j < t; ++j) {
+        const double v = B[i][j] * B[i][j];
+        tot += v;
+        if (i != j) off += v;
+      }
+    if (off <= 1e-34 * tot || off == 0.0) break;
+    for (int p = 0; p < t - 1; ++p) {
+      for (int q = p + 1; q < t; ++q) {
+        const double apq = B[p][q];
+        if (apq == 0.0) continue;
+        const double tau = (B[q][q] - B[p][p]) / (2.0 * apq);
+        const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        const double cs = 1.0 / sqrt(1.0 + tt * tt);
+        const double sn = tt * cs;
+        for (int k = 0; k < t; ++k) {  // B <- B J
+          const double bkp = B[k][p], bkq = B[k][q];
+          B[k][p] = cs * bkp - sn * bkq;
+          B[k][q] = sn * bkp + cs * bkq;
+        }
+        for (int k = 0; k < t; ++k) {  // B <- J^T B
+          const double bpk = B[p][k], bqk = B[q][k];
+          B[p][k] = cs * bpk - sn * bqk;
+          B[q][k] = sn * bpk + cs * bqk;
+        }
+        for (int k = 0; k < t; ++k) {  // V <- V J
+          const double vkp = V[k][p], vkq = V[k][q];
+          V[k][p] = cs * vkp - sn * vkq;
+          V[k][q] = sn * vkp + cs * vkq;
+        }
+      }
+    }
+  }
+  double smax = 0.0;
+  for (int k = 0; k < t; ++k) smax = fmax(smax, fabs(B[k][k]));
+  const double cut = rcond * smax;
+  double beta[kTMax];
+  for (int i = 0; i < t; ++i) beta[i] = 0.0;
+  for (int k = 0; k < t; ++k) {
+    const double lam = B[k][k];
+    if (!(fabs(lam) > cut)) continue;
+    double proj = 0.0;
+    for (int i = 0; i < t; ++i) proj += V[i][k] * c[i];
+    const double w = proj / lam;
+    for (int i = 0; i < t; ++i) beta[i] += w * V[i][k];
+  }
+  bool ok = true;
+  for (int i = 0; i < t; ++i) {
+    alpha[i] = beta[i] / s[i];
+    ok = ok && isfinite(alpha[i]);
+  }
+  return ok;
+}
+
+// triangle-wave order schedule (centering.py:254-260)
+__device__ __forceinline__ int sched_order(int t_max, int pos) {
+  if (t_max == 1) return 1;
+  const int len = 2 * t_max - 2;
+  const int k = pos % len;
+  return k < t_max ? k + 1 : 2 * t_max - 1 - k;
+}
+
+// loop top: `while iterations < max_iters`, residual checks, next order
+// (centering.py:296-304)
+__device__ inline void cta_head(SolveState* s) {
+  if (s->status != TS_RUNNING) return;
+  if (s->iterations >= s->max_iters) {
+    s->status = TS_ITERATION_CAP;
+    return;
+  }
+  if (!isfinite(s->r_norm)) {
+    s->status = TS_NUMERICAL_FAILURE;
+    s->detail = TS_DETAIL_NONFINITE_RESIDUAL;
+    return;
+  }
+  if (s->r_norm <= s->eps_abs) {
+    s->status = TS_APPROX_SOLUTION;
+    return;
+  }
+  s->t = sched_order(s->t_max, s->sched_pos);
+  s->sched_pos += 1;
+}
+
+// init (start = "zero"): r = b.  sums: b.b, r.r ; x = 0
+struct EpiCtaInit : EpiBase {
+  static constexpr int K = 2;
+  const double* b;
+  double *r, *x;
+  int64_t m, n;
+  __device__ bool active() const { return true; }
+  __device__ void elem(int64_t i, double (&acc)[K]) const {
+    if (i < m) {
+      const double bi = b[i];
+      r[i] = bi;
+      acc[0] = fma(bi, bi, acc[0]);
+      acc[1] = fma(bi, bi, acc[1]);
+    }
+    if (i < n) x[i] = 0.0;
+  }
+  __device__ void finish(double (&red)[K]) const;
+};
+// init (start = "random"): r = b - A x.  sums: b.b, r.r
+struct EpiCtaInitR : EpiBase {
+  static constexpr int K = 2;
+  const double* b;
+  double* r;
+  __device__ bool active() const { return true; }
+  __device__ void elem(int64_t i, double y, double (&acc)[K]) const {
+    const double bi = b[i];
+    const double ri = __dsub_rn(bi, y);
+    r[i] = ri;
+    acc[0] = fma(bi, bi, acc[0]);
+    acc[1] = fma(ri, ri, acc[1]);
+  }
+  __device__ void finish(double (&red)[K]) const;
+};
+
+__device__ inline void cta_init_finish(SolveState* s, double bb, double rr) {
+  s->t0 = globaltimer();
+  s->b_norm = sqrt(bb);
+  if (s->b_norm == 0.0) {
+    s->trivial = 1;
+    s->status = TS_APPROX_SOLUTION;
+    return;
+  }
+  s->eps_abs = s->epsilon * s->b_norm;
+  s->quad = s->eps_abs * s->eps_abs;
+  s->r_norm = sqrt(rr);
+  cta_head(s);
+}
+__device__ inline void EpiCtaInit::finish(double (&red)[K]) const { cta_init_finish(st, red[0], red[1]); }
+__device__ inline void EpiCtaInitR::finish(double (&red)[K]) const { cta_init_finish(st, red[0], red[1]); }
+
+__device__ __forceinline__ bool cta_pair_active(const SolveState* s, int i) {
+  return s->status == TS_RUNNING && s->maint == MAINT_NONE && s->t >= i;
+}
+
+// q_i = A^T p_{i-1}.  sums: q.q (kept for i == 1: ||A^T r||)
+struct EpiCtaQ : EpiBase {
+  static constexpr int K = 1;
+  double* q;
+  int i;
+  __device__ bool active() const { return cta_pair_active(st, i); }
+  __device__ void elem(int64_t j, double y, double (&acc)[K]) const {
+    q[j] = y;
+    acc[0] = fma(y, y, acc[0]);
+  }
+  __device__ void finish(double (&red)[K]) const {
+    if (i == 1) st->atr2 = red[0];
+  }
+};
+
+// p_i = A q_i (Gram) or A p_{i-1} (symmetric).  sums: p_{i-1}.p_i, p_i.p_i
+// -> phi_{2i-1}, phi_{2i} (centering.py:80-83)
+struct EpiCtaP : EpiBase {
+  static constexpr int K = 2;
+  const double* pprev;
+  double* p;
+  int i;
+  __device__ bool active() const { return cta_pair_active(st, i); }
+  __device__ void elem(int64_t r, double y, double (&acc)[K]) const {
+    p[r] = y;
+    acc[0] = fma(pprev[r], y, acc[0]);
+    acc[1] = fma(y, y, acc[1]);
+  }
+  __device__ void finish(double (&red)[K]) const {
+    st->phi[2 * i - 2] = red[0];
+    st->phi[2 * i - 1] = red[1];
+  }
+};
+
+// one thread per order: Hankel solves for orders 1..t (all speculatively; the
+// candidate pass then applies the reference's t..1 retry rule)
+__global__ void k_cta_hankel(SolveState* s) {
+  __shared__ int bad;
+  if (!(s->status == TS_RUNNING && s->maint == MAINT_NONE)) return;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  if (s->phi[1] == 0.0) {  // H r == 0: NormalEquationReached (centering.py:183-184)
+    if (threadIdx.x == 0) s->status = TS_NORMAL_EQ_SOLUTION;
+    return;
+  }
+  const int t = s->t;
+  const int o = threadIdx.x + 1;
+  if (o <= t) {
+    if (!hankel_min_norm(s->phi, o, s->rcond, s->alpha_o[o - 1])) atomicExch(&bad, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s->atr_norm = s->gram ? sqrt(s->atr2) : sqrt(s->phi[1]);
+    if (bad) {
+      s->status = TS_NUMERICAL_FAILURE;
+      s->detail = TS_DETAIL_MOMENT_SOLVE;
+    }
+  }
+}
+
+struct KrylovPtrs {
+  double* p[kTMax + 1];  // p[0] = r
+  double* q[kTMax];      // Gram directions
+};
+
+// candidate residuals for every order o <= t (r - sum_{i<=o} alpha^o_i p_i,
+// centering.py:189-199).  sums: ||cand_o||^2, o = 1..kTMax
+struct EpiCtaCand : EpiBase {
+  static constexpr int K = kTMax;
+  KrylovPtrs kp;
+  int64_t m;
+  __device__ bool active() const { return running(st); }
+  __device__ void elem(int64_t j, double (&acc)[K]) const {
+    const int t = st->t;
+    const double rj = kp.p[0][j];
+    double pv[kTMax];
+#pragma unroll
+    for (int i = 0; i < kTMax; ++i) pv[i] = (i < t) ? kp.p[i + 1][j] : 0.0;
+#pragma unroll
+    for (int o = 1; o <= kTMax; ++o) {
+      if (o > t) break;
+      double cv = rj;
+#pragma unroll
+      for (int i = 0; i < kTMax; ++i)
+        if (i < o) cv = __dsub_rn(cv, __dmul_rn(st->alpha_o[o - 1][i], pv[i]));
+      acc[o - 1] = fma(cv, cv, acc[o - 1]);
+    }
+  }
+  __device__ void finish(double (&red)[K]) const {
+    SolveState* s = st;
+    const int t = s->t;
+    int best = -1;
+    double best_n = 0.0;
+    for (int o = t; o >= 1; --o) {
+      const double cn = sqrt(red[o - 1]);
+      s->cand[o - 1] = cn;
+      if (best < 0 || cn < best_n) {
+        best = o;
+        best_n = cn;
+      }
+      if (cn <= s->r_norm * (1.0 + 1e-13)) {  // _MONOTONE_SLACK
+        best = o;
+        best_n = cn;
+        break;
+      }
+    }
+    s->sel_order = best;
+    trace_row(s, s->iterations, t, s->r_norm, s->atr_norm, 0.0, 0.0, globaltimer());
+    if (!s->known_solvable && s->atr_norm * s->atr_norm <= s->quad) {
+      s->status = TS_NORMAL_EQ_SOLUTION;  // x_new discarded (centering.py:318-323)
+      s->detail = TS_DETAIL_NE_CERTIFIED_CTA;
+      s->detail_value = s->eps_abs;
+      return;
+    }
+    s->blend = 0;
+    if (s->accelerate) {  // centering.py:324-332
+      const double ratio = s->r_norm > 0.0 ? best_n / s->r_norm : 0.0;
+      s->slow_steps = ratio > s->accel_ratio ? s->slow_steps + 1 : 0;
+      if (s->slow_steps >= s->accel_patience) {
+        s->w_blend = ratio / (1.0 + ratio);
+        s->blend = 1;
+        s->slow_steps = 0;
+      }
+    }
+  }
+};
+
+// r <- chosen candidate; x <- x + sum alpha_i dir_i (centering.py:200-204,
+// 333), optional acceleration blend.  sums: ||r||^2
+struct EpiCtaUpd : EpiBase {
+  static constexpr int K = 1;
+  KrylovPtrs kp;
+  double* x;
+  int64_t m, n;
+  int gram;
+  __device__ bool active() const { return running(st); }
+  __device__ void elem(int64_t j, double (&acc)[K]) const {
+    const int o = st->sel_order;
+    const double* al = st->alpha_o[o - 1];
+    const int blend = st->blend;
+    const double w = st->w_blend;
+    double rold = 0.0, rnew = 0.0;
+    if (j < m) {
+      rold = kp.p[0][j];
+      double cv = rold;
+      for (int i = 0; i < o; ++i) cv = __dsub_rn(cv, __dmul_rn(al[i], kp.p[i + 1][j]));
+      rnew = cv;
+    }
+    if (j < n) {
+      const double xo = x[j];
+      double xn = xo;
+      for (int i = 0; i < o; ++i) {
+        const double dv = gram ? kp.q[i][j] : (i == 0 ? rold : kp.p[i][j]);
+        xn = __dadd_rn(xn, __dmul_rn(al[i], dv));
+      }
+      if (blend) xn = __dadd_rn(__dmul_rn(w, xo), __dmul_rn(1.0 - w, xn));
+      x[j] = xn;
+    }
+    if (j < m) {
+      if (blend) rnew = __dadd_rn(__dmul_rn(w, rold), __dmul_rn(1.0 - w, rnew));
+      kp.p[0][j] = rnew;
+      acc[0] = fma(rnew, rnew, acc[0]);
+    }
+  }
+  __device__ void finish(double (&red)[K]) const {
+    SolveState* s = st;
+    s->iterations += 1;
+    s->r_norm = sqrt(red[0]);
+    if (s->recheck_every > 0 && (s->iterations % s->recheck_every) == 0) {
+      s->maint = MAINT_RECHECK;
+    } else {
+      cta_head(s);
+    }
+    tail();
+  }
+};
+
+// recheck (centering.py:344-352): fresh = b - A x; drift = ||fresh - r||;
+// r = fresh.  sums: ||fresh - r||^2, ||fresh||^2
+struct EpiCtaRecheck : EpiBase {
+  static constexpr int K = 2;
+  const double* b;
+  double* r;
+  __device__ bool active() const { return st->status == TS_RUNNING; }
+  __device__ void elem(int64_t i, double y, double (&acc)[K]) const {
+    const double f = __dsub_rn(b[i], y);
+    const double d = __dsub_rn(f, r[i]);
+    r[i] = f;
+    acc[0] = fma(d, d, acc[0]);
+    acc[1] = fma(f, f, acc[1]);
+  }
+  __device__ void finish(double (&red)[K]) const {
+    SolveState* s = st;
+    s->maint = MAINT_NONE;
+    const double drift = sqrt(red[0]);
+    const double scale = s->b_norm + s->a_fro * s->x_norm;
+    if (drift > 1e-10 * scale) {
+      s->status = TS_NUMERICAL_FAILURE;
+      s->detail = TS_DETAIL_DRIFT;
+      return;
+    }
+    s->r_norm = sqrt(red[1]);
+    cta_head(s);
+  }
+};
+
+}  // namespace ts

@@ -1,0 +1,465 @@
+// trisolve_b200: C ABI entry points, matrix creation, and the solve drivers.
+//
+// A solve = init kernels, then a CUDA graph whose single WHILE node runs one
+// device-resident iteration per trip (see ts_state.cuh) until the state
+// leaves RUNNING, needs host maintenance (CTA residual recheck every 250
+// iterations, TA b' revalidation every 512 pivots — both are cadences of the
+// reference, centering.py:344-352 / triangle.py:239-242), or the device trace
+// ring (seg_cap rows) needs flushing.  The host synchronises only at those
+// points, never inside an iteration.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "ts_cta.cuh"
+
+namespace ts {
+
+// ---------------------------------------------------------------- errors ----
+static thread_local char g_err[1024] = "";
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+static thread_local long long g_launches = 0;  // kernels enqueued by this thread
+
+// ------------------------------------------------------- device guards ----
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static std::once_flag g_pool_once[64];
+static void setup_pool(int dev) {
+  if (dev < 0 || dev >= 64) return;
+  std::call_once(g_pool_once[dev], [dev]() {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+static int sm_count(int dev) {
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
+// ------------------------------------------------------------ workspace ----
+// Owns stream-ordered allocations for one call.
+struct Arena {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Arena(cudaStream_t s) : st(s) {}
+  ~Arena() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <class T>
+  int get(T** out, size_t count) {
+    void* p = nullptr;
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) {
+      set_error("cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
+      return TS_ENOMEM;
+    }
+    ptrs.push_back(p);
+    *out = static_cast<T*>(p);
+    return 0;
+  }
+};
+
+static int make_work(Arena& ar, int pmax, Work* w) {
+  w->pmax = pmax;
+  TS_CHECK(ar.get(&w->bacc, (size_t)pmax * kKMax));
+  TS_CHECK(ar.get(&w->facc, (size_t)pmax * kKMax));
+  TS_CHECK(ar.get(&w->bpart, (size_t)pmax * 2));
+  TS_CHECK(ar.get(&w->tpart, (size_t)pmax * 2 * kCW));
+  TS_CHECK(ar.get(&w->cnt, (size_t)pmax));
+  TS_CHECK(ar.get(&w->done, 4));
+  TS_CUDA(cudaMemsetAsync(w->cnt, 0, sizeof(unsigned) * pmax, ar.st));
+  TS_CUDA(cudaMemsetAsync(w->done, 0, sizeof(unsigned) * 4, ar.st));
+  return 0;
+}
+
+// copy `count` doubles from any pointer (host or device) into a fresh buffer
+static int stage_in(Arena& ar, const double* src, size_t count, double** out) {
+  TS_CHECK(ar.get(out, count));
+  if (count) TS_CUDA(cudaMemcpyAsync(*out, src, count * sizeof(double), cudaMemcpyDefault, ar.st));
+  return 0;
+}
+
+// ----------------------------------------------------------------- plans ----
+static void flat_ranges(int64_t E, int64_t P, int64_t b, int wid, int64_t* s, int64_t* e) {
+  const int64_t S0 = E * b / P, S1 = E * (b + 1) / P, L = S1 - S0;
+  *s = S0 + L * wid / kWarps;
+  *e = S0 + L * (wid + 1) / kWarps;
+}
+
+int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* out,
+                  cudaStream_t st) {
+  RowPlan p;
+  const int64_t pmax = resident_blocks(sms);
+  const bool long_rows = rows > 0 && nnz / rows >= 32 && nnz >= (int64_t)kWarps * 256;
+  if (!long_rows) {
+    p.kind = PLAN_SHORT;
+    int64_t g = (rows + kNT - 1) / kNT;
+    p.P = (int)std::max<int64_t>(1, std::min(g, pmax));
+    *out = p;
+    return 0;
+  }
+  p.kind = PLAN_FLAT;
+  p.P = (int)std::max<int64_t>(1, std::min(pmax, nnz / ((int64_t)kWarps * 256)));
+  std::vector<int> wr((size_t)p.P * kWarps);
+  for (int64_t b = 0; b < p.P; ++b)
+    for (int w = 0; w < kWarps; ++w) {
+      int64_t s, e;
+      flat_ranges(nnz, p.P, b, w, &s, &e);
+      wr[b * kWarps + w] = (int)first_row_at(rp, rows, s);
+    }
+  TS_CUDA(cudaMalloc(&p.wrow, wr.size() * sizeof(int)));
+  TS_CUDA(cudaMemcpyAsync(p.wrow, wr.data(), wr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaStreamSynchronize(st));
+  *out = p;
+  return 0;
+}
+
+int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t st) {
+  RowPlan p;
+  const int64_t pmax = resident_blocks(sms);
+  const int64_t E = m * n;
+  if (n < 128 || E < (int64_t)kWarps * 256) {
+    p.kind = PLAN_SHORT;
+    p.P = (int)std::max<int64_t>(1, std::min((m + kNT - 1) / kNT, pmax));
+    *out = p;
+    return 0;
+  }
+  p.kind = PLAN_FLAT;
+  p.P = (int)std::max<int64_t>(1, std::min(pmax, E / ((int64_t)kWarps * 256)));
+  std::vector<int> wr((size_t)p.P * kWarps);
+  for (int64_t b = 0; b < p.P; ++b)
+    for (int w = 0; w < kWarps; ++w) {
+      int64_t s, e;
+      flat_ranges(E, p.P, b, w, &s, &e);
+      wr[b * kWarps + w] = (int)(s / n);
+    }
+  TS_CUDA(cudaMalloc(&p.wrow, wr.size() * sizeof(int)));
+  TS_CUDA(cudaMemcpyAsync(p.wrow, wr.data(), wr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaStreamSynchronize(st));
+  *out = p;
+  return 0;
+}
+
+// ------------------------------------------------------ small kernels ----
+struct EpiFroDense {
+  static constexpr int K = 1;
+  const double* a;
+  int64_t lda, n;
+  double* out;
+  __device__ int op(int) const { return RED_SUM; }
+  __device__ bool active() const { return true; }
+  __device__ void idle() const {}
+  __device__ void elem(int64_t i, double (&acc)[K]) const {
+    const double v = a[(i / n) * lda + (i % n)];
+    acc[0] = fma(v, v, acc[0]);
+  }
+  __device__ void finish(double (&r)[K]) const { *out = sqrt(r[0]); }
+};
+struct EpiFroVals {
+  static constexpr int K = 1;
+  const double* v;
+  double* out;
+  __device__ int op(int) const { return RED_SUM; }
+  __device__ bool active() const { return true; }
+  __device__ void idle() const {}
+  __device__ void elem(int64_t i, double (&acc)[K]) const { acc[0] = fma(v[i], v[i], acc[0]); }
+  __device__ void finish(double (&r)[K]) const { *out = sqrt(r[0]); }
+};
+// min / max of column indices (validation)
+struct EpiIdxRange {
+  static constexpr int K = 2;
+  const int* ci;
+  double* out;
+  __device__ int op(int k) const { return RED_MIN; }
+  __device__ bool active() const { return true; }
+  __device__ void idle() const {}
+  __device__ void elem(int64_t i, double (&acc)[K]) const {
+    const double v = (double)ci[i];
+    acc[0] = py_min(acc[0], v);
+    acc[1] = py_min(acc[1], -v);
+  }
+  __device__ void finish(double (&r)[K]) const {
+    out[0] = r[0];
+    out[1] = -r[1];
+  }
+};
+
+__global__ void k_expand_rows(const int* rp, int64_t rows, int* rowid) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    for (int k = rp[r]; k < rp[r + 1]; ++k) rowid[k] = (int)r;
+}
+__global__ void k_iota(int* v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int)i;
+}
+__global__ void k_gather_T(const int* perm, const int* rowid, const double* val, int* ciT,
+                           double* valT, int64_t nnz) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int k = perm[j];
+    ciT[j] = rowid[k];
+    valT[j] = val[k];
+  }
+}
+__global__ void k_rowptr_from_keys(const int* keys, int64_t nnz, int64_t ncols, int* rpT) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= nnz;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kc = (j < nnz) ? keys[j] : ncols;
+    const int64_t kp = (j > 0) ? keys[j - 1] : -1;
+    for (int64_t c = kp + 1; c <= kc; ++c) rpT[c] = (int)j;
+  }
+}
+
+static int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4096));
+}
+
+}  // namespace ts
+
+using namespace ts;
+
+struct ts_matrix : public ts::Mat {};
+
+// ======================================================================= ABI
+extern "C" {
+
+int ts_abi_version(void) { return TS_ABI_VERSION; }
+const char* ts_last_error(void) { return ts::last_error(); }
+int ts_device_count(int* count) {
+  TS_CUDA(cudaGetDeviceCount(count));
+  return 0;
+}
+
+int ts_matrix_destroy(ts_matrix* A) {
+  if (!A) return 0;
+  DeviceGuard g(A->dev);
+  void* ps[] = {A->a, A->rp, A->ci, A->val, A->rpT, A->ciT, A->valT, A->planN.wrow, A->planT.wrow};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  delete A;
+  return 0;
+}
+
+int ts_matrix_info(const ts_matrix* A, int64_t* m, int64_t* n, int64_t* nnz, int32_t* kind,
+                   double* fro) {
+  if (!A) TS_INVAL("null matrix handle");
+  if (m) *m = A->m;
+  if (n) *n = A->n;
+  if (nnz) *nnz = A->nnz;
+  if (kind) *kind = A->kind;
+  if (fro) *fro = A->fro;
+  return 0;
+}
+
+static int finish_create(ts_matrix* A, cudaStream_t st, Arena& ar) {
+  // Frobenius norm once (linalg.py:64-69); cached on the immutable handle
+  Work wk;
+  TS_CHECK(make_work(ar, resident_blocks(A->sms), &wk));
+  double* dfro;
+  TS_CHECK(ar.get(&dfro, 1));
+  if (A->kind == 0) {
+    EpiFroDense e{A->a, A->lda, A->n, dfro};
+    TS_CHECK(launch_vec(A->m * A->n, A->sms, e, wk, st));
+  } else {
+    EpiFroVals e{A->val, dfro};
+    TS_CHECK(launch_vec(A->nnz, A->sms, e, wk, st));
+  }
+  TS_CUDA(cudaMemcpyAsync(&A->fro, dfro, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TS_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, int device,
+                           void* stream, ts_matrix** out) {
+  if (!out) TS_INVAL("null output handle");
+  *out = nullptr;
+  if (m < 1 || n < 1) TS_INVAL("matrix must have at least one row and one column (got %lld x %lld)",
+                               (long long)m, (long long)n);
+  if (lda < n) TS_INVAL("lda (%lld) < n (%lld)", (long long)lda, (long long)n);
+  if (!a) TS_INVAL("null matrix data");
+  DeviceGuard g(device);
+  setup_pool(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  ts_matrix* A = new ts_matrix();
+  A->dev = device;
+  A->sms = sm_count(device);
+  A->kind = 0;
+  A->m = m;
+  A->n = n;
+  A->nnz = m * n;
+  A->lda = n >= 64 ? (n + 15) / 16 * 16 : (n + 1) / 2 * 2;
+  int rc = 0;
+  {
+    Arena ar(st);
+    cudaError_t e = cudaMalloc(&A->a, (size_t)A->lda * m * sizeof(double));
+    if (e != cudaSuccess) {
+      set_error("cudaMalloc(dense %lld x %lld) failed: %s", (long long)m, (long long)A->lda,
+                cudaGetErrorString(e));
+      rc = TS_ENOMEM;
+    }
+    if (!rc && A->lda != n) e = cudaMemsetAsync(A->a, 0, (size_t)A->lda * m * sizeof(double), st);
+    if (!rc && e == cudaSuccess)
+      e = cudaMemcpy2DAsync(A->a, A->lda * sizeof(double), a, lda * sizeof(double),
+                            n * sizeof(double), m, cudaMemcpyDefault, st);
+    if (!rc && e != cudaSuccess) {
+      set_error("dense upload failed: %s", cudaGetErrorString(e));
+      rc = TS_ECUDA;
+    }
+    if (!rc) rc = plan_rows_dense(m, n, A->sms, &A->planN, st);
+    if (!rc) {
+      A->planT.kind = PLAN_TILE;
+      A->planT.P = tile_grid(m, n, A->sms);
+    }
+    if (!rc) rc = finish_create(A, st, ar);
+  }
+  if (rc) {
+    ts_matrix_destroy(A);
+    return rc;
+  }
+  *out = A;
+  return 0;
+}
+
+int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const double* data,
+                         int64_t m, int64_t n, int64_t nnz, int device, void* stream,
+                         ts_matrix** out) {
+  if (!out) TS_INVAL("null output handle");
+  *out = nullptr;
+  if (m < 1 || n < 1) TS_INVAL("matrix must have at least one row and one column (got %lld x %lld)",
+                               (long long)m, (long long)n);
+  if (nnz < 0 || nnz >= (int64_t)INT32_MAX) TS_INVAL("nnz %lld outside the int32 index range", (long long)nnz);
+  if (!indptr || (nnz > 0 && (!indices || !data))) TS_INVAL("null CSR array");
+  DeviceGuard g(device);
+  setup_pool(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  // host copy of the row pointer for validation and planning
+  std::vector<int> rp_h((size_t)m + 1);
+  TS_CUDA(cudaMemcpyAsync(rp_h.data(), indptr, (m + 1) * sizeof(int), cudaMemcpyDefault, st));
+  TS_CUDA(cudaStreamSynchronize(st));
+  if (rp_h[0] != 0 || rp_h[m] != nnz) TS_INVAL("CSR indptr must start at 0 and end at nnz");
+  for (int64_t r = 0; r < m; ++r)
+    if (rp_h[r + 1] < rp_h[r]) TS_INVAL("CSR indptr is not nondecreasing at row %lld", (long long)r);
+
+  ts_matrix* A = new ts_matrix();
+  A->dev = device;
+  A->sms = sm_count(device);
+  A->kind = 1;
+  A->m = m;
+  A->n = n;
+  A->nnz = nnz;
+  int rc = 0;
+  auto fail = [&](int code) {
+    ts_matrix_destroy(A);
+    return code;
+  };
+  {
+    Arena ar(st);
+    const size_t nz = (size_t)std::max<int64_t>(nnz, 1);
+    if (cudaMalloc(&A->rp, (m + 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&A->ci, nz * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&A->val, nz * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&A->rpT, (n + 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&A->ciT, nz * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&A->valT, nz * sizeof(double)) != cudaSuccess) {
+      set_error("cudaMalloc for CSR storage failed (nnz=%lld)", (long long)nnz);
+      return fail(TS_ENOMEM);
+    }
+    if (cudaMemcpyAsync(A->rp, rp_h.data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice, st) ||
+        (nnz && cudaMemcpyAsync(A->ci, indices, nnz * sizeof(int), cudaMemcpyDefault, st)) ||
+        (nnz && cudaMemcpyAsync(A->val, data, nnz * sizeof(double), cudaMemcpyDefault, st))) {
+      set_error("CSR upload failed");
+      return fail(TS_ECUDA);
+    }
+    if (nnz > 0) {
+      // validate column indices on the device
+      Work wk;
+      if ((rc = make_work(ar, resident_blocks(A->sms), &wk))) return fail(rc);
+      double* rng;
+      if ((rc = ar.get(&rng, 2))) return fail(rc);
+      EpiIdxRange er{A->ci, rng};
+      if ((rc = launch_vec(nnz, A->sms, er, wk, st))) return fail(rc);
+      double hr[2];
+      cudaMemcpyAsync(hr, rng, sizeof(hr), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (hr[0] < 0 || hr[1] >= (double)n) {
+        set_error("CSR column index out of range [0, %lld)", (long long)n);
+        return fail(TS_EINVAL);
+      }
+      // transposed CSR: stable radix sort of (column, position)
+      int *rowid, *keys_out, *perm_in, *perm_out;
+      if ((rc = ar.get(&rowid, nz)) || (rc = ar.get(&keys_out, nz)) || (rc = ar.get(&perm_in, nz)) ||
+          (rc = ar.get(&perm_out, nz)))
+        return fail(rc);
+      k_expand_rows<<<grid_for(m), 256, 0, st>>>(A->rp, m, rowid);
+      k_iota<<<grid_for(nnz), 256, 0, st>>>(perm_in, nnz);
+      int end_bit = 1;
+      while (end_bit < 31 && ((int64_t)1 << end_bit) < n) ++end_bit;
+      size_t tmp_bytes = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, A->ci, keys_out, perm_in, perm_out,
+                                      (int)nnz, 0, end_bit, st);
+      void* tmp;
+      if ((rc = ar.get((char**)&tmp, tmp_bytes))) return fail(rc);
+      if (cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, A->ci, keys_out, perm_in, perm_out,
+                                          (int)nnz, 0, end_bit, st) != cudaSuccess) {
+        set_error("radix sort for the transposed CSR failed");
+        return fail(TS_ECUDA);
+      }
+      k_gather_T<<<grid_for(nnz), 256, 0, st>>>(perm_out, rowid, A->val, A->ciT, A->valT, nnz);
+      k_rowptr_from_keys<<<grid_for(nnz + 1), 256, 0, st>>>(keys_out, nnz, n, A->rpT);
+    } else {
+      cudaMemsetAsync(A->rpT, 0, (n + 1) * sizeof(int), st);
+    }
+    if (cudaGetLastError() != cudaSuccess) {
+      set_error("CSR transpose kernels failed");
+      return fail(TS_ECUDA);
+    }
+    std::vector<int> rpT_h((size_t)n + 1);
+    cudaMemcpyAsync(rpT_h.data(), A->rpT, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("CSR transpose failed: %s", cudaGetErrorString(cudaGetLastError()));
+      return fail(TS_ECUDA);
+    }
+    if ((rc = plan_rows_csr(rp_h.data(), m, nnz, A->sms, &A->planN, st))) return fail(rc);
+    if ((rc = plan_rows_csr(rpT_h.data(), n, nnz, A->sms, &A->planT, st))) return fail(rc);
+    if (nnz > 0) {
+      if ((rc = finish_create(A, st, ar))) return fail(rc);
+    } else {
+      A->fro = 0.0;
+    }
+  }
+  *out = A;
+  return 0;
+}
+
+}  // extern "C"
+
+#include "ts_drivers.cuh"

@@ -1,0 +1,128 @@
+// Matrix handles (ts_matrix) and launch plans.
+//
+// HBM layout:
+//   dense  row-major fp64, leading dimension padded to a multiple of 16
+//          doubles (128 B) for n >= 64 (even otherwise) so every row starts
+//          on a 128-byte line and every double2 load is aligned.
+//   CSR    int32 row pointers, int32 column indices, fp64 values (A v).
+//   CSR^T  the transposed CSR (= CSC of A), built on the device once by a
+//          stable radix sort on the column index, so A^T v is a per-column
+//          gather in ascending row order (the reference's `v @ csr` scatter
+//          order, linalg.py:55) with no atomics.
+//
+// Each orientation gets a RowPlan: which kernel (flat split or thread-per-row)
+// and, for the flat split, the first row touched by every warp.
+#pragma once
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "ts_passes.cuh"
+
+namespace ts {
+
+enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2 };
+
+struct RowPlan {
+  int kind = PLAN_SHORT;
+  int P = 1;            // blocks
+  int* wrow = nullptr;  // device [P * kWarps] (PLAN_FLAT)
+};
+
+struct Mat {
+  int dev = 0;
+  int sms = 148;
+  int64_t m = 0, n = 0, nnz = 0;
+  int kind = 0;  // 0 dense, 1 csr
+  // dense
+  double* a = nullptr;
+  int64_t lda = 0;
+  // csr + transposed csr
+  int *rp = nullptr, *ci = nullptr, *rpT = nullptr, *ciT = nullptr;
+  double *val = nullptr, *valT = nullptr;
+  double fro = 0.0;
+  RowPlan planN, planT;
+  int Pmax = 0;  // largest grid any pass of this matrix uses
+
+  DenseRows dense() const { return DenseRows{a, lda, m, n}; }
+  CsrRows csr() const { return CsrRows{rp, ci, val, m, nnz}; }
+  CsrRows csrT() const { return CsrRows{rpT, ciT, valT, n, nnz}; }
+};
+
+inline int resident_blocks(int sms) { return sms * (2048 / kNT); }
+
+// first row touched by the warp whose range starts at s (see k_rows_flat)
+inline int64_t first_row_at(const int* rp, int64_t rows, int64_t s) {
+  // q = largest r in [0, rows) with rp[r] <= s
+  int64_t lo = 0, hi = rows - 1;
+  while (lo < hi) {
+    int64_t mid = (lo + hi + 1) / 2;
+    if (rp[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  int64_t q = lo;
+  if (rp[q] < s) return q;  // s strictly inside row q (continuation)
+  // rp[q] == s: first row of the run starting at s
+  int64_t lo2 = 0, hi2 = q;
+  while (lo2 < hi2) {
+    int64_t mid = (lo2 + hi2) / 2;
+    if (rp[mid] >= s) hi2 = mid; else lo2 = mid + 1;
+  }
+  return lo2;
+}
+
+int plan_rows_csr(const int* rp_host, int64_t rows, int64_t nnz, int sms, RowPlan* out,
+                  cudaStream_t st);
+int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t st);
+
+inline int vec_grid(int64_t len, int sms) {
+  int64_t g = (len + kNT * 4 - 1) / (kNT * 4);
+  int64_t pmax = resident_blocks(sms);
+  if (g > pmax) g = pmax;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+inline int tile_grid(int64_t m, int64_t n, int sms) {
+  const int64_t nct = (n + kCW - 1) / kCW;
+  const int64_t U = nct * m;
+  int64_t g = U / 32;  // >= 32 rows of a tile per block
+  const int64_t pmax = resident_blocks(sms);
+  if (g > pmax) g = pmax;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ------------------------------------------------------------ dispatch ----
+// y = M v (trans = 0) or y = M^T v (trans = 1) with a fused epilogue.
+template <class Epi>
+int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi, const Work& wk,
+                cudaStream_t st) {
+  if (M.kind == 0) {
+    if (!trans) {
+      if (M.planN.kind == PLAN_FLAT)
+        k_rows_flat<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk,
+                                                                 M.planN.wrow);
+      else
+        k_rows_short<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+    } else {
+      k_cols_tile<Epi><<<M.planT.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+    }
+  } else {
+    const RowPlan& pl = trans ? M.planT : M.planN;
+    const CsrRows acc = trans ? M.csrT() : M.csr();
+    if (pl.kind == PLAN_FLAT)
+      k_rows_flat<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk, pl.wrow);
+    else
+      k_rows_short<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
+  }
+  TS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <class Epi>
+int launch_vec(int64_t len, int sms, const Epi& epi, const Work& wk, cudaStream_t st) {
+  k_vec<Epi><<<vec_grid(len, sms), kNT, 0, st>>>(len, epi, wk);
+  TS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace ts

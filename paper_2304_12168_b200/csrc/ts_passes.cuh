@@ -1,0 +1,466 @@
+// Streaming "pass" kernels: one read of the matrix per launch, a per-output
+// epilogue fused in, and a deterministic multi-slot reduction whose last
+// arriving block runs a scalar finisher (the solver state machine).
+//
+//   k_rows_flat  y = M v, M row-major (dense rows or CSR).  The flat element
+//                range [0, E) is split into equal contiguous ranges per block
+//                and per warp, so every launch is perfectly load balanced for
+//                any row-length distribution; rows cut by a warp boundary are
+//                merged inside the block, rows cut by a block boundary are
+//                merged by the last block to arrive on that row (counter per
+//                end block).  Used for dense A v (n >= 128) and CSR rows with
+//                >= 32 nnz on average (C5's A v: ~1000 nnz / row).
+//   k_rows_short one thread per row, sequential left-to-right sum without FMA
+//                contraction: bitwise identical to scipy's csr_matvec for
+//                CSR (C3/C4 rows, C5's transposed CSR = CSC columns).
+//   k_cols_tile  y = A^T v for dense row-major A without materialising A^T:
+//                512-column tiles, the (tile, row) unit space split evenly over
+//                blocks, partial tiles at block boundaries merged by the last
+//                arriving block.  Fixed-order, no atomics on values.
+//   k_vec        fused elementwise vector pass (+ reductions, + finisher).
+//
+// Epilogue contract (class Epi):
+//   static constexpr int K;               reduction slots (<= kKMax)
+//   __device__ int  op(int k) const;       RED_SUM / RED_MIN
+//   __device__ bool active() const;        read once at kernel entry
+//   __device__ void elem(int64 i, double y, double (&acc)[K]) const;   passes
+//   __device__ void elem(int64 i, double (&acc)[K]) const;             k_vec
+//   __device__ void finish(double (&red)[K]) const;  thread 0, last block
+//   __device__ void idle() const;           block 0 / thread 0 when inactive
+#pragma once
+
+#include "ts_common.cuh"
+
+namespace ts {
+
+// Input-vector transform applied on load: identity, or v -> s * v, or
+// v -> s * max(v, 0) (the TA pivot preimage rho c / ||c||, c+ for the LP).
+// `s` is read from device state at kernel entry.
+struct XS {
+  const double* sp = nullptr;  // nullptr: identity
+  int relu = 0;
+  double s = 1.0;
+  __device__ __forceinline__ void load() {
+    if (sp) s = *sp;
+  }
+  __device__ __forceinline__ double operator()(double v) const {
+    if (!sp) return v;
+    if (relu) v = (v >= 0.0 || v != v) ? v : 0.0;  // numpy.maximum(c, 0.0) (NaN kept)
+    return __dmul_rn(s, v);
+  }
+};
+
+__device__ __forceinline__ double2 ldg2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+// ------------------------------------------------------------ accessors ----
+struct DenseRows {
+  const double* a;
+  int64_t lda, m, n;
+  __device__ __forceinline__ int64_t rbeg(int64_t r) const { return r * n; }
+  __device__ __forceinline__ int64_t rend(int64_t r) const { return (r + 1) * n; }
+  __device__ __forceinline__ int64_t total() const { return m * n; }
+  __device__ __forceinline__ int64_t rows() const { return m; }
+  // lane partial of sum_{k0<=k<k1} a[r, k - r n] * xs(x[k - r n])
+  __device__ __forceinline__ double seg(int64_t r, int64_t k0, int64_t k1, const double* x,
+                                        const XS& xs, int lane) const {
+    const int64_t c0 = k0 - r * n, c1 = k1 - r * n;
+    const double* row = a + r * lda;
+    double h = 0.0, t = 0.0;
+    int64_t c = c0;
+    if (c & 1) {
+      if (lane == 0) h = row[c] * xs(__ldg(x + c));
+      ++c;
+    }
+    const int64_t npair = (c1 - c) >> 1;
+    const int64_t cend = c + 2 * npair;
+    if (cend < c1 && lane == 0) t = row[cend] * xs(__ldg(x + cend));
+    const double* rp = row + c;
+    const double* xp = x + c;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t p = lane;
+    for (; p + 96 < npair; p += 128) {
+      double2 v0 = ld_stream2(rp + 2 * p), v1 = ld_stream2(rp + 2 * (p + 32));
+      double2 v2 = ld_stream2(rp + 2 * (p + 64)), v3 = ld_stream2(rp + 2 * (p + 96));
+      double2 x0 = ldg2(xp + 2 * p), x1 = ldg2(xp + 2 * (p + 32));
+      double2 x2 = ldg2(xp + 2 * (p + 64)), x3 = ldg2(xp + 2 * (p + 96));
+      a0 = fma(v0.x, xs(x0.x), a0); a0 = fma(v0.y, xs(x0.y), a0);
+      a1 = fma(v1.x, xs(x1.x), a1); a1 = fma(v1.y, xs(x1.y), a1);
+      a2 = fma(v2.x, xs(x2.x), a2); a2 = fma(v2.y, xs(x2.y), a2);
+      a3 = fma(v3.x, xs(x3.x), a3); a3 = fma(v3.y, xs(x3.y), a3);
+    }
+    for (; p < npair; p += 32) {
+      double2 v0 = ld_stream2(rp + 2 * p);
+      double2 x0 = ldg2(xp + 2 * p);
+      a0 = fma(v0.x, xs(x0.x), a0); a0 = fma(v0.y, xs(x0.y), a0);
+    }
+    return ((a0 + a1) + (a2 + a3)) + (h + t);
+  }
+  // whole row, one thread, column order (short-row path)
+  __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
+    const double* row = a + r * lda;
+    double s = 0.0;
+    for (int64_t c = 0; c < n; ++c) s = fma(row[c], xs(__ldg(x + c)), s);
+    return s;
+  }
+};
+
+struct CsrRows {
+  const int* rp;
+  const int* ci;
+  const double* val;
+  int64_t m, nnz;
+  __device__ __forceinline__ int64_t rbeg(int64_t r) const { return __ldg(rp + r); }
+  __device__ __forceinline__ int64_t rend(int64_t r) const { return __ldg(rp + r + 1); }
+  __device__ __forceinline__ int64_t total() const { return nnz; }
+  __device__ __forceinline__ int64_t rows() const { return m; }
+  __device__ __forceinline__ double seg(int64_t r, int64_t k0, int64_t k1, const double* x,
+                                        const XS& xs, int lane) const {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t k = k0 + lane;
+    for (; k + 96 < k1; k += 128) {
+      double v0 = ld_stream(val + k), v1 = ld_stream(val + k + 32);
+      double v2 = ld_stream(val + k + 64), v3 = ld_stream(val + k + 96);
+      int j0 = ld_stream_i(ci + k), j1 = ld_stream_i(ci + k + 32);
+      int j2 = ld_stream_i(ci + k + 64), j3 = ld_stream_i(ci + k + 96);
+      a0 = fma(v0, xs(__ldg(x + j0)), a0);
+      a1 = fma(v1, xs(__ldg(x + j1)), a1);
+      a2 = fma(v2, xs(__ldg(x + j2)), a2);
+      a3 = fma(v3, xs(__ldg(x + j3)), a3);
+    }
+    for (; k < k1; k += 32) a0 = fma(ld_stream(val + k), xs(__ldg(x + ld_stream_i(ci + k))), a0);
+    return (a0 + a1) + (a2 + a3);
+  }
+  // scipy csr_matvec order: sum = 0; sum += A_ij * x_j left to right; no FMA
+  __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
+    const int k0 = __ldg(rp + r), k1 = __ldg(rp + r + 1);
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k)
+      s = __dadd_rn(s, __dmul_rn(ld_stream(val + k), xs(__ldg(x + ld_stream_i(ci + k)))));
+    return s;
+  }
+};
+
+// block containing flat element p when [0,E) is split as floor(b E / P)
+__device__ __forceinline__ int64_t blk_of(int64_t p, int64_t E, int64_t P) {
+  return ((p + 1) * P + E - 1) / E - 1;
+}
+
+// ----------------------------------------------------------- k_rows_flat ----
+template <class Acc, class Epi>
+__global__ void __launch_bounds__(kNT) k_rows_flat(Acc A, const double* __restrict__ x, XS xs,
+                                                   Epi epi, Work wk,
+                                                   const int* __restrict__ wrow) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ double wacc[kWarps][K];
+  __shared__ long long prow[kWarps][2];
+  __shared__ double psum[kWarps][2];
+  __shared__ int pcnt[kWarps];
+  __shared__ int sflag;
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  xs.load();
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t E = A.total();
+  const int64_t S0 = E * b / P, S1 = E * (b + 1) / P;
+  const int64_t L = S1 - S0;
+  const int64_t s = S0 + L * wid / kWarps, e = S0 + L * (wid + 1) / kWarps;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  int np = 0;
+  long long pr[2] = {0, 0};
+  double ps[2] = {0.0, 0.0};
+  if (s < e) {
+    const bool gl_last = (b == P - 1) && (wid == kWarps - 1);
+    for (int64_t r = wrow[b * kWarps + wid]; r < A.rows(); ++r) {
+      const int64_t rb = A.rbeg(r), re = A.rend(r);
+      if (!(rb < e || (gl_last && rb == e))) break;
+      const int64_t k0 = rb > s ? rb : s, k1 = re < e ? re : e;
+      double v = (k1 > k0) ? A.seg(r, k0, k1, x, xs, lane) : 0.0;
+      v = warp_reduce(v, RED_SUM);
+      if (k0 == rb && k1 == re) {
+        if (lane == 0) epi.elem(r, v, acc);
+      } else if (np < 2) {
+        pr[np] = r;
+        ps[np] = v;
+        ++np;
+      }
+    }
+  }
+  if (lane == 0) {
+    pcnt[wid] = np;
+    prow[wid][0] = pr[0];
+    prow[wid][1] = pr[1];
+    psum[wid][0] = ps[0];
+    psum[wid][1] = ps[1];
+#pragma unroll
+    for (int k = 0; k < K; ++k) wacc[wid][k] = acc[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double macc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) macc[k] = red_identity(epi.op(k));
+    // merge warp pieces in warp order; rows wholly inside the block finish here
+    long long cur = -1;
+    double csum = 0.0;
+    long long brow_first = -1, brow_last = -1;
+    double bsum_first = 0.0, bsum_last = 0.0;
+    auto flush = [&](long long row, double sum) {
+      const int64_t rb = A.rbeg(row), re = A.rend(row);
+      const bool before = rb < S0, after = re > S1;
+      if (!before && !after) {
+        epi.elem(row, sum, macc);
+      } else if (before) {
+        brow_first = row;
+        bsum_first = sum;
+      } else {
+        brow_last = row;
+        bsum_last = sum;
+      }
+    };
+    for (int j = 0; j < kWarps; ++j) {
+      for (int i = 0; i < pcnt[j]; ++i) {
+        const long long row = prow[j][i];
+        const double sum = psum[j][i];
+        if (cur == row) {
+          csum += sum;
+        } else {
+          if (cur >= 0) flush(cur, csum);
+          cur = row;
+          csum = sum;
+        }
+      }
+    }
+    if (cur >= 0) flush(cur, csum);
+    // block accumulator: warps in order, then the merged rows
+    double bacc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double v = wacc[0][k];
+      for (int j = 1; j < kWarps; ++j) v = red_combine(epi.op(k), v, wacc[j][k]);
+      bacc[k] = red_combine(epi.op(k), v, macc[k]);
+      wk.bacc[b * kKMax + k] = bacc[k];
+    }
+    // is this block the end block of a row that started in an earlier block?
+    bool end_block = false;
+    if (brow_first >= 0 && A.rend(brow_first) <= S1) end_block = true;
+    if (!end_block) {
+      for (int k = 0; k < K; ++k) wk.facc[b * kKMax + k] = red_identity(epi.op(k));
+    }
+    // publish boundary pieces, then take part in the split-row merges
+    if (brow_first >= 0) wk.bpart[b * 2 + 0] = bsum_first;
+    if (brow_last >= 0) wk.bpart[b * 2 + 1] = bsum_last;
+    for (int which = 0; which < 2; ++which) {
+      const long long row = which == 0 ? brow_first : brow_last;
+      if (row < 0) continue;
+      const int64_t rb = A.rbeg(row), re = A.rend(row);
+      const int64_t ba = blk_of(rb, E, P), bb = blk_of(re - 1, E, P);
+      __threadfence();
+      const unsigned prev = atomicAdd(wk.cnt + bb, 1u);
+      if (prev == (unsigned)(bb - ba)) {
+        __threadfence();
+        double y = __ldcg(wk.bpart + ba * 2 + 1);
+        for (int64_t q = ba + 1; q <= bb; ++q) y += __ldcg(wk.bpart + q * 2 + 0);
+        double facc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) facc[k] = red_identity(epi.op(k));
+        epi.elem(row, y, facc);
+#pragma unroll
+        for (int k = 0; k < K; ++k) wk.facc[bb * kKMax + k] = facc[k];
+        wk.cnt[bb] = 0u;
+      }
+    }
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
+    if (threadIdx.x == 0) epi.finish(red);
+  }
+}
+
+// ---------------------------------------------------------- k_rows_short ----
+template <class Acc, class Epi>
+__global__ void __launch_bounds__(kNT) k_rows_short(Acc A, const double* __restrict__ x, XS xs,
+                                                    Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  xs.load();
+  const int64_t P = gridDim.x, b = blockIdx.x, m = A.rows();
+  const int64_t R0 = m * b / P, R1 = m * (b + 1) / P;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  for (int64_t r = R0 + threadIdx.x; r < R1; r += kNT) epi.elem(r, A.row_serial(r, x, xs), acc);
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, epi);
+    if (threadIdx.x == 0) epi.finish(red);
+  }
+}
+
+// ----------------------------------------------------------- k_cols_tile ----
+template <class Epi>
+__global__ void __launch_bounds__(kNT) k_cols_tile(DenseRows A, const double* __restrict__ x,
+                                                   XS xs, Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  constexpr int RU = 8;  // rows in flight per thread
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  xs.load();
+  const int64_t m = A.m, n = A.n, lda = A.lda;
+  const int64_t nct = (n + kCW - 1) / kCW;
+  const int64_t U = nct * m;
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  long long ct_first = -1, ct_last = -1;
+  for (int64_t u = U0; u < U1;) {
+    const int64_t ct = u / m, r0 = u - ct * m;
+    const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
+    const int64_t c = ct * kCW + 2 * threadIdx.x;
+    const bool two = c + 1 < n, one = c < n;
+    double ax[RU], ay[RU];
+#pragma unroll
+    for (int i = 0; i < RU; ++i) ax[i] = ay[i] = 0.0;
+    const double* base = A.a + c;
+    int64_t r = r0;
+    if (two) {
+      for (; r + RU <= r1; r += RU) {
+        double2 v[RU];
+        double xr[RU];
+#pragma unroll
+        for (int i = 0; i < RU; ++i) v[i] = ld_stream2(base + (r + i) * lda);
+#pragma unroll
+        for (int i = 0; i < RU; ++i) xr[i] = xs(__ldg(x + r + i));
+#pragma unroll
+        for (int i = 0; i < RU; ++i) {
+          ax[i] = fma(v[i].x, xr[i], ax[i]);
+          ay[i] = fma(v[i].y, xr[i], ay[i]);
+        }
+      }
+      for (; r < r1; ++r) {
+        const double2 v = ld_stream2(base + r * lda);
+        const double xr = xs(__ldg(x + r));
+        ax[0] = fma(v.x, xr, ax[0]);
+        ay[0] = fma(v.y, xr, ay[0]);
+      }
+    } else if (one) {
+      for (; r < r1; ++r) ax[0] = fma(ld_stream(base + r * lda), xs(__ldg(x + r)), ax[0]);
+    }
+    const double sx = ((ax[0] + ax[1]) + (ax[2] + ax[3])) + ((ax[4] + ax[5]) + (ax[6] + ax[7]));
+    const double sy = ((ay[0] + ay[1]) + (ay[2] + ay[3])) + ((ay[4] + ay[5]) + (ay[6] + ay[7]));
+    if (r0 == 0 && r1 == m) {
+      if (one) epi.elem(c, sx, acc);
+      if (two) epi.elem(c + 1, sy, acc);
+    } else {
+      const int which = (r0 > 0) ? 0 : 1;  // 0: tile began in an earlier block
+      double* dst = wk.tpart + ((size_t)b * 2 + which) * kCW + 2 * threadIdx.x;
+      dst[0] = sx;
+      dst[1] = sy;
+      if (which == 0) ct_first = ct; else ct_last = ct;
+    }
+    u += r1 - r0;
+  }
+  // split-tile merges (whole block participates in a finalisation)
+  bool end_block = false;
+  if (ct_first >= 0 && ct_first * m + m <= U1) end_block = true;
+  for (int which = 0; which < 2; ++which) {
+    const long long ct = which == 0 ? ct_first : ct_last;
+    if (ct < 0) continue;
+    const int64_t ba = blk_of(ct * m, U, P), bb = blk_of(ct * m + m - 1, U, P);
+    __threadfence();  // every thread's tpart stores before the arrival
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned prev = atomicAdd(wk.cnt + bb, 1u);
+      sflag = (prev == (unsigned)(bb - ba));
+    }
+    __syncthreads();
+    if (sflag) {
+      __threadfence();
+      const int64_t c = ct * kCW + 2 * threadIdx.x;
+      double y0 = __ldcg(wk.tpart + ((size_t)ba * 2 + 1) * kCW + 2 * threadIdx.x);
+      double y1 = __ldcg(wk.tpart + ((size_t)ba * 2 + 1) * kCW + 2 * threadIdx.x + 1);
+      for (int64_t q = ba + 1; q <= bb; ++q) {
+        y0 += __ldcg(wk.tpart + ((size_t)q * 2) * kCW + 2 * threadIdx.x);
+        y1 += __ldcg(wk.tpart + ((size_t)q * 2) * kCW + 2 * threadIdx.x + 1);
+      }
+      double facc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) facc[k] = red_identity(epi.op(k));
+      if (c < n) epi.elem(c, y0, facc);
+      if (c + 1 < n) epi.elem(c + 1, y1, facc);
+      block_reduce<K>(facc, sm, epi);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) wk.facc[bb * kKMax + k] = facc[k];
+        wk.cnt[bb] = 0u;
+      }
+    }
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      wk.bacc[b * kKMax + k] = acc[k];
+      if (!end_block) wk.facc[b * kKMax + k] = red_identity(epi.op(k));
+    }
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
+    if (threadIdx.x == 0) epi.finish(red);
+  }
+}
+
+// ----------------------------------------------------------------- k_vec ----
+template <class Epi>
+__global__ void __launch_bounds__(kNT) k_vec(int64_t len, Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  const int64_t stride = (int64_t)gridDim.x * kNT;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < len; i += stride) epi.elem(i, acc);
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+  }
+  if (arrive_last(wk.done, gridDim.x, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, nullptr, (int)gridDim.x, red, sm, epi);
+    if (threadIdx.x == 0) epi.finish(red);
+  }
+}
+
+}  // namespace ts
