@@ -1,0 +1,430 @@
+"""Benchmark contract for the TA / CTA iteration path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c1|c3|c4|c5]
+
+Workload (default, BASELINE.json configs[1]): C2, dense rank-deficient
+5000 x 20000 fp64, A = U V^T (rank 2000), b = A x* + 1e-3 noise.  One STEP is
+one complete ``centering_solve(A, b, CenteringOptions(epsilon=1e-8))`` to the
+reference's own stopping rule (normal-equation clause, ~23 iterations), so
+``value`` = CTA iterations / s over K steps and ``time_to_tolerance_ms`` is
+the per-step solve time.
+
+* value: A resident in HBM (DeviceMatrix built before the timed region), b on
+  the device; CUDA events on the launching (default) stream around K steps,
+  barrier + synchronize on both sides, max over ranks.  A is 800 MB > L2, so
+  no L2 flush is needed between steps.
+* e2e: the same metric through the public API from pinned HOST buffers:
+  every step uploads A and b (H2D) and reads x and the trace back (D2H).
+* roofline: the dominant kernel (dense A v / A^T v pass) timed live inside
+  the timed solves by the library's per-class kernel timers (%globaltimer,
+  earliest block start to the finishing block), algorithmic bytes
+  8mn + 8(m+n) per launch, peak = MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline: the oracle port (same numpy/OpenBLAS calls as the reference)
+  on the host cores, bounded sample.
+* --impl reference: the reference's CPU algorithm (oracle port) timed for
+  K steps on the host; rank 0 only.
+
+N > 1 (torchrun): "replicas only" for this dense workload:
+each rank solves its own copy, value = all ranks' iterations / max time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TA/CTA iterations/s & time to rel. residual 1e-8; matvec-pair HBM GB/s"
+CONFIGS = {
+    "c1": dict(gen="c1", solver="cta", eps=1e-8, max_iters=10000,
+               desc="C1 dense gaussian 1000x1000, CTA eps=1e-8, cap 10000"),
+    "c2": dict(gen="c2", solver="cta", eps=1e-8, max_iters=100000,
+               desc="C2 dense rank-2000 5000x20000 (variance reading), CTA eps=1e-8"),
+    "c3": dict(gen="c3", solver="cta", eps=1e-8, max_iters=2000,
+               desc="C3 Clement variant n=100001 CSR, CTA eps=1e-8, fixed budget 2000 iterations"),
+    "c4": dict(gen="c4", solver="cta", eps=1e-8, max_iters=600,
+               desc="C4 upwind conv-diff n=1e6 CSR, CTA eps=1e-8, fixed budget 600 iterations"),
+    "c5": dict(gen="c5", solver="lp", eps=1e-6, max_iters=100000,
+               desc="C5 LP 1e4 x 1e6 CSR+CSC, TA non-negativity eps=1e-6*||b|| (stalls @11)"),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        for info in threadpool_info():
+            if info.get("user_api") == "blas":
+                return int(info.get("num_threads", os.cpu_count() or 1))
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def make_workload(cfg):
+    from paper_2304_12168_b200 import workloads as W
+
+    return W.make(cfg["gen"])
+
+
+def pass_bytes(a, trans: bool):
+    """Algorithmic bytes of one matvec pass."""
+    import scipy.sparse as sp
+
+    m, n = a.shape
+    if sp.issparse(a):
+        nnz = a.nnz
+        if trans:
+            return 12 * nnz + 4 * (n + 1) + 8 * m + 8 * n
+        return 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+    return 8 * m * n + 8 * (m + n)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(smax)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- reference ---
+def run_oracle_step(cfg, w):
+    from oracle import port
+
+    bn = float(np.linalg.norm(w.b))
+    if cfg["solver"] == "cta":
+        return port.cta_solve(w.a, w.b, epsilon=cfg["eps"], max_iters=cfg["max_iters"])
+    return port.lp_feasibility(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cfg["max_iters"])
+
+
+def reference_arm(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    w = make_workload(cfg)
+    for _ in range(args.warmup):
+        run_oracle_step(cfg, w)
+    iters = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = run_oracle_step(cfg, w)
+        iters += out["iterations"]
+    dt = time.perf_counter() - t0
+    val = iters / dt
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "iterations/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy, BASELINE.json formula)",
+        "config": {"workload": cfg["desc"], "step": "one full solve, reference stopping rule",
+                   "status": out["status"], "iterations_per_step": out["iterations"]},
+        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full solves (oracle/port.py, numpy+OpenBLAS "
+                                   f"{cores} threads; same calls as the reference)"},
+        "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- ours ---
+def solve_once(ts, cfg, dm, b, bn):
+    if cfg["solver"] == "cta":
+        return ts.centering_solve(dm, b, ts.CenteringOptions(epsilon=cfg["eps"],
+                                                             max_iters=cfg["max_iters"]))
+    return ts.nonnegative_feasibility(dm, b, eps=cfg["eps"] * bn, max_iters=cfg["max_iters"])
+
+
+def ours_arm(args, cfg):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    import paper_2304_12168_b200 as ts
+
+    w = make_workload(cfg)
+    bn = float(np.linalg.norm(w.b))
+    dm = ts.DeviceMatrix(w.a, device=dev)
+    b_dev = torch.from_numpy(w.b).to(f"cuda:{dev}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        solve_once(ts, cfg, dm, b_dev, bn)
+
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(dev) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            results.append(solve_once(ts, cfg, dm, b_dev, bn))
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = float(ev0.elapsed_time(ev1))
+    iters = sum(r.iterations for r in results)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        it = torch.tensor([float(iters)], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(it)
+        iters_all = int(it.item())
+    else:
+        iters_all = iters
+    value = iters_all / (ms / 1e3)
+
+    # live kernel accounting over the timed solves
+    kms = np.zeros(4)
+    kcnt = np.zeros(4, dtype=np.int64)
+    launches = 0
+    for r in results:
+        kms += np.array(r.kernel_ms)
+        kcnt += np.array(r.kernel_count, dtype=np.int64)
+        launches += r.kernel_launches
+    peak, peak_src = measured_peak()
+    classes = {0: ("A v", False), 1: ("A^T v", True)}
+    breakdown = {}
+    for k, (nm, trans) in classes.items():
+        if kcnt[k]:
+            avg_ms = kms[k] / kcnt[k]
+            byt = pass_bytes(w.a, trans)
+            breakdown[nm] = {"launches": int(kcnt[k]), "avg_us": avg_ms * 1e3,
+                             "bytes_per_launch": int(byt),
+                             "gbs": byt / (avg_ms * 1e-3) / 1e9,
+                             "share_of_step": float(kms[k] / ms)}
+    breakdown["vector passes"] = {"launches": int(kcnt[2]), "ms_total": float(kms[2]),
+                                  "share_of_step": float(kms[2] / ms)}
+    breakdown["scalar kernels"] = {"launches": int(kcnt[3]), "ms_total": float(kms[3]),
+                                   "share_of_step": float(kms[3] / ms)}
+    dom = max((k for k in classes if kcnt[k]), key=lambda k: kms[k])
+    dom_name = classes[dom][0]
+    achieved = breakdown[dom_name]["gbs"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}:{dom_name}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
+                "peak_source": peak_src,
+                "pair_gbs": (sum(breakdown[c[0]]["bytes_per_launch"] * breakdown[c[0]]["launches"]
+                                 for c in classes.values() if c[0] in breakdown)
+                             / (sum(kms[k] for k in classes) * 1e-3) / 1e9)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy, BASELINE.json formula; SURVEY.md Appendix A)",
+        "config": {"workload": cfg["desc"], "step": "one full solve, reference stopping rule",
+                   "status": results[-1].status, "iterations_per_step": results[-1].iterations,
+                   "time_to_tolerance_ms": float(np.median([r.device_ms for r in results])),
+                   "final_rel_residual": results[-1].residual_norm / bn,
+                   "l2": "no flush: matrix larger than L2" if cfg["gen"] in ("c2", "c4", "c5")
+                         else "L2-resident matrix (latency-bound config)",
+                   "parallelism": "single GPU" if world == 1 else f"replicas x{world}"},
+        "roofline": roofline,
+        "kernel_breakdown": breakdown,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(ts, cfg, w, bn, args, dev, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, w)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def e2e_measure(ts, cfg, w, bn, args, dev, world):
+    """Same metric through the public API with pinned HOST buffers: every
+    step uploads A and b and reads x (+ trace) back."""
+    import scipy.sparse as sp
+    import torch
+
+    def pinned_copy(arr):
+        t = torch.empty(arr.shape, dtype=torch.float64 if arr.dtype == np.float64 else torch.int32,
+                        pin_memory=True)
+        out = t.numpy()
+        out[...] = arr
+        return out, t
+
+    keep = []
+    if sp.issparse(w.a):
+        csr = w.a
+        data, t1 = pinned_copy(csr.data)
+        ind, t2 = pinned_copy(csr.indices.astype(np.int32))
+        ptr, t3 = pinned_copy(csr.indptr.astype(np.int32))
+        keep += [t1, t2, t3]
+        a_host = sp.csr_array((data, ind, ptr), shape=csr.shape)
+        a_host.indices = ind
+        a_host.indptr = ptr
+        h2d = data.nbytes + ind.nbytes + ptr.nbytes
+    else:
+        a_host, t1 = pinned_copy(w.a)
+        keep.append(t1)
+        h2d = a_host.nbytes
+    b_host, t4 = pinned_copy(w.b)
+    keep.append(t4)
+    h2d += b_host.nbytes
+    steps = max(1, min(args.steps, 10))
+
+    def step():
+        dm = ts.DeviceMatrix(a_host, device=dev)
+        r = solve_once(ts, cfg, dm, b_host, bn)
+        del dm
+        return r
+
+    step()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    iters = 0
+    rows = 0
+    for _ in range(steps):
+        r = step()
+        iters += r.iterations
+        rows += len(r.trace)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = float(ev0.elapsed_time(ev1))
+    n = w.a.shape[1]
+    return {"value": iters * world / (ms / 1e3), "unit": "iterations/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * n + 48 * rows // steps),
+            "steps": steps, "ms_per_step": ms / steps,
+            "note": "A uploaded from pinned host memory every step (DeviceMatrix), b from "
+                    "pinned host, x and trace read back"}
+
+
+def cpu_baseline(cfg, w):
+    t0 = time.perf_counter()
+    out = run_oracle_step(cfg, w)
+    dt = time.perf_counter() - t0
+    cores = blas_threads()
+    return {"value": out["iterations"] / dt, "unit": "iterations/s", "cores": cores,
+            "kind": "port",
+            "sample": f"1 full solve ({out['iterations']} iterations, {out['status']}) with "
+                      f"oracle/port.py (numpy/OpenBLAS, {cores} threads; the reference's calls)"}
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+    return ours_arm(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

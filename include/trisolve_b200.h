@@ -118,6 +118,11 @@ typedef struct {
   int32_t trivial;             /* 1: the b == 0 early return (no residual recompute) */
   double elapsed_ms;           /* device time of the solve loop (CUDA events) */
   int64_t kernel_launches;     /* kernels launched by the solve (incl. graph nodes) */
+  /* live per-class kernel accounting inside the solve (%globaltimer, earliest
+   * block start to last block's finisher): [0] A v passes, [1] A^T v passes,
+   * [2] fused vector passes, [3] small scalar kernels */
+  double kernel_ms[4];
+  int64_t kernel_count[4];
 } ts_result;
 
 typedef struct {

@@ -51,7 +51,8 @@ class Result(C.Structure):
                 ("rho", C.c_double), ("lower_bound", C.c_double), ("min_x_entry", C.c_double),
                 ("detail_value", C.c_double), ("trace_rows", C.c_int64),
                 ("has_lower_bound", C.c_int32), ("trivial", C.c_int32),
-                ("elapsed_ms", C.c_double), ("kernel_launches", C.c_int64)]
+                ("elapsed_ms", C.c_double), ("kernel_launches", C.c_int64),
+                ("kernel_ms", C.c_double * 4), ("kernel_count", C.c_int64 * 4)]
 
 
 class CtaOptions(C.Structure):

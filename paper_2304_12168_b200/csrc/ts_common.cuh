@@ -120,6 +120,25 @@ __device__ __forceinline__ void block_reduce(double (&v)[K], double* sm, const O
   }
 }
 
+// Live kernel accounting: earliest block start (atomicMin) to the finisher.
+struct KTimer {
+  unsigned long long start;
+  unsigned long long total_ns;
+  long long count;
+  long long pad;
+};
+__device__ __forceinline__ void ktimer_begin(KTimer* kt) {
+  if (kt && threadIdx.x == 0) atomicMin(&kt->start, globaltimer());
+}
+__device__ __forceinline__ void ktimer_end(KTimer* kt) {
+  if (kt) {
+    const unsigned long long now = globaltimer();
+    kt->total_ns += now - kt->start;
+    kt->count += 1;
+    kt->start = ~0ull;
+  }
+}
+
 // Per-solve reduction workspace (device pointers).
 struct Work {
   double* bacc;     // [pmax * kKMax] per-block partials

@@ -211,10 +211,14 @@ struct EpiCtaP : EpiBase {
 __global__ void k_cta_hankel(SolveState* s) {
   __shared__ int bad;
   if (!(s->status == TS_RUNNING && s->maint == MAINT_NONE)) return;
+  ktimer_begin(&s->kt[3]);
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   if (s->phi[1] == 0.0) {  // H r == 0: NormalEquationReached (centering.py:183-184)
-    if (threadIdx.x == 0) s->status = TS_NORMAL_EQ_SOLUTION;
+    if (threadIdx.x == 0) {
+      s->status = TS_NORMAL_EQ_SOLUTION;
+      ktimer_end(&s->kt[3]);
+    }
     return;
   }
   const int t = s->t;
@@ -229,6 +233,7 @@ __global__ void k_cta_hankel(SolveState* s) {
       s->status = TS_NUMERICAL_FAILURE;
       s->detail = TS_DETAIL_MOMENT_SOLVE;
     }
+    ktimer_end(&s->kt[3]);
   }
 }
 

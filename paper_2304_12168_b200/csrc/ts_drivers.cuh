@@ -3,6 +3,7 @@
 #pragma once
 
 #include <functional>
+#include <type_traits>
 
 namespace ts {
 
@@ -64,6 +65,7 @@ struct SolveCtx {
     ucap = trace ? trace_cap : 0;
     init_state.trace = dtrace;
     init_state.seg_cap = seg_cap;
+    for (int i = 0; i < 4; ++i) init_state.kt[i] = KTimer{~0ull, 0ull, 0, 0};
     *hs = init_state;
     TS_CUDA(cudaMemcpyAsync(ds, hs, sizeof(SolveState), cudaMemcpyHostToDevice, st));
     TS_CUDA(cudaEventCreate(&ev0));
@@ -166,12 +168,24 @@ template <class Epi>
 static int pass(const Mat& M, int trans, const double* x, XS xs, const Epi& e, const Work& w,
                 cudaStream_t s) {
   ++g_launches;
-  return launch_pass(M, trans, x, xs, e, w, s);
+  if constexpr (std::is_base_of<EpiBase, Epi>::value) {
+    Epi e2 = e;
+    e2.tclass = trans ? 1 : 0;
+    return launch_pass(M, trans, x, xs, e2, w, s);
+  } else {
+    return launch_pass(M, trans, x, xs, e, w, s);
+  }
 }
 template <class Epi>
 static int vecpass(const Mat& M, int64_t len, const Epi& e, const Work& w, cudaStream_t s) {
   ++g_launches;
-  return launch_vec(len, M.sms, e, w, s);
+  if constexpr (std::is_base_of<EpiBase, Epi>::value) {
+    Epi e2 = e;
+    e2.tclass = 2;
+    return launch_vec(len, M.sms, e2, w, s);
+  } else {
+    return launch_vec(len, M.sms, e, w, s);
+  }
 }
 
 static void fill_result(const SolveState& s, ts_result* r) {
@@ -187,6 +201,10 @@ static void fill_result(const SolveState& s, ts_result* r) {
   r->detail_value = s.detail_value;
   r->trace_rows = s.trace_count;
   r->trivial = s.trivial;
+  for (int i = 0; i < 4; ++i) {
+    r->kernel_ms[i] = s.kt[i].total_ns * 1e-6;
+    r->kernel_count[i] = s.kt[i].count;
+  }
 }
 
 // ================================================================== TA ====
@@ -241,13 +259,15 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
   // operator products with fused epilogue: y = Op v  (Op = A, or A^T A)
   auto op_apply = [&](cudaStream_t s, const double* v, XS xs, auto epi, int pred) -> int {
     if (!a.gram) return pass(M, 0, v, xs, epi, wk, s);
-    EpiStore es{t1, nullptr, ds, pred};
+    EpiStore es;
+    es.st = ds; es.y = t1; es.pred = pred;
     TS_CHECK(pass(M, 0, v, xs, es, wk, s));
     return pass(M, 1, t1, XS{}, epi, wk, s);
   };
   auto op_apply_t = [&](cudaStream_t s, const double* v, auto epi, int pred) -> int {
     if (!a.gram) return pass(M, 1, v, XS{}, epi, wk, s);
-    EpiStore es{t1, nullptr, ds, pred};
+    EpiStore es;
+    es.st = ds; es.y = t1; es.pred = pred;
     TS_CHECK(pass(M, 0, v, XS{}, es, wk, s));
     return pass(M, 1, t1, XS{}, epi, wk, s);
   };
@@ -473,7 +493,8 @@ int ts_matvec(const ts_matrix* A, const double* x, double* y, void* stream) {
     double *dx, *dy;
     TS_CHECK(stage_in(ar, x, A->n, &dx));
     TS_CHECK(ar.get(&dy, A->m));
-    EpiStore e{dy, nullptr};
+    EpiStore e;
+    e.y = dy;
     TS_CHECK(pass(*A, 0, dx, XS{}, e, wk, st));
     TS_CUDA(cudaMemcpyAsync(y, dy, A->m * sizeof(double), cudaMemcpyDefault, st));
   }
@@ -492,7 +513,8 @@ int ts_rmatvec(const ts_matrix* A, const double* x, double* y, void* stream) {
     double *dx, *dy;
     TS_CHECK(stage_in(ar, x, A->m, &dx));
     TS_CHECK(ar.get(&dy, A->n));
-    EpiStore e{dy, nullptr};
+    EpiStore e;
+    e.y = dy;
     TS_CHECK(pass(*A, 1, dx, XS{}, e, wk, st));
     TS_CUDA(cudaMemcpyAsync(y, dy, A->n * sizeof(double), cudaMemcpyDefault, st));
   }
@@ -512,9 +534,11 @@ int ts_gram_matvec(const ts_matrix* A, const double* x, double* y, void* stream)
     TS_CHECK(stage_in(ar, x, A->n, &dx));
     TS_CHECK(ar.get(&dt, A->m));
     TS_CHECK(ar.get(&dy, A->n));
-    EpiStore e1{dt, nullptr};
+    EpiStore e1;
+    e1.y = dt;
     TS_CHECK(pass(*A, 0, dx, XS{}, e1, wk, st));
-    EpiStore e2{dy, nullptr};
+    EpiStore e2;
+    e2.y = dy;
     TS_CHECK(pass(*A, 1, dt, XS{}, e2, wk, st));
     TS_CUDA(cudaMemcpyAsync(y, dy, A->n * sizeof(double), cudaMemcpyDefault, st));
   }

@@ -175,6 +175,7 @@ struct EpiFroDense {
   __device__ int op(int) const { return RED_SUM; }
   __device__ bool active() const { return true; }
   __device__ void idle() const {}
+  __device__ KTimer* timer() const { return nullptr; }
   __device__ void elem(int64_t i, double (&acc)[K]) const {
     const double v = a[(i / n) * lda + (i % n)];
     acc[0] = fma(v, v, acc[0]);
@@ -188,6 +189,7 @@ struct EpiFroVals {
   __device__ int op(int) const { return RED_SUM; }
   __device__ bool active() const { return true; }
   __device__ void idle() const {}
+  __device__ KTimer* timer() const { return nullptr; }
   __device__ void elem(int64_t i, double (&acc)[K]) const { acc[0] = fma(v[i], v[i], acc[0]); }
   __device__ void finish(double (&r)[K]) const { *out = sqrt(r[0]); }
 };
@@ -199,6 +201,7 @@ struct EpiIdxRange {
   __device__ int op(int k) const { return RED_MIN; }
   __device__ bool active() const { return true; }
   __device__ void idle() const {}
+  __device__ KTimer* timer() const { return nullptr; }
   __device__ void elem(int64_t i, double (&acc)[K]) const {
     const double v = (double)ci[i];
     acc[0] = py_min(acc[0], v);

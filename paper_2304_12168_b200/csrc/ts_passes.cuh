@@ -27,6 +27,7 @@
 //   __device__ void elem(int64 i, double (&acc)[K]) const;             k_vec
 //   __device__ void finish(double (&red)[K]) const;  thread 0, last block
 //   __device__ void idle() const;           block 0 / thread 0 when inactive
+//   __device__ KTimer* timer() const;       live accounting slot or nullptr
 #pragma once
 
 #include "ts_common.cuh"
@@ -164,6 +165,8 @@ __global__ void __launch_bounds__(kNT) k_rows_flat(Acc A, const double* __restri
     return;
   }
   xs.load();
+  KTimer* kt = epi.timer();
+  ktimer_begin(kt);
   const int64_t P = gridDim.x, b = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t E = A.total();
@@ -281,7 +284,10 @@ __global__ void __launch_bounds__(kNT) k_rows_flat(Acc A, const double* __restri
   if (arrive_last(wk.done, (unsigned)P, &sflag)) {
     double red[K];
     reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
-    if (threadIdx.x == 0) epi.finish(red);
+    if (threadIdx.x == 0) {
+      ktimer_end(kt);
+      epi.finish(red);
+    }
   }
 }
 
@@ -297,6 +303,8 @@ __global__ void __launch_bounds__(kNT) k_rows_short(Acc A, const double* __restr
     return;
   }
   xs.load();
+  KTimer* kt = epi.timer();
+  ktimer_begin(kt);
   const int64_t P = gridDim.x, b = blockIdx.x, m = A.rows();
   const int64_t R0 = m * b / P, R1 = m * (b + 1) / P;
   double acc[K];
@@ -311,7 +319,10 @@ __global__ void __launch_bounds__(kNT) k_rows_short(Acc A, const double* __restr
   if (arrive_last(wk.done, (unsigned)P, &sflag)) {
     double red[K];
     reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, epi);
-    if (threadIdx.x == 0) epi.finish(red);
+    if (threadIdx.x == 0) {
+      ktimer_end(kt);
+      epi.finish(red);
+    }
   }
 }
 
@@ -328,6 +339,8 @@ __global__ void __launch_bounds__(kNT) k_cols_tile(DenseRows A, const double* __
     return;
   }
   xs.load();
+  KTimer* kt = epi.timer();
+  ktimer_begin(kt);
   const int64_t m = A.m, n = A.n, lda = A.lda;
   const int64_t nct = (n + kCW - 1) / kCW;
   const int64_t U = nct * m;
@@ -432,7 +445,10 @@ __global__ void __launch_bounds__(kNT) k_cols_tile(DenseRows A, const double* __
   if (arrive_last(wk.done, (unsigned)P, &sflag)) {
     double red[K];
     reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
-    if (threadIdx.x == 0) epi.finish(red);
+    if (threadIdx.x == 0) {
+      ktimer_end(kt);
+      epi.finish(red);
+    }
   }
 }
 
@@ -446,6 +462,8 @@ __global__ void __launch_bounds__(kNT) k_vec(int64_t len, Epi epi, Work wk) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
+  KTimer* kt = epi.timer();
+  ktimer_begin(kt);
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
@@ -459,7 +477,10 @@ __global__ void __launch_bounds__(kNT) k_vec(int64_t len, Epi epi, Work wk) {
   if (arrive_last(wk.done, gridDim.x, &sflag)) {
     double red[K];
     reduce_partials<K>(wk.bacc, nullptr, (int)gridDim.x, red, sm, epi);
-    if (threadIdx.x == 0) epi.finish(red);
+    if (threadIdx.x == 0) {
+      ktimer_end(kt);
+      epi.finish(red);
+    }
   }
 }
 

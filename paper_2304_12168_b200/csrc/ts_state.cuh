@@ -47,6 +47,7 @@ struct alignas(16) SolveState {
   // final report
   double residual_norm, normal_residual_norm;
   ts_trace_row* trace;  // device ring of seg_cap rows
+  KTimer kt[4];         // [0] A v, [1] A^T v, [2] vector passes, [3] scalar kernels
 };
 
 __device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, int use, const SolveState* s) {
@@ -192,10 +193,14 @@ __device__ inline void ta_decide(SolveState* s, double c2, double cp2) {
 
 // ------------------------------------------------------------ epilogues ----
 struct EpiBase {
-  SolveState* st;
-  cudaGraphConditionalHandle cond;
-  int use_cond;
+  SolveState* st = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+  int use_cond = 0;
+  int tclass = -1;  // live accounting class (set by the launch helper)
   __device__ __forceinline__ int op(int) const { return RED_SUM; }
+  __device__ __forceinline__ KTimer* timer() const {
+    return (st && tclass >= 0) ? &st->kt[tclass] : nullptr;
+  }
   __device__ __forceinline__ void idle() const {
     if (use_cond) {
       st->body_runs += 1;
@@ -413,13 +418,11 @@ struct EpiFinalNR : EpiBase {
 
 // plain y = M v with an optional sum of squares into a scalar slot.
 // pred: 0 always; 1 while running (TA c pass); 2 on pivot iterations.
-struct EpiStore {
+struct EpiStore : EpiBase {
   static constexpr int K = 1;
-  double* y;
-  double* sq;  // optional: ||y||^2
-  const SolveState* st = nullptr;
+  double* y = nullptr;
+  double* sq = nullptr;  // optional: ||y||^2
   int pred = 0;
-  __device__ int op(int) const { return RED_SUM; }
   __device__ bool active() const {
     if (pred == 0) return true;
     if (pred == 1) return running(st);
@@ -443,6 +446,7 @@ struct EpiDot {
   __device__ int op(int) const { return RED_SUM; }
   __device__ bool active() const { return true; }
   __device__ void idle() const {}
+  __device__ KTimer* timer() const { return nullptr; }
   __device__ void elem(int64_t i, double (&acc)[K]) const { acc[0] = fma(u[i], v[i], acc[0]); }
   __device__ void finish(double (&r)[K]) const { *out = sqrt_out ? sqrt(r[0]) : r[0]; }
 };

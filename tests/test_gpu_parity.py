@@ -56,24 +56,29 @@ def test_golden_parity(name):
         pytest.skip("enhanced probe not implemented on the device path yet")
     res = run_device(g)
     assert res.status == g.status, (res, g.status, g.detail, res.detail)
+    bn = float(np.linalg.norm(g.b))
+    # final relative residual within a factor of 2 (north_star), floor at the
+    # cancellation level of b - A x
+    floor = 1e-11 * bn
+    assert (0.5 * g.residual_norm - floor <= res.residual_norm <= 2.0 * g.residual_norm + floor), (
+        res.residual_norm, g.residual_norm)
+    if name in CHAOTIC:
+        # iteration count to tolerance within +-1% (north_star), at least +-2
+        band = max(2, int(np.ceil(0.01 * g.iterations)))
+        assert abs(res.iterations - g.iterations) <= band, (res.iterations, g.iterations)
+        return
     assert res.iterations == g.iterations
     tr = trace_rows_numeric(res.trace.rows, res.trace.columns)
     assert tr.shape == g.trace.shape
     if "event" in g.trace_columns:
-        ev = g.trace_columns.index("event") - 0
+        ev = g.trace_columns.index("event")
         assert np.array_equal(tr[:, ev], g.trace[:, ev])
-    bn = float(np.linalg.norm(g.b))
-    if name in CHAOTIC:
-        rr, gr = res.residual_norm / bn, g.residual_norm / bn
-        assert 0.5 * gr <= rr <= 2.0 * gr, (rr, gr)
-        return
     assert res.detail == g.detail
     tol = LOOSE_X.get(name, 1e-9)
     assert rel_l2(res.x, g.x) <= tol, rel_l2(res.x, g.x)
-    scale = np.maximum(np.abs(g.trace), 1e-300)
-    assert np.all(np.abs(tr - g.trace) <= tol * np.maximum(scale, np.abs(g.trace).max(axis=0)))
-    absr = 1e-12 * max(bn, 1.0)
-    assert res.residual_norm == pytest.approx(g.residual_norm, rel=max(tol, 1e-9) * 10, abs=absr)
+    if g.trace.size:
+        colmax = np.abs(g.trace).max(axis=0)
+        assert np.all(np.abs(tr - g.trace) <= tol * np.maximum(np.abs(g.trace), colmax))
     for key, val in g.extras.items():
         got = getattr(res, key)
         if isinstance(val, np.ndarray):
@@ -115,4 +120,14 @@ def test_moment_kats():
     for phi, (t, order), alpha in zip(z["phi"], z["orders"], z["alpha"]):
         mom = Moments(int(t), phi[: 2 * t], [], None)
         got = min_norm_coefficients(mom, int(order))
-        np.testing.assert_allclose(got, alpha[:order], rtol=1e-9, atol=1e-12)
+        # both sides are backward-stable SVD solves (LAPACK gelsd vs device Jacobi):
+        # agreement is bounded by eps * cond of the equilibrated Hankel system
+        idx = np.add.outer(np.arange(order), np.arange(order)) + 1
+        hk = phi[idx]
+        s = np.sqrt(np.abs(np.diag(hk)))
+        s[s == 0] = 1.0
+        sv = np.linalg.svd(hk / np.outer(s, s), compute_uv=False)
+        kept = sv[sv > 1e-13 * sv[0]] if sv[0] > 0 else sv[:1]
+        cond = sv[0] / kept[-1] if kept.size and kept[-1] > 0 else 1.0
+        rtol = max(1e-10, 50 * 2.2e-16 * cond)
+        np.testing.assert_allclose(got, alpha[:order], rtol=rtol, atol=1e-12 * np.abs(alpha).max())
