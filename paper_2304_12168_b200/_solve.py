@@ -86,6 +86,8 @@ def build_result(kind, res: N.Result, x, trace: Trace, **extra) -> SolveResult:
     )
     out.device_ms = float(res.elapsed_ms)
     out.kernel_launches = int(res.kernel_launches)
+    out.kernel_ms = tuple(float(v) for v in res.kernel_ms)
+    out.kernel_count = tuple(int(v) for v in res.kernel_count)
     return out
 
 

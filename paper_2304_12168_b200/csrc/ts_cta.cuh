@@ -14,72 +14,73 @@ namespace ts {
 // <= rcond * s_max dropped.  The balanced matrix is exactly symmetric, so its
 // SVD is |eigen-decomposition|: cyclic Jacobi in fp64 gives the eigenpairs.
 // Returns false on non-finite input (numpy raises LinAlgError there).
-__device__ inline bool hankel_min_norm(const double* phi, int order, double rcond, double* alpha) {
-  double B[kTMax][kTMax], V[kTMax][kTMax], s[kTMax], c[kTMax];
+// `w` is per-thread scratch of 2 * kTMax * kTMax doubles (shared memory).
+__device__ inline bool hankel_min_norm(const double* phi, int order, double rcond, double* alpha,
+                                       double* w) {
+  double* B = w;                    // B[i * kTMax + j]
+  double* V = w + kTMax * kTMax;    // V[i * kTMax + j]
+  double s[kTMax], c[kTMax];
   const int t = order;
   for (int i = 0; i < t; ++i) {
-    const double d = fabs(phi[2 * i + 1]);
-    s[i] = sqrt(d);
+    s[i] = sqrt(fabs(phi[2 * i + 1]));
     if (s[i] == 0.0) s[i] = 1.0;
   }
   bool finite = true;
   for (int i = 0; i < t; ++i) {
     for (int j = 0; j < t; ++j) {
-      B[i][j] = phi[i + j + 1] / (s[i] * s[j]);
-      V[i][j] = (i == j) ? 1.0 : 0.0;
-      finite = finite && isfinite(B[i][j]);
+      const double v = phi[i + j + 1] / (s[i] * s[j]);  // hankel / outer(s, s)
+      B[i * kTMax + j] = v;
+      V[i * kTMax + j] = (i == j) ? 1.0 : 0.0;
+      finite = finite && isfinite(v);
     }
     c[i] = phi[i] / s[i];
     finite = finite && isfinite(c[i]);
   }
   if (!finite) return false;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int i = 0; i < t; ++i)
-      for (int j = 0; j < t; ++j) {
-        const double v = B[i][j] * B[i][j];
-        tot += v;
-        if (i != j) off += v;
-      }
-    if (off <= 1e-34 * tot || off == 0.0) break;
+  // cyclic Jacobi: rotate while some |b_pq| exceeds eps * sqrt|b_pp b_qq|
+  for (int sweep = 0; sweep < 32; ++sweep) {
+    bool rotated = false;
     for (int p = 0; p < t - 1; ++p) {
       for (int q = p + 1; q < t; ++q) {
-        const double apq = B[p][q];
-        if (apq == 0.0) continue;
-        const double tau = (B[q][q] - B[p][p]) / (2.0 * apq);
+        const double apq = B[p * kTMax + q];
+        const double app = B[p * kTMax + p], aqq = B[q * kTMax + q];
+        if (apq == 0.0 || fabs(apq) <= 1e-16 * sqrt(fabs(app * aqq))) continue;
+        rotated = true;
+        const double tau = (aqq - app) / (2.0 * apq);
         const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
         const double cs = 1.0 / sqrt(1.0 + tt * tt);
         const double sn = tt * cs;
         for (int k = 0; k < t; ++k) {  // B <- B J
-          const double bkp = B[k][p], bkq = B[k][q];
-          B[k][p] = cs * bkp - sn * bkq;
-          B[k][q] = sn * bkp + cs * bkq;
+          const double bkp = B[k * kTMax + p], bkq = B[k * kTMax + q];
+          B[k * kTMax + p] = cs * bkp - sn * bkq;
+          B[k * kTMax + q] = sn * bkp + cs * bkq;
         }
         for (int k = 0; k < t; ++k) {  // B <- J^T B
-          const double bpk = B[p][k], bqk = B[q][k];
-          B[p][k] = cs * bpk - sn * bqk;
-          B[q][k] = sn * bpk + cs * bqk;
+          const double bpk = B[p * kTMax + k], bqk = B[q * kTMax + k];
+          B[p * kTMax + k] = cs * bpk - sn * bqk;
+          B[q * kTMax + k] = sn * bpk + cs * bqk;
         }
         for (int k = 0; k < t; ++k) {  // V <- V J
-          const double vkp = V[k][p], vkq = V[k][q];
-          V[k][p] = cs * vkp - sn * vkq;
-          V[k][q] = sn * vkp + cs * vkq;
+          const double vkp = V[k * kTMax + p], vkq = V[k * kTMax + q];
+          V[k * kTMax + p] = cs * vkp - sn * vkq;
+          V[k * kTMax + q] = sn * vkp + cs * vkq;
         }
       }
     }
+    if (!rotated) break;
   }
   double smax = 0.0;
-  for (int k = 0; k < t; ++k) smax = fmax(smax, fabs(B[k][k]));
-  const double cut = rcond * smax;
+  for (int k = 0; k < t; ++k) smax = fmax(smax, fabs(B[k * kTMax + k]));
+  const double cut = rcond * smax;  // gelsd: s_i <= rcond * s_max treated as zero
   double beta[kTMax];
   for (int i = 0; i < t; ++i) beta[i] = 0.0;
   for (int k = 0; k < t; ++k) {
-    const double lam = B[k][k];
+    const double lam = B[k * kTMax + k];
     if (!(fabs(lam) > cut)) continue;
     double proj = 0.0;
-    for (int i = 0; i < t; ++i) proj += V[i][k] * c[i];
-    const double w = proj / lam;
-    for (int i = 0; i < t; ++i) beta[i] += w * V[i][k];
+    for (int i = 0; i < t; ++i) proj += V[i * kTMax + k] * c[i];
+    const double wk = proj / lam;
+    for (int i = 0; i < t; ++i) beta[i] += wk * V[i * kTMax + k];
   }
   bool ok = true;
   for (int i = 0; i < t; ++i) {
@@ -210,6 +211,7 @@ struct EpiCtaP : EpiBase {
 // candidate pass then applies the reference's t..1 retry rule)
 __global__ void k_cta_hankel(SolveState* s) {
   __shared__ int bad;
+  __shared__ double scratch[kTMax][2 * kTMax * kTMax];
   if (!(s->status == TS_RUNNING && s->maint == MAINT_NONE)) return;
   ktimer_begin(&s->kt[3]);
   if (threadIdx.x == 0) bad = 0;
@@ -224,7 +226,7 @@ __global__ void k_cta_hankel(SolveState* s) {
   const int t = s->t;
   const int o = threadIdx.x + 1;
   if (o <= t) {
-    if (!hankel_min_norm(s->phi, o, s->rcond, s->alpha_o[o - 1])) atomicExch(&bad, 1);
+    if (!hankel_min_norm(s->phi, o, s->rcond, s->alpha_o[o - 1], scratch[o - 1])) atomicExch(&bad, 1);
   }
   __syncthreads();
   if (threadIdx.x == 0) {

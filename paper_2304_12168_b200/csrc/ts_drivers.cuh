@@ -469,7 +469,9 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
 }
 
 __global__ void k_hankel_one(const double* phi, int order, double rcond, double* alpha, int* ok) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *ok = hankel_min_norm(phi, order, rcond, alpha) ? 1 : 0;
+  __shared__ double scratch[2 * kTMax * kTMax];
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    *ok = hankel_min_norm(phi, order, rcond, alpha, scratch) ? 1 : 0;
 }
 
 }  // namespace ts
