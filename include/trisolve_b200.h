@@ -209,6 +209,11 @@ TS_API int ts_cta_step(const ts_matrix* a, int32_t h_mode, const double* x, cons
                 double rcond, double* x_out, double* r_out, int32_t* order_out,
                 double* atr_norm_out, int32_t* status_out, void* stream);
 
+/* Events-timed back-to-back launches of one matvec pass (A v or A^T v) on
+ * device-resident vectors: average milliseconds per launch (kernel tuning and
+ * the bench's cross-check of the in-solve kernel timers). */
+TS_API int ts_time_pass(const ts_matrix* a, int32_t trans, int32_t reps, double* avg_ms, void* stream);
+
 /* ---- solvers --------------------------------------------------------------- */
 TS_API int ts_cta_solve(const ts_matrix* a, const double* b, const ts_cta_options* opts, double* x_out,
                  ts_trace_row* trace, int64_t trace_cap, ts_result* res, void* stream);

@@ -20,7 +20,7 @@ EXPORTS = (
     "ts_abi_version", "ts_last_error", "ts_device_count",
     "ts_matrix_create_dense", "ts_matrix_create_csr", "ts_matrix_destroy", "ts_matrix_info",
     "ts_matvec", "ts_rmatvec", "ts_gram_matvec", "ts_norm2", "ts_dot",
-    "ts_moments", "ts_hankel_min_norm", "ts_cta_step",
+    "ts_moments", "ts_hankel_min_norm", "ts_cta_step", "ts_time_pass",
     "ts_cta_solve", "ts_ta_adaptive", "ts_ta_in_ball", "ts_lp_feasibility",
 )
 
@@ -109,6 +109,7 @@ def _declare(lib):
         "ts_hankel_min_norm": ([_P, _I32, _I32, _D, _P, _P], C.c_int),
         "ts_cta_step": ([_P, _I32, _P, _P, _I32, _D, _P, _P, C.POINTER(_I32), C.POINTER(_D),
                          C.POINTER(_I32), _P], C.c_int),
+        "ts_time_pass": ([_P, _I32, _I32, C.POINTER(_D), _P], C.c_int),
         "ts_cta_solve": ([_P, _P, C.POINTER(CtaOptions), _P, _P, _I64, C.POINTER(Result), _P],
                          C.c_int),
         "ts_ta_adaptive": ([_P, _P, C.POINTER(TaOptions), _P, _P, _I64, C.POINTER(Result), _P],

@@ -53,6 +53,7 @@ struct Err {
 
 // ------------------------------------------------------------- constants ----
 constexpr int kNT = 256;          // threads per block for every pass kernel
+constexpr int kMinBlocks = 4;     // __launch_bounds__ min blocks/SM (<= 64 registers)
 constexpr int kWarps = kNT / 32;  // warps per block
 constexpr int kKMax = 8;          // max reduction slots per pass
 constexpr int kCW = 2 * kNT;      // dense A^T tile width (columns): 2 per thread

@@ -55,7 +55,7 @@ struct SolveCtx {
       return TS_ENOMEM;
     }
     hflushed = reinterpret_cast<long long*>(reinterpret_cast<char*>(hs) + sizeof(SolveState));
-    TS_CHECK(make_work(ar, resident_blocks(M.sms), &wk));
+    TS_CHECK(make_work(ar, work_blocks(M.sms), &wk));
     TS_CHECK(ar.get(&ds, 1));
     long long want = max_iters + 2;
     if (want < 16) want = 16;
@@ -491,7 +491,7 @@ int ts_matvec(const ts_matrix* A, const double* x, double* y, void* stream) {
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, resident_blocks(A->sms), &wk));
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk));
     double *dx, *dy;
     TS_CHECK(stage_in(ar, x, A->n, &dx));
     TS_CHECK(ar.get(&dy, A->m));
@@ -511,7 +511,7 @@ int ts_rmatvec(const ts_matrix* A, const double* x, double* y, void* stream) {
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, resident_blocks(A->sms), &wk));
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk));
     double *dx, *dy;
     TS_CHECK(stage_in(ar, x, A->m, &dx));
     TS_CHECK(ar.get(&dy, A->n));
@@ -531,7 +531,7 @@ int ts_gram_matvec(const ts_matrix* A, const double* x, double* y, void* stream)
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, resident_blocks(A->sms), &wk));
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk));
     double *dx, *dt, *dy;
     TS_CHECK(stage_in(ar, x, A->n, &dx));
     TS_CHECK(ar.get(&dt, A->m));
@@ -558,7 +558,7 @@ static int dot_impl(const double* u, const double* v, int64_t len, double* out, 
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, resident_blocks(dummy.sms), &wk));
+    TS_CHECK(make_work(ar, work_blocks(dummy.sms), &wk));
     double *du, *dv, *dout;
     TS_CHECK(stage_in(ar, u, (size_t)len, &du));
     dv = du;
@@ -693,6 +693,39 @@ int ts_cta_step(const ts_matrix* A, int32_t h_mode, const double* x, const doubl
     }
     TS_CUDA(cudaStreamSynchronize(st));
   }
+  return 0;
+}
+
+int ts_time_pass(const ts_matrix* A, int32_t trans, int32_t reps, double* avg_ms, void* stream) {
+  TS_CHECK_HANDLE(A);
+  if (reps < 1) TS_INVAL("reps must be positive");
+  DeviceGuard g(A->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  float ms = 0.f;
+  {
+    Arena ar(st);
+    Work wk;
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk));
+    double *dx, *dy;
+    const int64_t nin = trans ? A->m : A->n, nout = trans ? A->n : A->m;
+    TS_CHECK(ar.get(&dx, nin));
+    TS_CHECK(ar.get(&dy, nout));
+    TS_CUDA(cudaMemsetAsync(dx, 0, nin * sizeof(double), st));
+    EpiStore e;
+    e.y = dy;
+    TS_CHECK(pass(*A, trans, dx, XS{}, e, wk, st));  // warm-up
+    cudaEvent_t e0, e1;
+    TS_CUDA(cudaEventCreate(&e0));
+    TS_CUDA(cudaEventCreate(&e1));
+    TS_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < reps; ++i) TS_CHECK(pass(*A, trans, dx, XS{}, e, wk, st));
+    TS_CUDA(cudaEventRecord(e1, st));
+    TS_CUDA(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  *avg_ms = ms / reps;
   return 0;
 }
 

@@ -286,7 +286,7 @@ int ts_matrix_info(const ts_matrix* A, int64_t* m, int64_t* n, int64_t* nnz, int
 static int finish_create(ts_matrix* A, cudaStream_t st, Arena& ar) {
   // Frobenius norm once (linalg.py:64-69); cached on the immutable handle
   Work wk;
-  TS_CHECK(make_work(ar, resident_blocks(A->sms), &wk));
+  TS_CHECK(make_work(ar, work_blocks(A->sms), &wk));
   double* dfro;
   TS_CHECK(ar.get(&dfro, 1));
   if (A->kind == 0) {
@@ -405,7 +405,7 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
     if (nnz > 0) {
       // validate column indices on the device
       Work wk;
-      if ((rc = make_work(ar, resident_blocks(A->sms), &wk))) return fail(rc);
+      if ((rc = make_work(ar, work_blocks(A->sms), &wk))) return fail(rc);
       double* rng;
       if ((rc = ar.get(&rng, 2))) return fail(rc);
       EpiIdxRange er{A->ci, rng};

@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cstdlib>
 
 #include "ts_passes.cuh"
 
@@ -48,7 +49,18 @@ struct Mat {
   CsrRows csrT() const { return CsrRows{rpT, ciT, valT, n, nnz}; }
 };
 
-inline int resident_blocks(int sms) { return sms * (2048 / kNT); }
+// one full wave of pass blocks (occupancy is register-bound at kMinBlocks per
+// SM); TS_BLOCKS_PER_SM overrides for experiments
+inline int blocks_per_sm() {
+  static int v = [] {
+    const char* e = getenv("TS_BLOCKS_PER_SM");
+    int b = e ? atoi(e) : kMinBlocks;
+    return (b > 0 && b <= 8) ? b : kMinBlocks;
+  }();
+  return v;
+}
+inline int resident_blocks(int sms) { return sms * blocks_per_sm(); }
+inline int work_blocks(int sms) { return sms * 8; }  // workspace sizing upper bound
 
 // first row touched by the warp whose range starts at s (see k_rows_flat)
 inline int64_t first_row_at(const int* rp, int64_t rows, int64_t s) {

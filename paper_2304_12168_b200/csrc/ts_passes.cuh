@@ -81,15 +81,19 @@ struct DenseRows {
     const double* xp = x + c;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int64_t p = lane;
-    for (; p + 96 < npair; p += 128) {
-      double2 v0 = ld_stream2(rp + 2 * p), v1 = ld_stream2(rp + 2 * (p + 32));
-      double2 v2 = ld_stream2(rp + 2 * (p + 64)), v3 = ld_stream2(rp + 2 * (p + 96));
-      double2 x0 = ldg2(xp + 2 * p), x1 = ldg2(xp + 2 * (p + 32));
-      double2 x2 = ldg2(xp + 2 * (p + 64)), x3 = ldg2(xp + 2 * (p + 96));
-      a0 = fma(v0.x, xs(x0.x), a0); a0 = fma(v0.y, xs(x0.y), a0);
-      a1 = fma(v1.x, xs(x1.x), a1); a1 = fma(v1.y, xs(x1.y), a1);
-      a2 = fma(v2.x, xs(x2.x), a2); a2 = fma(v2.y, xs(x2.y), a2);
-      a3 = fma(v3.x, xs(x3.x), a3); a3 = fma(v3.y, xs(x3.y), a3);
+    for (; p + 224 < npair; p += 256) {
+      double2 v[8], xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ld_stream2(rp + 2 * (p + 32 * u));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = ldg2(xp + 2 * (p + 32 * u));
+#pragma unroll
+      for (int u = 0; u < 8; u += 4) {
+        a0 = fma(v[u].x, xs(xv[u].x), a0); a0 = fma(v[u].y, xs(xv[u].y), a0);
+        a1 = fma(v[u + 1].x, xs(xv[u + 1].x), a1); a1 = fma(v[u + 1].y, xs(xv[u + 1].y), a1);
+        a2 = fma(v[u + 2].x, xs(xv[u + 2].x), a2); a2 = fma(v[u + 2].y, xs(xv[u + 2].y), a2);
+        a3 = fma(v[u + 3].x, xs(xv[u + 3].x), a3); a3 = fma(v[u + 3].y, xs(xv[u + 3].y), a3);
+      }
     }
     for (; p < npair; p += 32) {
       double2 v0 = ld_stream2(rp + 2 * p);
@@ -150,7 +154,7 @@ __device__ __forceinline__ int64_t blk_of(int64_t p, int64_t E, int64_t P) {
 
 // ----------------------------------------------------------- k_rows_flat ----
 template <class Acc, class Epi>
-__global__ void __launch_bounds__(kNT) k_rows_flat(Acc A, const double* __restrict__ x, XS xs,
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_flat(Acc A, const double* __restrict__ x, XS xs,
                                                    Epi epi, Work wk,
                                                    const int* __restrict__ wrow) {
   constexpr int K = Epi::K;
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(kNT) k_rows_flat(Acc A, const double* __restri
 
 // ---------------------------------------------------------- k_rows_short ----
 template <class Acc, class Epi>
-__global__ void __launch_bounds__(kNT) k_rows_short(Acc A, const double* __restrict__ x, XS xs,
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const double* __restrict__ x, XS xs,
                                                     Epi epi, Work wk) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(kNT) k_rows_short(Acc A, const double* __restr
 
 // ----------------------------------------------------------- k_cols_tile ----
 template <class Epi>
-__global__ void __launch_bounds__(kNT) k_cols_tile(DenseRows A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, const double* __restrict__ x,
                                                    XS xs, Epi epi, Work wk) {
   constexpr int K = Epi::K;
   constexpr int RU = 8;  // rows in flight per thread
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(kNT) k_cols_tile(DenseRows A, const double* __
 
 // ----------------------------------------------------------------- k_vec ----
 template <class Epi>
-__global__ void __launch_bounds__(kNT) k_vec(int64_t len, Epi epi, Work wk) {
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_vec(int64_t len, Epi epi, Work wk) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
