@@ -14,80 +14,107 @@ namespace ts {
 // <= rcond * s_max dropped.  The balanced matrix is exactly symmetric, so its
 // SVD is |eigen-decomposition|: cyclic Jacobi in fp64 gives the eigenpairs.
 // Returns false on non-finite input (numpy raises LinAlgError there).
-// `w` is per-thread scratch of 2 * kTMax * kTMax doubles (shared memory).
-__device__ inline bool hankel_min_norm(const double* phi, int order, double rcond, double* alpha,
-                                       double* w) {
-  double* B = w;                    // B[i * kTMax + j]
-  double* V = w + kTMax * kTMax;    // V[i * kTMax + j]
-  double s[kTMax], c[kTMax];
-  const int t = order;
-  for (int i = 0; i < t; ++i) {
+// Register-resident version: every index is a compile-time constant after
+// unrolling, so B, V stay in registers (T <= kTMax).
+template <int T>
+__device__ __forceinline__ bool hankel_T(const double* phi, double rcond, double* alpha) {
+  double B[T][T], V[T][T], s[T], c[T];
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
     s[i] = sqrt(fabs(phi[2 * i + 1]));
     if (s[i] == 0.0) s[i] = 1.0;
   }
-  bool finite = true;
-  for (int i = 0; i < t; ++i) {
-    for (int j = 0; j < t; ++j) {
-      const double v = phi[i + j + 1] / (s[i] * s[j]);  // hankel / outer(s, s)
-      B[i * kTMax + j] = v;
-      V[i * kTMax + j] = (i == j) ? 1.0 : 0.0;
-      finite = finite && isfinite(v);
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      B[i][j] = phi[i + j + 1] / (s[i] * s[j]);  // hankel / outer(s, s)
+      V[i][j] = (i == j) ? 1.0 : 0.0;
+      finite = finite && isfinite(B[i][j]);
     }
     c[i] = phi[i] / s[i];
     finite = finite && isfinite(c[i]);
   }
   if (!finite) return false;
-  // cyclic Jacobi: rotate while some |b_pq| exceeds eps * sqrt|b_pp b_qq|
+  // cyclic Jacobi: rotate while some |b_pq| > eps * sqrt|b_pp b_qq|
   for (int sweep = 0; sweep < 32; ++sweep) {
     bool rotated = false;
-    for (int p = 0; p < t - 1; ++p) {
-      for (int q = p + 1; q < t; ++q) {
-        const double apq = B[p * kTMax + q];
-        const double app = B[p * kTMax + p], aqq = B[q * kTMax + q];
-        if (apq == 0.0 || fabs(apq) <= 1e-16 * sqrt(fabs(app * aqq))) continue;
-        rotated = true;
-        const double tau = (aqq - app) / (2.0 * apq);
-        const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-        const double cs = 1.0 / sqrt(1.0 + tt * tt);
-        const double sn = tt * cs;
-        for (int k = 0; k < t; ++k) {  // B <- B J
-          const double bkp = B[k * kTMax + p], bkq = B[k * kTMax + q];
-          B[k * kTMax + p] = cs * bkp - sn * bkq;
-          B[k * kTMax + q] = sn * bkp + cs * bkq;
-        }
-        for (int k = 0; k < t; ++k) {  // B <- J^T B
-          const double bpk = B[p * kTMax + k], bqk = B[q * kTMax + k];
-          B[p * kTMax + k] = cs * bpk - sn * bqk;
-          B[q * kTMax + k] = sn * bpk + cs * bqk;
-        }
-        for (int k = 0; k < t; ++k) {  // V <- V J
-          const double vkp = V[k * kTMax + p], vkq = V[k * kTMax + q];
-          V[k * kTMax + p] = cs * vkp - sn * vkq;
-          V[k * kTMax + q] = sn * vkp + cs * vkq;
+#pragma unroll
+    for (int p = 0; p < T - 1; ++p) {
+#pragma unroll
+      for (int q = p + 1; q < T; ++q) {
+        const double apq = B[p][q], app = B[p][p], aqq = B[q][q];
+        if (apq != 0.0 && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
+          rotated = true;
+          const double tau = (aqq - app) / (2.0 * apq);
+          const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          const double cs = 1.0 / sqrt(1.0 + tt * tt);
+          const double sn = tt * cs;
+#pragma unroll
+          for (int k = 0; k < T; ++k) {  // B <- B J
+            const double bkp = B[k][p], bkq = B[k][q];
+            B[k][p] = cs * bkp - sn * bkq;
+            B[k][q] = sn * bkp + cs * bkq;
+          }
+#pragma unroll
+          for (int k = 0; k < T; ++k) {  // B <- J^T B
+            const double bpk = B[p][k], bqk = B[q][k];
+            B[p][k] = cs * bpk - sn * bqk;
+            B[q][k] = sn * bpk + cs * bqk;
+          }
+#pragma unroll
+          for (int k = 0; k < T; ++k) {  // V <- V J
+            const double vkp = V[k][p], vkq = V[k][q];
+            V[k][p] = cs * vkp - sn * vkq;
+            V[k][q] = sn * vkp + cs * vkq;
+          }
         }
       }
     }
     if (!rotated) break;
   }
   double smax = 0.0;
-  for (int k = 0; k < t; ++k) smax = fmax(smax, fabs(B[k * kTMax + k]));
+#pragma unroll
+  for (int k = 0; k < T; ++k) smax = fmax(smax, fabs(B[k][k]));
   const double cut = rcond * smax;  // gelsd: s_i <= rcond * s_max treated as zero
-  double beta[kTMax];
-  for (int i = 0; i < t; ++i) beta[i] = 0.0;
-  for (int k = 0; k < t; ++k) {
-    const double lam = B[k * kTMax + k];
-    if (!(fabs(lam) > cut)) continue;
-    double proj = 0.0;
-    for (int i = 0; i < t; ++i) proj += V[i * kTMax + k] * c[i];
-    const double wk = proj / lam;
-    for (int i = 0; i < t; ++i) beta[i] += wk * V[i * kTMax + k];
+  double beta[T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) beta[i] = 0.0;
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const double lam = B[k][k];
+    if (fabs(lam) > cut) {
+      double proj = 0.0;
+#pragma unroll
+      for (int i = 0; i < T; ++i) proj += V[i][k] * c[i];
+      const double wk = proj / lam;
+#pragma unroll
+      for (int i = 0; i < T; ++i) beta[i] += wk * V[i][k];
+    }
   }
   bool ok = true;
-  for (int i = 0; i < t; ++i) {
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
     alpha[i] = beta[i] / s[i];
     ok = ok && isfinite(alpha[i]);
   }
   return ok;
+}
+
+__device__ __noinline__ bool hankel_min_norm(const double* phi, int order, double rcond,
+                                             double* alpha) {
+  switch (order) {
+    case 1: return hankel_T<1>(phi, rcond, alpha);
+    case 2: return hankel_T<2>(phi, rcond, alpha);
+    case 3: return hankel_T<3>(phi, rcond, alpha);
+    case 4: return hankel_T<4>(phi, rcond, alpha);
+    case 5: return hankel_T<5>(phi, rcond, alpha);
+    case 6: return hankel_T<6>(phi, rcond, alpha);
+    case 7: return hankel_T<7>(phi, rcond, alpha);
+    case 8: return hankel_T<8>(phi, rcond, alpha);
+    default: return false;
+  }
 }
 
 // triangle-wave order schedule (centering.py:254-260)
@@ -204,38 +231,42 @@ struct EpiCtaP : EpiBase {
   __device__ void finish(double (&red)[K]) const {
     st->phi[2 * i - 2] = red[0];
     st->phi[2 * i - 1] = red[1];
+    if (i == st->t && with_solve) {
+      if (st->phi[1] == 0.0) {  // H r == 0: NormalEquationReached (centering.py:183-184)
+        st->status = TS_NORMAL_EQ_SOLUTION;
+        return;
+      }
+      st->atr_norm = st->gram ? sqrt(st->atr2) : sqrt(st->phi[1]);
+    }
   }
+  // the last pass of the moments runs the order-1..t Hankel solves, one
+  // thread per order, in its finishing block (no separate launch)
+  __device__ void finish_block() const {
+    __shared__ int bad;
+    if (!(with_solve && i == st->t && st->status == TS_RUNNING)) return;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    const int o = threadIdx.x + 1;
+    if (o <= st->t) {
+      if (!hankel_min_norm(st->phi, o, st->rcond, st->alpha_o[o - 1])) atomicExch(&bad, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && bad) {
+      st->status = TS_NUMERICAL_FAILURE;
+      st->detail = TS_DETAIL_MOMENT_SOLVE;
+    }
+  }
+  int with_solve = 1;
 };
 
-// one thread per order: Hankel solves for orders 1..t (all speculatively; the
-// candidate pass then applies the reference's t..1 retry rule)
-__global__ void k_cta_hankel(SolveState* s) {
-  __shared__ int bad;
-  __shared__ double scratch[kTMax][2 * kTMax * kTMax];
-  if (!(s->status == TS_RUNNING && s->maint == MAINT_NONE)) return;
-  ktimer_begin(&s->kt[3]);
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  if (s->phi[1] == 0.0) {  // H r == 0: NormalEquationReached (centering.py:183-184)
-    if (threadIdx.x == 0) {
-      s->status = TS_NORMAL_EQ_SOLUTION;
-      ktimer_end(&s->kt[3]);
-    }
-    return;
-  }
-  const int t = s->t;
-  const int o = threadIdx.x + 1;
-  if (o <= t) {
-    if (!hankel_min_norm(s->phi, o, s->rcond, s->alpha_o[o - 1], scratch[o - 1])) atomicExch(&bad, 1);
-  }
-  __syncthreads();
+// WHILE-body head: select the order-t case of the SWITCH node (t - 1), or
+// no case when the state is not running (defensive: the tail of the previous
+// trip already cleared the loop condition then).
+__global__ void k_cta_head(SolveState* s, cudaGraphConditionalHandle sw, int ncases) {
   if (threadIdx.x == 0) {
-    s->atr_norm = s->gram ? sqrt(s->atr2) : sqrt(s->phi[1]);
-    if (bad) {
-      s->status = TS_NUMERICAL_FAILURE;
-      s->detail = TS_DETAIL_MOMENT_SOLVE;
-    }
-    ktimer_end(&s->kt[3]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&s->launches), 1ull);
+    const bool run = s->status == TS_RUNNING && s->maint == MAINT_NONE;
+    cudaGraphSetConditional(sw, run ? (unsigned)(s->t - 1) : (unsigned)ncases);
   }
 }
 

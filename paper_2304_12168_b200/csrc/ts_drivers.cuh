@@ -7,7 +7,44 @@
 
 namespace ts {
 
-using BodyFn = std::function<int(cudaStream_t, cudaGraphConditionalHandle, int)>;
+// direct (non-graph) iteration: every kernel predicated on device state
+using BodyFn = std::function<int(cudaStream_t)>;
+// graph iteration: populate the WHILE body graph (captures + conditional nodes)
+using GraphFn = std::function<int(cudaGraph_t body, cudaGraphConditionalHandle hwhile, cudaStream_t cap)>;
+
+// add a SWITCH node at the current point of an ongoing capture on `cap`
+static int capture_switch(cudaStream_t cap, cudaGraphConditionalHandle h, int ncases,
+                          cudaGraph_t** cases) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  TS_CUDA(cudaStreamGetCaptureInfo(cap, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeSwitch;
+  np.conditional.size = ncases;
+  cudaGraphNode_t node;
+  TS_CUDA(cudaGraphAddNode(&node, g, deps, nd, &np));
+  TS_CUDA(cudaStreamUpdateCaptureDependencies(cap, &node, 1, cudaStreamSetCaptureDependencies));
+  *cases = np.conditional.phGraph_out;
+  return 0;
+}
+
+static int capture_into(cudaStream_t cap, cudaGraph_t g, const std::function<int(cudaStream_t)>& f) {
+  TS_CUDA(cudaStreamBeginCaptureToGraph(cap, g, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeThreadLocal));
+  const int rc = f(cap);
+  cudaGraph_t out = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cap, &out);
+  if (rc) return rc;
+  if (ce != cudaSuccess) {
+    set_error("graph capture failed: %s", cudaGetErrorString(ce));
+    return TS_ECUDA;
+  }
+  return 0;
+}
 
 static SolveState* pinned_state() {
   static thread_local SolveState* hs = nullptr;
@@ -103,7 +140,7 @@ struct SolveCtx {
     return 0;
   }
 
-  int build(const BodyFn& body) {
+  int build(const GraphFn& gbody) {
     TS_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle h;
     TS_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
@@ -116,23 +153,15 @@ struct SolveCtx {
     TS_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
     cudaGraph_t bodyg = np.conditional.phGraph_out[0];
     TS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    TS_CUDA(cudaStreamBeginCaptureToGraph(cap, bodyg, nullptr, nullptr, 0,
-                                          cudaStreamCaptureModeThreadLocal));
     const long long l0 = g_launches;
-    const int rc = body(cap, h, 1);
-    body_kernels = g_launches - l0;
-    cudaGraph_t outg = nullptr;
-    const cudaError_t ce = cudaStreamEndCapture(cap, &outg);
-    if (rc) return rc;
-    if (ce != cudaSuccess) {
-      set_error("graph capture failed: %s", cudaGetErrorString(ce));
-      return TS_ECUDA;
-    }
+    TS_CHECK(gbody(bodyg, h, cap));
+    body_kernels = g_launches - l0;  // captured once (per-trip count is derived on device)
     TS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     return 0;
   }
 
-  int run(const BodyFn& body, const std::function<int(cudaStream_t)>& maint) {
+  int run(const BodyFn& body, const GraphFn& gbody,
+          const std::function<int(cudaStream_t)>& maint) {
     TS_CHECK(read_state());
     TS_CHECK(flush());
     static const bool no_graph = getenv("TS_NO_GRAPH") != nullptr;
@@ -140,10 +169,10 @@ struct SolveCtx {
       if (hs->maint != MAINT_NONE) {
         TS_CHECK(maint(st));
       } else if (!no_graph) {
-        if (!exec) TS_CHECK(build(body));
+        if (!exec) TS_CHECK(build(gbody));
         TS_CUDA(cudaGraphLaunch(exec, st));
       } else {
-        TS_CHECK(body(st, 0, 0));
+        TS_CHECK(body(st));
       }
       TS_CHECK(read_state());
       TS_CHECK(flush());
@@ -157,8 +186,9 @@ struct SolveCtx {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev0, ev1);
     res->elapsed_ms = ms;
-    direct = (g_launches - l_start) - body_kernels;  // all direct launches of this solve
-    res->kernel_launches = direct + body_kernels * hs->body_runs;
+    // direct launches counted on the host; graph-executed kernels counted on
+    // the device (every pass / scalar kernel bumps its class counter)
+    res->kernel_launches = hs->launches;  // every solver kernel bumps it on the device
     return 0;
   }
 };
@@ -289,28 +319,48 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
     TS_CHECK(vecpass(M, mx, ez, wk, st));
   }
 
-  BodyFn body = [&](cudaStream_t s, cudaGraphConditionalHandle h, int use) -> int {
+  // one TA iteration: c = Op^T gap (finisher decides pivot / expand / stop)
+  auto c_pass = [&](cudaStream_t s, cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hsw,
+                    int use) -> int {
     EpiTaC ec;
-    ec.st = ds; ec.use_cond = 0; ec.c = cv;
-    TS_CHECK(op_apply_t(s, gap, ec, 1));
+    ec.st = ds; ec.c = cv; ec.cond = hw; ec.use_cond = use; ec.sw = hsw; ec.use_sw = use;
+    return op_apply_t(s, gap, ec, 1);
+  };
+  // pivot: v = Op pre (fused d.d, gap.d), then the convex-combination update
+  auto pivot = [&](cudaStream_t s, cudaGraphConditionalHandle hw, int use) -> int {
     EpiTaV ev;
-    ev.st = ds; ev.use_cond = 0; ev.bp = bp; ev.gap = gap; ev.d = d;
+    ev.st = ds; ev.bp = bp; ev.gap = gap; ev.d = d;
     XS xs;
     xs.sp = &ds->scale;
     xs.relu = relu;
     TS_CHECK(op_apply(s, cv, xs, ev, 2));
     EpiTaUpd eu;
-    eu.st = ds; eu.cond = h; eu.use_cond = use;
+    eu.st = ds; eu.cond = hw; eu.use_cond = use;
     eu.b = b; eu.d = d; eu.c = cv; eu.bp = bp; eu.gap = gap; eu.x = x; eu.m = mo; eu.n = no;
     eu.relu = relu;
     return vecpass(M, mx, eu, wk, s);
   };
+  BodyFn body = [&](cudaStream_t s) -> int {
+    TS_CHECK(c_pass(s, 0, 0, 0));
+    return pivot(s, 0, 0);
+  };
+  // graph body: [c pass] -> SWITCH{0: pivot}  (expand / stop select no case)
+  GraphFn gbody = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
+    cudaGraphConditionalHandle hsw;
+    TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
+    cudaGraph_t* cases = nullptr;
+    TS_CHECK(capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
+      TS_CHECK(c_pass(s, hw, hsw, 1));
+      return capture_switch(s, hsw, 1, &cases);
+    }));
+    return capture_into(cap, cases[0], [&](cudaStream_t s) -> int { return pivot(s, hw, 1); });
+  };
   auto maint = [&](cudaStream_t s) -> int {
     EpiTaBp eb;
-    eb.st = ds; eb.use_cond = 0; eb.b = b; eb.bp = bp; eb.gap = gap; eb.kind = 1;
+    eb.st = ds; eb.b = b; eb.bp = bp; eb.gap = gap; eb.kind = 1;
     return op_apply(s, x, XS{}, eb, 0);
   };
-  TS_CHECK(c.run(body, maint));
+  TS_CHECK(c.run(body, gbody, maint));
   if (c.hs->error == TS_EDEGENERATE) {
     set_error("degenerate pivot: v coincides with the iterate");
     return TS_EDEGENERATE;
@@ -364,35 +414,35 @@ static int cta_alloc(Arena& ar, const Mat& M, int t_max, int gram, CtaBuffers* B
   return 0;
 }
 
-// moments pairs for orders 1..t_max (predicated on state t)
-static int cta_pairs(const Mat& M, SolveState* ds, const Work& wk, const CtaBuffers& B, int t_max,
-                     int gram, cudaStream_t s) {
-  for (int i = 1; i <= t_max; ++i) {
+// moments pairs for orders 1..npairs (predicated on state t); `solve_last`
+// makes the pair that equals the state's t run the Hankel solves
+static int cta_pairs(const Mat& M, SolveState* ds, const Work& wk, const CtaBuffers& B, int npairs,
+                     int gram, int solve_last, cudaStream_t s) {
+  for (int i = 1; i <= npairs; ++i) {
     if (gram) {
       EpiCtaQ eq;
-      eq.st = ds; eq.use_cond = 0; eq.q = B.kp.q[i - 1]; eq.i = i;
+      eq.st = ds; eq.q = B.kp.q[i - 1]; eq.i = i;
       TS_CHECK(pass(M, 1, B.kp.p[i - 1], XS{}, eq, wk, s));
       EpiCtaP ep;
-      ep.st = ds; ep.use_cond = 0; ep.pprev = B.kp.p[i - 1]; ep.p = B.kp.p[i]; ep.i = i;
+      ep.st = ds; ep.pprev = B.kp.p[i - 1]; ep.p = B.kp.p[i]; ep.i = i; ep.with_solve = solve_last;
       TS_CHECK(pass(M, 0, B.kp.q[i - 1], XS{}, ep, wk, s));
     } else {
       EpiCtaP ep;
-      ep.st = ds; ep.use_cond = 0; ep.pprev = B.kp.p[i - 1]; ep.p = B.kp.p[i]; ep.i = i;
+      ep.st = ds; ep.pprev = B.kp.p[i - 1]; ep.p = B.kp.p[i]; ep.i = i; ep.with_solve = solve_last;
       TS_CHECK(pass(M, 0, B.kp.p[i - 1], XS{}, ep, wk, s));
     }
   }
   return 0;
 }
 
+// one CTA step of at most `npairs` pairs: moments (+ Hankel in the last pair's
+// finisher), candidate norms / retry rule, fused r / x update (tail)
 static int cta_step_kernels(const Mat& M, SolveState* ds, const Work& wk, const CtaBuffers& B,
-                            int t_max, int gram, cudaStream_t s, cudaGraphConditionalHandle h,
+                            int npairs, int gram, cudaStream_t s, cudaGraphConditionalHandle h,
                             int use) {
-  TS_CHECK(cta_pairs(M, ds, wk, B, t_max, gram, s));
-  ++g_launches;
-  k_cta_hankel<<<1, 32, 0, s>>>(ds);
-  TS_CUDA(cudaGetLastError());
+  TS_CHECK(cta_pairs(M, ds, wk, B, npairs, gram, 1, s));
   EpiCtaCand ecd;
-  ecd.st = ds; ecd.use_cond = 0; ecd.kp = B.kp; ecd.m = M.m;
+  ecd.st = ds; ecd.kp = B.kp; ecd.m = M.m;
   TS_CHECK(vecpass(M, M.m, ecd, wk, s));
   EpiCtaUpd eu;
   eu.st = ds; eu.cond = h; eu.use_cond = use; eu.kp = B.kp; eu.x = B.x; eu.m = M.m; eu.n = M.n;
@@ -440,18 +490,36 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     ei.st = ds; ei.use_cond = 0; ei.b = B.b; ei.r = B.kp.p[0]; ei.x = B.x; ei.m = M.m; ei.n = M.n;
     TS_CHECK(vecpass(M, std::max(M.m, M.n), ei, wk, st));
   }
-  BodyFn body = [&](cudaStream_t s, cudaGraphConditionalHandle h, int use) -> int {
-    return cta_step_kernels(M, ds, wk, B, a.t_max, a.gram, s, h, use);
+  BodyFn body = [&](cudaStream_t s) -> int {
+    return cta_step_kernels(M, ds, wk, B, a.t_max, a.gram, s, 0, 0);
+  };
+  // graph body: [head: switch = t - 1] -> SWITCH{order 1 .. t_max}: each case
+  // launches exactly its t pairs + candidate + update
+  GraphFn gbody = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
+    cudaGraphConditionalHandle hsw;
+    TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
+    cudaGraph_t* cases = nullptr;
+    TS_CHECK(capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
+      ++g_launches;
+      k_cta_head<<<1, 32, 0, s>>>(ds, hsw, a.t_max);
+      TS_CUDA(cudaGetLastError());
+      return capture_switch(s, hsw, a.t_max, &cases);
+    }));
+    for (int k = 0; k < a.t_max; ++k)
+      TS_CHECK(capture_into(cap, cases[k], [&](cudaStream_t s) -> int {
+        return cta_step_kernels(M, ds, wk, B, k + 1, a.gram, s, hw, 1);
+      }));
+    return 0;
   };
   auto maint = [&](cudaStream_t s) -> int {
     EpiNormTo en;
-    en.st = ds; en.use_cond = 0; en.v = B.x; en.len = M.n; en.what = 1;
+    en.st = ds; en.v = B.x; en.len = M.n; en.what = 1;
     TS_CHECK(vecpass(M, M.n, en, wk, s));
     EpiCtaRecheck er;
-    er.st = ds; er.use_cond = 0; er.b = B.b; er.r = B.kp.p[0];
+    er.st = ds; er.b = B.b; er.r = B.kp.p[0];
     return pass(M, 0, B.x, XS{}, er, wk, s);
   };
-  TS_CHECK(c.run(body, maint));
+  TS_CHECK(c.run(body, gbody, maint));
   if (!c.hs->trivial) {
     EpiFinalR efr;
     efr.st = ds; efr.use_cond = 0; efr.b = B.b; efr.fr = B.fr;
@@ -469,9 +537,7 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
 }
 
 __global__ void k_hankel_one(const double* phi, int order, double rcond, double* alpha, int* ok) {
-  __shared__ double scratch[2 * kTMax * kTMax];
-  if (threadIdx.x == 0 && blockIdx.x == 0)
-    *ok = hankel_min_norm(phi, order, rcond, alpha, scratch) ? 1 : 0;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *ok = hankel_min_norm(phi, order, rcond, alpha) ? 1 : 0;
 }
 
 }  // namespace ts
@@ -629,7 +695,7 @@ int ts_moments(const ts_matrix* A, int32_t h_mode, const double* r, int32_t t, d
     CtaBuffers B;
     TS_CHECK(cta_alloc(c.ar, *A, t, gram, &B));
     TS_CUDA(cudaMemcpyAsync(B.kp.p[0], r, A->m * sizeof(double), cudaMemcpyDefault, st));
-    TS_CHECK(cta_pairs(*A, c.ds, c.wk, B, t, gram, st));
+    TS_CHECK(cta_pairs(*A, c.ds, c.wk, B, t, gram, 0, st));
     TS_CHECK(c.read_state());
     memcpy(phi, c.hs->phi, 2 * t * sizeof(double));
     if (krylov)

@@ -28,6 +28,8 @@
 //   __device__ void finish(double (&red)[K]) const;  thread 0, last block
 //   __device__ void idle() const;           block 0 / thread 0 when inactive
 //   __device__ KTimer* timer() const;       live accounting slot or nullptr
+//   __device__ void finish_block() const;   whole last block, after finish()
+//   __device__ void count_launch() const;   block 0 / thread 0 at entry
 #pragma once
 
 #include "ts_common.cuh"
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_flat(Acc A, const doub
   __shared__ double psum[kWarps][2];
   __shared__ int pcnt[kWarps];
   __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
@@ -292,6 +295,8 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_flat(Acc A, const doub
       ktimer_end(kt);
       epi.finish(red);
     }
+    __syncthreads();
+    epi.finish_block();
   }
 }
 
@@ -302,6 +307,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const dou
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
@@ -327,6 +333,8 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const dou
       ktimer_end(kt);
       epi.finish(red);
     }
+    __syncthreads();
+    epi.finish_block();
   }
 }
 
@@ -338,6 +346,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
   constexpr int RU = 8;  // rows in flight per thread
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
@@ -453,6 +462,8 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
       ktimer_end(kt);
       epi.finish(red);
     }
+    __syncthreads();
+    epi.finish_block();
   }
 }
 
@@ -462,6 +473,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_vec(int64_t len, Epi epi, W
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
@@ -485,6 +497,8 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_vec(int64_t len, Epi epi, W
       ktimer_end(kt);
       epi.finish(red);
     }
+    __syncthreads();
+    epi.finish_block();
   }
 }
 

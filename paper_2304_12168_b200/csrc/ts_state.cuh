@@ -32,7 +32,7 @@ struct alignas(16) SolveState {
   int accel_patience, enhanced, seg_cap, pad0;
   long long iterations, max_iters, recheck_every;
   long long m_rows, n_cols;
-  long long trace_count, trace_flushed, body_runs;
+  long long trace_count, trace_flushed, body_runs, launches;
   unsigned long long t0, wall_pending;
   // TA / ball / LP
   double eps, eps_prime, rho, rho_cap, rho_max;
@@ -194,9 +194,14 @@ __device__ inline void ta_decide(SolveState* s, double c2, double cp2) {
 // ------------------------------------------------------------ epilogues ----
 struct EpiBase {
   SolveState* st = nullptr;
-  cudaGraphConditionalHandle cond = 0;
+  cudaGraphConditionalHandle cond = 0;  // WHILE loop condition (tail kernels)
+  cudaGraphConditionalHandle sw = 0;    // SWITCH selector set by a finisher
   int use_cond = 0;
+  int use_sw = 0;
   int tclass = -1;  // live accounting class (set by the launch helper)
+  __device__ __forceinline__ void count_launch() const {
+    if (st) atomicAdd(reinterpret_cast<unsigned long long*>(&st->launches), 1ull);
+  }
   __device__ __forceinline__ int op(int) const { return RED_SUM; }
   __device__ __forceinline__ KTimer* timer() const {
     return (st && tclass >= 0) ? &st->kt[tclass] : nullptr;
@@ -213,6 +218,7 @@ struct EpiBase {
       set_cond(cond, 1, st);
     }
   }
+  __device__ __forceinline__ void finish_block() const {}
 };
 
 __device__ __forceinline__ bool running(const SolveState* s) {
@@ -307,7 +313,14 @@ struct EpiTaC : EpiBase {
     const double cp = (y >= 0.0 || y != y) ? y : 0.0;
     acc[1] = fma(cp, cp, acc[1]);
   }
-  __device__ void finish(double (&r)[K]) const { ta_decide(st, r[0], r[1]); }
+  __device__ void finish(double (&r)[K]) const {
+    ta_decide(st, r[0], r[1]);
+    if (use_sw) cudaGraphSetConditional(sw, st->event == EV_PIVOT ? 0u : 1u);
+    if (use_cond) {
+      if (st->event != EV_PIVOT) st->body_runs += 1;
+      set_cond(cond, 1, st);
+    }
+  }
 };
 
 // v = A pre, d = v - b'.  sums: d.d, gap.d  (move_to_pivot, triangle.py:69-81)
@@ -447,6 +460,8 @@ struct EpiDot {
   __device__ bool active() const { return true; }
   __device__ void idle() const {}
   __device__ KTimer* timer() const { return nullptr; }
+  __device__ void finish_block() const {}
+  __device__ void count_launch() const {}
   __device__ void elem(int64_t i, double (&acc)[K]) const { acc[0] = fma(u[i], v[i], acc[0]); }
   __device__ void finish(double (&r)[K]) const { *out = sqrt_out ? sqrt(r[0]) : r[0]; }
 };
