@@ -56,144 +56,7 @@ static SolveState* pinned_state() {
   return hs;
 }
 
-struct SolveCtx {
-  const Mat& M;
-  cudaStream_t st;
-  Arena ar;
-  Work wk;
-  SolveState* ds = nullptr;
-  SolveState* hs = nullptr;
-  long long* hflushed = nullptr;
-  ts_trace_row* dtrace = nullptr;
-  int seg_cap = 1;
-  ts_trace_row* utrace = nullptr;
-  int64_t ucap = 0;
-  long long flushed = 0;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  cudaStream_t cap = nullptr;
-  long long direct = 0, body_kernels = 0, l_start = 0;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-
-  SolveCtx(const Mat& m, cudaStream_t s) : M(m), st(s), ar(s) {}
-  ~SolveCtx() {
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    if (cap) cudaStreamDestroy(cap);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-  }
-
-  int init(SolveState& init_state, int64_t max_iters, ts_trace_row* trace, int64_t trace_cap) {
-    l_start = g_launches;
-    hs = pinned_state();
-    if (!hs) {
-      set_error("cudaHostAlloc for the solve state failed");
-      return TS_ENOMEM;
-    }
-    hflushed = reinterpret_cast<long long*>(reinterpret_cast<char*>(hs) + sizeof(SolveState));
-    TS_CHECK(make_work(ar, work_blocks(M.sms), &wk));
-    TS_CHECK(ar.get(&ds, 1));
-    long long want = max_iters + 2;
-    if (want < 16) want = 16;
-    seg_cap = (int)std::min<long long>(want, 8192);
-    TS_CHECK(ar.get(&dtrace, (size_t)seg_cap));
-    utrace = trace;
-    ucap = trace ? trace_cap : 0;
-    init_state.trace = dtrace;
-    init_state.seg_cap = seg_cap;
-    for (int i = 0; i < 4; ++i) init_state.kt[i] = KTimer{~0ull, 0ull, 0, 0};
-    *hs = init_state;
-    TS_CUDA(cudaMemcpyAsync(ds, hs, sizeof(SolveState), cudaMemcpyHostToDevice, st));
-    TS_CUDA(cudaEventCreate(&ev0));
-    TS_CUDA(cudaEventCreate(&ev1));
-    TS_CUDA(cudaEventRecord(ev0, st));
-    return 0;
-  }
-
-  int read_state() {
-    TS_CUDA(cudaMemcpyAsync(hs, ds, sizeof(SolveState), cudaMemcpyDeviceToHost, st));
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) {
-      set_error("device failure during solve: %s", cudaGetErrorString(e));
-      return TS_ECUDA;
-    }
-    return 0;
-  }
-
-  int flush() {
-    const long long upto = hs->trace_count;
-    while (flushed < upto) {
-      const long long ring = flushed % seg_cap;
-      long long chunk = std::min<long long>(upto - flushed, seg_cap - ring);
-      if (flushed < ucap) {
-        const long long n = std::min<long long>(chunk, ucap - flushed);
-        TS_CUDA(cudaMemcpyAsync(utrace + flushed, dtrace + ring, n * sizeof(ts_trace_row),
-                                cudaMemcpyDefault, st));
-      }
-      flushed += chunk;
-    }
-    *hflushed = flushed;
-    TS_CUDA(cudaMemcpyAsync(&ds->trace_flushed, hflushed, sizeof(long long),
-                            cudaMemcpyHostToDevice, st));
-    TS_CUDA(cudaStreamSynchronize(st));  // hflushed / ring reuse
-    return 0;
-  }
-
-  int build(const GraphFn& gbody) {
-    TS_CUDA(cudaGraphCreate(&graph, 0));
-    cudaGraphConditionalHandle h;
-    TS_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams np = {};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    cudaGraphNode_t node;
-    TS_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
-    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
-    TS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    const long long l0 = g_launches;
-    TS_CHECK(gbody(bodyg, h, cap));
-    body_kernels = g_launches - l0;  // captured once (per-trip count is derived on device)
-    TS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-    return 0;
-  }
-
-  int run(const BodyFn& body, const GraphFn& gbody,
-          const std::function<int(cudaStream_t)>& maint) {
-    TS_CHECK(read_state());
-    TS_CHECK(flush());
-    static const bool no_graph = getenv("TS_NO_GRAPH") != nullptr;
-    while (hs->status == TS_RUNNING) {
-      if (hs->maint != MAINT_NONE) {
-        TS_CHECK(maint(st));
-      } else if (!no_graph) {
-        if (!exec) TS_CHECK(build(gbody));
-        TS_CUDA(cudaGraphLaunch(exec, st));
-      } else {
-        TS_CHECK(body(st));
-      }
-      TS_CHECK(read_state());
-      TS_CHECK(flush());
-    }
-    return 0;
-  }
-
-  int finish_timing(ts_result* res) {
-    TS_CUDA(cudaEventRecord(ev1, st));
-    TS_CUDA(cudaEventSynchronize(ev1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev0, ev1);
-    res->elapsed_ms = ms;
-    // direct launches counted on the host; graph-executed kernels counted on
-    // the device (every pass / scalar kernel bumps its class counter)
-    res->kernel_launches = hs->launches;  // every solver kernel bumps it on the device
-    return 0;
-  }
-};
-
-// count every launch we enqueue (graph bodies are counted once at capture)
+// count every launch we enqueue
 template <class Epi>
 static int pass(const Mat& M, int trans, const double* x, XS xs, const Epi& e, const Work& w,
                 cudaStream_t s) {
@@ -217,6 +80,237 @@ static int vecpass(const Mat& M, int64_t len, const Epi& e, const Work& w, cudaS
     return launch_vec(len, M.sms, e, w, s);
   }
 }
+
+// ----------------------------------------------------------- instances ----
+// A solver instance owns everything a solve touches on the device — state,
+// reduction workspace, trace ring, vectors — plus the instantiated CUDA graph
+// whose kernel nodes bake those addresses in.  Instances are cached on the
+// (immutable) matrix handle per solver shape, so a repeated solve is just
+// memcpy-in, init kernels, graph launches, final kernels, memcpy-out.
+struct Instance {
+  int key[4] = {0, 0, 0, 0};
+  bool in_use = false;
+  std::vector<void*> allocs;
+  SolveState* ds = nullptr;
+  Work wk;
+  ts_trace_row* dtrace = nullptr;
+  int seg_cap = 8192;
+  // TA family vectors
+  double *b = nullptr, *bp = nullptr, *gap = nullptr, *d = nullptr, *x = nullptr, *cv = nullptr,
+         *fr = nullptr, *t1 = nullptr, *x0 = nullptr;
+  // CTA vectors
+  double *xs = nullptr;
+  KrylovPtrs kp;
+  // graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  template <class T>
+  int alloc(T** out, size_t count) {
+    void* p = nullptr;
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      set_error("cudaMalloc(%zu) for a solver instance failed", bytes);
+      return TS_ENOMEM;
+    }
+    allocs.push_back(p);
+    *out = static_cast<T*>(p);
+    return 0;
+  }
+  int init_common(const Mat& M) {
+    const int pmax = work_blocks(M.sms);
+    TS_CHECK(alloc(&wk.bacc, (size_t)pmax * kKMax));
+    TS_CHECK(alloc(&wk.facc, (size_t)pmax * kKMax));
+    TS_CHECK(alloc(&wk.bpart, (size_t)pmax * 2));
+    TS_CHECK(alloc(&wk.tpart, (size_t)pmax * 2 * kCW));
+    TS_CHECK(alloc(&wk.cnt, (size_t)pmax));
+    TS_CHECK(alloc(&wk.done, 4));
+    wk.pmax = pmax;
+    TS_CUDA(cudaMemset(wk.cnt, 0, sizeof(unsigned) * pmax));
+    TS_CUDA(cudaMemset(wk.done, 0, sizeof(unsigned) * 4));
+    TS_CHECK(alloc(&ds, 1));
+    TS_CHECK(alloc(&dtrace, (size_t)seg_cap));
+    TS_CUDA(cudaEventCreate(&ev0));
+    TS_CUDA(cudaEventCreate(&ev1));
+    return 0;
+  }
+  ~Instance() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (cap) cudaStreamDestroy(cap);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    for (void* p : allocs) cudaFree(p);
+  }
+
+  int build(const GraphFn& gbody) {
+    TS_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    TS_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    TS_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+    TS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    TS_CHECK(gbody(bodyg, h, cap));
+    TS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    return 0;
+  }
+};
+
+void destroy_instances(Mat* M) {
+  std::lock_guard<std::mutex> g(M->cache_mu);
+  for (Instance* I : M->cache) delete I;
+  M->cache.clear();
+}
+
+// Take a free cached instance with this key, or make one with `setup`.
+static int acquire(const Mat& Mc, const int key[4], const std::function<int(Instance*)>& setup,
+                   Instance** out) {
+  Mat& M = const_cast<Mat&>(Mc);  // the cache is the handle's only mutable part
+  {
+    std::lock_guard<std::mutex> g(M.cache_mu);
+    for (Instance* I : M.cache) {
+      if (!I->in_use && memcmp(I->key, key, sizeof(I->key)) == 0) {
+        I->in_use = true;
+        *out = I;
+        return 0;
+      }
+    }
+  }
+  Instance* I = new Instance();
+  memcpy(I->key, key, sizeof(I->key));
+  int rc = I->init_common(M);
+  if (!rc) rc = setup(I);
+  if (rc) {
+    delete I;
+    return rc;
+  }
+  I->in_use = true;
+  {
+    std::lock_guard<std::mutex> g(M.cache_mu);
+    if (M.cache.size() < 16) M.cache.push_back(I);
+    else I->key[3] = -1;  // uncached: released by delete
+  }
+  *out = I;
+  return 0;
+}
+static void release(const Mat& Mc, Instance* I) {
+  Mat& M = const_cast<Mat&>(Mc);
+  if (I->key[3] == -1) {
+    delete I;
+    return;
+  }
+  std::lock_guard<std::mutex> g(M.cache_mu);
+  I->in_use = false;
+}
+struct InstanceLease {
+  const Mat& M;
+  Instance* I = nullptr;
+  explicit InstanceLease(const Mat& m) : M(m) {}
+  ~InstanceLease() {
+    if (I) release(M, I);
+  }
+};
+
+// Per-call driver state around an instance.
+struct SolveCtx {
+  const Mat& M;
+  cudaStream_t st;
+  Instance* I;
+  SolveState* hs = nullptr;
+  long long* hflushed = nullptr;
+  ts_trace_row* utrace = nullptr;
+  int64_t ucap = 0;
+  long long flushed = 0;
+
+  SolveCtx(const Mat& m, cudaStream_t s, Instance* inst) : M(m), st(s), I(inst) {}
+
+  int init(SolveState& init_state, ts_trace_row* trace, int64_t trace_cap) {
+    hs = pinned_state();
+    if (!hs) {
+      set_error("cudaHostAlloc for the solve state failed");
+      return TS_ENOMEM;
+    }
+    hflushed = reinterpret_cast<long long*>(reinterpret_cast<char*>(hs) + sizeof(SolveState));
+    utrace = trace;
+    ucap = trace ? trace_cap : 0;
+    init_state.trace = I->dtrace;
+    init_state.seg_cap = I->seg_cap;
+    for (int i = 0; i < 4; ++i) init_state.kt[i] = KTimer{~0ull, 0ull, 0, 0};
+    *hs = init_state;
+    TS_CUDA(cudaEventRecord(I->ev0, st));
+    TS_CUDA(cudaMemcpyAsync(I->ds, hs, sizeof(SolveState), cudaMemcpyHostToDevice, st));
+    return 0;
+  }
+
+  int read_state() {
+    TS_CUDA(cudaMemcpyAsync(hs, I->ds, sizeof(SolveState), cudaMemcpyDeviceToHost, st));
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error("device failure during solve: %s", cudaGetErrorString(e));
+      return TS_ECUDA;
+    }
+    return 0;
+  }
+
+  int flush() {
+    const long long upto = hs->trace_count;
+    if (upto == flushed) return 0;
+    const int seg_cap = I->seg_cap;
+    while (flushed < upto) {
+      const long long ring = flushed % seg_cap;
+      long long chunk = std::min<long long>(upto - flushed, seg_cap - ring);
+      if (flushed < ucap) {
+        const long long n = std::min<long long>(chunk, ucap - flushed);
+        TS_CUDA(cudaMemcpyAsync(utrace + flushed, I->dtrace + ring, n * sizeof(ts_trace_row),
+                                cudaMemcpyDefault, st));
+      }
+      flushed += chunk;
+    }
+    *hflushed = flushed;
+    TS_CUDA(cudaMemcpyAsync(&I->ds->trace_flushed, hflushed, sizeof(long long),
+                            cudaMemcpyHostToDevice, st));
+    TS_CUDA(cudaStreamSynchronize(st));  // hflushed / ring reuse
+    return 0;
+  }
+
+  int run(const BodyFn& body, const GraphFn& gbody,
+          const std::function<int(cudaStream_t)>& maint) {
+    TS_CHECK(read_state());
+    TS_CHECK(flush());
+    static const bool no_graph = getenv("TS_NO_GRAPH") != nullptr;
+    while (hs->status == TS_RUNNING) {
+      if (hs->maint != MAINT_NONE) {
+        TS_CHECK(maint(st));
+      } else if (!no_graph) {
+        if (!I->exec) TS_CHECK(I->build(gbody));
+        TS_CUDA(cudaGraphLaunch(I->exec, st));
+      } else {
+        TS_CHECK(body(st));
+      }
+      TS_CHECK(read_state());
+      TS_CHECK(flush());
+    }
+    return 0;
+  }
+
+  int finish_timing(ts_result* res) {
+    TS_CUDA(cudaEventRecord(I->ev1, st));
+    TS_CUDA(cudaEventSynchronize(I->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, I->ev0, I->ev1);
+    res->elapsed_ms = ms;
+    res->kernel_launches = hs->launches;  // every solver kernel bumps it on the device
+    return 0;
+  }
+};
 
 static void fill_result(const SolveState& s, ts_result* r) {
   r->status = s.status;
@@ -247,13 +341,87 @@ struct TaArgs {
   const double* x0 = nullptr;
 };
 
+// kernels of the TA family bound to one instance
+struct TaKernels {
+  const Mat& M;
+  Instance* I;
+  int gram, relu;
+  int64_t mo, no, mx;
+
+  // y = Op v with a fused epilogue (Op = A, or A^T A for the Gram pair)
+  template <class Epi>
+  int op_apply(cudaStream_t s, const double* v, XS xs, const Epi& epi, int pred) const {
+    if (!gram) return pass(M, 0, v, xs, epi, I->wk, s);
+    EpiStore es;
+    es.st = I->ds; es.y = I->t1; es.pred = pred;
+    TS_CHECK(pass(M, 0, v, xs, es, I->wk, s));
+    return pass(M, 1, I->t1, XS{}, epi, I->wk, s);
+  }
+  template <class Epi>
+  int op_apply_t(cudaStream_t s, const double* v, const Epi& epi, int pred) const {
+    if (!gram) return pass(M, 1, v, XS{}, epi, I->wk, s);
+    EpiStore es;
+    es.st = I->ds; es.y = I->t1; es.pred = pred;
+    TS_CHECK(pass(M, 0, v, XS{}, es, I->wk, s));
+    return pass(M, 1, I->t1, XS{}, epi, I->wk, s);
+  }
+  // c = Op^T gap; the finisher decides pivot / expand / stop
+  int c_pass(cudaStream_t s, cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hsw,
+             int use) const {
+    EpiTaC ec;
+    ec.st = I->ds; ec.c = I->cv; ec.cond = hw; ec.use_cond = use; ec.sw = hsw; ec.use_sw = use;
+    return op_apply_t(s, I->gap, ec, 1);
+  }
+  // pivot: v = Op pre (fused d.d, gap.d), then the convex-combination update
+  int pivot(cudaStream_t s, cudaGraphConditionalHandle hw, int use) const {
+    EpiTaV ev;
+    ev.st = I->ds; ev.bp = I->bp; ev.gap = I->gap; ev.d = I->d;
+    XS xs;
+    xs.sp = &I->ds->scale;
+    xs.relu = relu;
+    TS_CHECK(op_apply(s, I->cv, xs, ev, 2));
+    EpiTaUpd eu;
+    eu.st = I->ds; eu.cond = hw; eu.use_cond = use;
+    eu.b = I->b; eu.d = I->d; eu.c = I->cv; eu.bp = I->bp; eu.gap = I->gap; eu.x = I->x;
+    eu.m = mo; eu.n = no; eu.relu = relu;
+    return vecpass(M, mx, eu, I->wk, s);
+  }
+  // graph body: [c pass] -> SWITCH{0: pivot}  (expand / stop select no case)
+  int graph(cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) const {
+    cudaGraphConditionalHandle hsw;
+    TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
+    cudaGraph_t* cases = nullptr;
+    TS_CHECK(capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
+      TS_CHECK(c_pass(s, hw, hsw, 1));
+      return capture_switch(s, hsw, 1, &cases);
+    }));
+    return capture_into(cap, cases[0], [&](cudaStream_t s) -> int { return pivot(s, hw, 1); });
+  }
+};
+
 static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x_out,
                     double* bp_out, ts_trace_row* trace, int64_t trace_cap, ts_result* res,
                     cudaStream_t st) {
   const int64_t mo = a.gram ? M.n : M.m;  // operator rows (TA's b-space)
   const int64_t no = M.n;                 // operator cols (x-space)
   const int64_t mx = std::max(mo, no);
-  SolveCtx c(M, st);
+  const int relu = a.mode == MODE_LP;
+  const int key[4] = {1, a.gram, relu, 0};
+  InstanceLease lease(M);
+  TS_CHECK(acquire(M, key, [&](Instance* I) -> int {
+    TS_CHECK(I->alloc(&I->b, mo));
+    TS_CHECK(I->alloc(&I->bp, mo));
+    TS_CHECK(I->alloc(&I->gap, mo));
+    TS_CHECK(I->alloc(&I->d, mo));
+    TS_CHECK(I->alloc(&I->fr, mo));
+    TS_CHECK(I->alloc(&I->x, no));
+    TS_CHECK(I->alloc(&I->cv, no));
+    TS_CHECK(I->alloc(&I->x0, no));
+    if (a.gram) TS_CHECK(I->alloc(&I->t1, M.m));
+    return 0;
+  }, &lease.I));
+  Instance* I = lease.I;
+  SolveCtx c(M, st, I);
   SolveState s0;
   memset(&s0, 0, sizeof(s0));
   s0.mode = a.mode;
@@ -268,97 +436,40 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
   s0.a_fro = a.gram ? M.fro * M.fro : M.fro;
   s0.m_rows = mo;
   s0.n_cols = no;
-  s0.x_min = 0.0;
-  s0.lower_bound = 0.0;
-  TS_CHECK(c.init(s0, a.max_iters, trace, trace_cap));
-  Arena& ar = c.ar;
-  double *b, *bp, *gap, *d, *x, *cv, *fr, *t1 = nullptr, *x0 = nullptr;
-  TS_CHECK(stage_in(ar, b_in, mo, &b));
-  TS_CHECK(ar.get(&bp, mo));
-  TS_CHECK(ar.get(&gap, mo));
-  TS_CHECK(ar.get(&d, mo));
-  TS_CHECK(ar.get(&fr, mo));
-  TS_CHECK(ar.get(&x, no));
-  TS_CHECK(ar.get(&cv, no));
-  if (a.gram) TS_CHECK(ar.get(&t1, M.m));
-  if (a.x0) TS_CHECK(stage_in(ar, a.x0, no, &x0));
-  SolveState* ds = c.ds;
-  const Work& wk = c.wk;
-  const int relu = a.mode == MODE_LP;
+  TS_CHECK(c.init(s0, trace, trace_cap));
+  SolveState* ds = I->ds;
+  const Work& wk = I->wk;
+  TaKernels K{M, I, a.gram, relu, mo, no, mx};
+  TS_CUDA(cudaMemcpyAsync(I->b, b_in, mo * sizeof(double), cudaMemcpyDefault, st));
 
-  // operator products with fused epilogue: y = Op v  (Op = A, or A^T A)
-  auto op_apply = [&](cudaStream_t s, const double* v, XS xs, auto epi, int pred) -> int {
-    if (!a.gram) return pass(M, 0, v, xs, epi, wk, s);
-    EpiStore es;
-    es.st = ds; es.y = t1; es.pred = pred;
-    TS_CHECK(pass(M, 0, v, xs, es, wk, s));
-    return pass(M, 1, t1, XS{}, epi, wk, s);
-  };
-  auto op_apply_t = [&](cudaStream_t s, const double* v, auto epi, int pred) -> int {
-    if (!a.gram) return pass(M, 1, v, XS{}, epi, wk, s);
-    EpiStore es;
-    es.st = ds; es.y = t1; es.pred = pred;
-    TS_CHECK(pass(M, 0, v, XS{}, es, wk, s));
-    return pass(M, 1, t1, XS{}, epi, wk, s);
-  };
-
-  // ---- init
-  if (x0) {
+  // ---- init (triangle.py:197-204, feasibility.py:77-79)
+  if (a.x0) {
+    TS_CUDA(cudaMemcpyAsync(I->x0, a.x0, no * sizeof(double), cudaMemcpyDefault, st));
     EpiNormTo en;
-    en.st = ds; en.use_cond = 0; en.v = x0; en.len = no; en.what = 0;
+    en.st = ds; en.v = I->x0; en.len = no; en.what = 0;
     TS_CHECK(vecpass(M, no, en, wk, st));
     EpiCopyWarm ec;
-    ec.st = ds; ec.use_cond = 0; ec.src = x0; ec.dst = x;
+    ec.st = ds; ec.src = I->x0; ec.dst = I->x;
     TS_CHECK(vecpass(M, no, ec, wk, st));
     EpiTaBp eb;
-    eb.st = ds; eb.use_cond = 0; eb.b = b; eb.bp = bp; eb.gap = gap; eb.kind = 0;
-    TS_CHECK(op_apply(st, x, XS{}, eb, 0));
+    eb.st = ds; eb.b = I->b; eb.bp = I->bp; eb.gap = I->gap; eb.kind = 0;
+    TS_CHECK(K.op_apply(st, I->x, XS{}, eb, 0));
   } else {
     EpiTaInitZero ez;
-    ez.st = ds; ez.use_cond = 0; ez.b = b; ez.bp = bp; ez.gap = gap; ez.x = x; ez.m = mo; ez.n = no;
+    ez.st = ds; ez.b = I->b; ez.bp = I->bp; ez.gap = I->gap; ez.x = I->x; ez.m = mo; ez.n = no;
     TS_CHECK(vecpass(M, mx, ez, wk, st));
   }
-
-  // one TA iteration: c = Op^T gap (finisher decides pivot / expand / stop)
-  auto c_pass = [&](cudaStream_t s, cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hsw,
-                    int use) -> int {
-    EpiTaC ec;
-    ec.st = ds; ec.c = cv; ec.cond = hw; ec.use_cond = use; ec.sw = hsw; ec.use_sw = use;
-    return op_apply_t(s, gap, ec, 1);
-  };
-  // pivot: v = Op pre (fused d.d, gap.d), then the convex-combination update
-  auto pivot = [&](cudaStream_t s, cudaGraphConditionalHandle hw, int use) -> int {
-    EpiTaV ev;
-    ev.st = ds; ev.bp = bp; ev.gap = gap; ev.d = d;
-    XS xs;
-    xs.sp = &ds->scale;
-    xs.relu = relu;
-    TS_CHECK(op_apply(s, cv, xs, ev, 2));
-    EpiTaUpd eu;
-    eu.st = ds; eu.cond = hw; eu.use_cond = use;
-    eu.b = b; eu.d = d; eu.c = cv; eu.bp = bp; eu.gap = gap; eu.x = x; eu.m = mo; eu.n = no;
-    eu.relu = relu;
-    return vecpass(M, mx, eu, wk, s);
-  };
   BodyFn body = [&](cudaStream_t s) -> int {
-    TS_CHECK(c_pass(s, 0, 0, 0));
-    return pivot(s, 0, 0);
+    TS_CHECK(K.c_pass(s, 0, 0, 0));
+    return K.pivot(s, 0, 0);
   };
-  // graph body: [c pass] -> SWITCH{0: pivot}  (expand / stop select no case)
   GraphFn gbody = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
-    cudaGraphConditionalHandle hsw;
-    TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
-    cudaGraph_t* cases = nullptr;
-    TS_CHECK(capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
-      TS_CHECK(c_pass(s, hw, hsw, 1));
-      return capture_switch(s, hsw, 1, &cases);
-    }));
-    return capture_into(cap, cases[0], [&](cudaStream_t s) -> int { return pivot(s, hw, 1); });
+    return K.graph(bodyg, hw, cap);
   };
   auto maint = [&](cudaStream_t s) -> int {
     EpiTaBp eb;
-    eb.st = ds; eb.b = b; eb.bp = bp; eb.gap = gap; eb.kind = 1;
-    return op_apply(s, x, XS{}, eb, 0);
+    eb.st = ds; eb.b = I->b; eb.bp = I->bp; eb.gap = I->gap; eb.kind = 1;
+    return K.op_apply(s, I->x, XS{}, eb, 0);
   };
   TS_CHECK(c.run(body, gbody, maint));
   if (c.hs->error == TS_EDEGENERATE) {
@@ -366,18 +477,18 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
     return TS_EDEGENERATE;
   }
   if (c.hs->trivial) {
-    TS_CUDA(cudaMemsetAsync(x, 0, no * sizeof(double), st));
+    TS_CUDA(cudaMemsetAsync(I->x, 0, no * sizeof(double), st));
   } else {
     EpiFinalR efr;
-    efr.st = ds; efr.use_cond = 0; efr.b = b; efr.fr = fr;
-    TS_CHECK(op_apply(st, x, XS{}, efr, 0));
+    efr.st = ds; efr.b = I->b; efr.fr = I->fr;
+    TS_CHECK(K.op_apply(st, I->x, XS{}, efr, 0));
     EpiFinalNR enr;
-    enr.st = ds; enr.use_cond = 0; enr.out = nullptr;
-    TS_CHECK(op_apply_t(st, fr, enr, 0));
+    enr.st = ds; enr.out = nullptr;
+    TS_CHECK(K.op_apply_t(st, I->fr, enr, 0));
   }
   TS_CHECK(c.read_state());
-  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, x, no * sizeof(double), cudaMemcpyDefault, st));
-  if (bp_out) TS_CUDA(cudaMemcpyAsync(bp_out, bp, mo * sizeof(double), cudaMemcpyDefault, st));
+  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, no * sizeof(double), cudaMemcpyDefault, st));
+  if (bp_out) TS_CUDA(cudaMemcpyAsync(bp_out, I->bp, mo * sizeof(double), cudaMemcpyDefault, st));
   fill_result(*c.hs, res);
   TS_CHECK(c.finish_timing(res));
   TS_CUDA(cudaStreamSynchronize(st));
@@ -399,37 +510,36 @@ struct CtaArgs {
   const double* x_start = nullptr;
 };
 
-struct CtaBuffers {
-  double *b = nullptr, *x = nullptr, *fr = nullptr, *xs = nullptr;
-  KrylovPtrs kp;
-};
-
-static int cta_alloc(Arena& ar, const Mat& M, int t_max, int gram, CtaBuffers* B) {
-  memset(&B->kp, 0, sizeof(B->kp));
-  for (int i = 0; i <= t_max; ++i) TS_CHECK(ar.get(&B->kp.p[i], M.m));
+static int cta_alloc(Instance* I, const Mat& M, int t_max, int gram) {
+  memset(&I->kp, 0, sizeof(I->kp));
+  for (int i = 0; i <= t_max; ++i) TS_CHECK(I->alloc(&I->kp.p[i], M.m));
   if (gram)
-    for (int i = 0; i < t_max; ++i) TS_CHECK(ar.get(&B->kp.q[i], M.n));
-  TS_CHECK(ar.get(&B->x, M.n));
-  TS_CHECK(ar.get(&B->fr, M.m));
+    for (int i = 0; i < t_max; ++i) TS_CHECK(I->alloc(&I->kp.q[i], M.n));
+  TS_CHECK(I->alloc(&I->b, M.m));
+  TS_CHECK(I->alloc(&I->x, M.n));
+  TS_CHECK(I->alloc(&I->xs, M.n));
+  TS_CHECK(I->alloc(&I->fr, M.m));
   return 0;
 }
 
 // moments pairs for orders 1..npairs (predicated on state t); `solve_last`
 // makes the pair that equals the state's t run the Hankel solves
-static int cta_pairs(const Mat& M, SolveState* ds, const Work& wk, const CtaBuffers& B, int npairs,
-                     int gram, int solve_last, cudaStream_t s) {
+static int cta_pairs(const Mat& M, const Instance* I, int npairs, int gram, int solve_last,
+                     cudaStream_t s) {
   for (int i = 1; i <= npairs; ++i) {
     if (gram) {
       EpiCtaQ eq;
-      eq.st = ds; eq.q = B.kp.q[i - 1]; eq.i = i;
-      TS_CHECK(pass(M, 1, B.kp.p[i - 1], XS{}, eq, wk, s));
+      eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i;
+      TS_CHECK(pass(M, 1, I->kp.p[i - 1], XS{}, eq, I->wk, s));
       EpiCtaP ep;
-      ep.st = ds; ep.pprev = B.kp.p[i - 1]; ep.p = B.kp.p[i]; ep.i = i; ep.with_solve = solve_last;
-      TS_CHECK(pass(M, 0, B.kp.q[i - 1], XS{}, ep, wk, s));
+      ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
+      ep.with_solve = solve_last;
+      TS_CHECK(pass(M, 0, I->kp.q[i - 1], XS{}, ep, I->wk, s));
     } else {
       EpiCtaP ep;
-      ep.st = ds; ep.pprev = B.kp.p[i - 1]; ep.p = B.kp.p[i]; ep.i = i; ep.with_solve = solve_last;
-      TS_CHECK(pass(M, 0, B.kp.p[i - 1], XS{}, ep, wk, s));
+      ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
+      ep.with_solve = solve_last;
+      TS_CHECK(pass(M, 0, I->kp.p[i - 1], XS{}, ep, I->wk, s));
     }
   }
   return 0;
@@ -437,22 +547,26 @@ static int cta_pairs(const Mat& M, SolveState* ds, const Work& wk, const CtaBuff
 
 // one CTA step of at most `npairs` pairs: moments (+ Hankel in the last pair's
 // finisher), candidate norms / retry rule, fused r / x update (tail)
-static int cta_step_kernels(const Mat& M, SolveState* ds, const Work& wk, const CtaBuffers& B,
-                            int npairs, int gram, cudaStream_t s, cudaGraphConditionalHandle h,
-                            int use) {
-  TS_CHECK(cta_pairs(M, ds, wk, B, npairs, gram, 1, s));
+static int cta_step_kernels(const Mat& M, const Instance* I, int npairs, int gram, cudaStream_t s,
+                            cudaGraphConditionalHandle h, int use) {
+  TS_CHECK(cta_pairs(M, I, npairs, gram, 1, s));
   EpiCtaCand ecd;
-  ecd.st = ds; ecd.kp = B.kp; ecd.m = M.m;
-  TS_CHECK(vecpass(M, M.m, ecd, wk, s));
+  ecd.st = I->ds; ecd.kp = I->kp; ecd.m = M.m;
+  TS_CHECK(vecpass(M, M.m, ecd, I->wk, s));
   EpiCtaUpd eu;
-  eu.st = ds; eu.cond = h; eu.use_cond = use; eu.kp = B.kp; eu.x = B.x; eu.m = M.m; eu.n = M.n;
-  eu.gram = gram;
-  return vecpass(M, std::max(M.m, M.n), eu, wk, s);
+  eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = M.m;
+  eu.n = M.n; eu.gram = gram;
+  return vecpass(M, std::max(M.m, M.n), eu, I->wk, s);
 }
 
 static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double* x_out,
                      ts_trace_row* trace, int64_t trace_cap, ts_result* res, cudaStream_t st) {
-  SolveCtx c(M, st);
+  const int key[4] = {2, a.gram, a.t_max, 0};
+  InstanceLease lease(M);
+  TS_CHECK(acquire(M, key, [&](Instance* I) { return cta_alloc(I, M, a.t_max, a.gram); },
+                   &lease.I));
+  Instance* I = lease.I;
+  SolveCtx c(M, st, I);
   SolveState s0;
   memset(&s0, 0, sizeof(s0));
   s0.mode = MODE_CTA;
@@ -470,28 +584,25 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   s0.m_rows = M.m;
   s0.n_cols = M.n;
   s0.warm = 1;
-  TS_CHECK(c.init(s0, a.max_iters, trace, trace_cap));
-  Arena& ar = c.ar;
-  CtaBuffers B;
-  TS_CHECK(stage_in(ar, b_in, M.m, &B.b));
-  TS_CHECK(cta_alloc(ar, M, a.t_max, a.gram, &B));
-  SolveState* ds = c.ds;
-  const Work& wk = c.wk;
+  TS_CHECK(c.init(s0, trace, trace_cap));
+  SolveState* ds = I->ds;
+  const Work& wk = I->wk;
+  TS_CUDA(cudaMemcpyAsync(I->b, b_in, M.m * sizeof(double), cudaMemcpyDefault, st));
   if (a.x_start) {
-    TS_CHECK(stage_in(ar, a.x_start, M.n, &B.xs));
+    TS_CUDA(cudaMemcpyAsync(I->xs, a.x_start, M.n * sizeof(double), cudaMemcpyDefault, st));
     EpiCopyWarm ec;
-    ec.st = ds; ec.use_cond = 0; ec.src = B.xs; ec.dst = B.x;
+    ec.st = ds; ec.src = I->xs; ec.dst = I->x;
     TS_CHECK(vecpass(M, M.n, ec, wk, st));
     EpiCtaInitR ei;
-    ei.st = ds; ei.use_cond = 0; ei.b = B.b; ei.r = B.kp.p[0];
-    TS_CHECK(pass(M, 0, B.x, XS{}, ei, wk, st));
+    ei.st = ds; ei.b = I->b; ei.r = I->kp.p[0];
+    TS_CHECK(pass(M, 0, I->x, XS{}, ei, wk, st));
   } else {
     EpiCtaInit ei;
-    ei.st = ds; ei.use_cond = 0; ei.b = B.b; ei.r = B.kp.p[0]; ei.x = B.x; ei.m = M.m; ei.n = M.n;
+    ei.st = ds; ei.b = I->b; ei.r = I->kp.p[0]; ei.x = I->x; ei.m = M.m; ei.n = M.n;
     TS_CHECK(vecpass(M, std::max(M.m, M.n), ei, wk, st));
   }
   BodyFn body = [&](cudaStream_t s) -> int {
-    return cta_step_kernels(M, ds, wk, B, a.t_max, a.gram, s, 0, 0);
+    return cta_step_kernels(M, I, a.t_max, a.gram, s, 0, 0);
   };
   // graph body: [head: switch = t - 1] -> SWITCH{order 1 .. t_max}: each case
   // launches exactly its t pairs + candidate + update
@@ -507,29 +618,29 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     }));
     for (int k = 0; k < a.t_max; ++k)
       TS_CHECK(capture_into(cap, cases[k], [&](cudaStream_t s) -> int {
-        return cta_step_kernels(M, ds, wk, B, k + 1, a.gram, s, hw, 1);
+        return cta_step_kernels(M, I, k + 1, a.gram, s, hw, 1);
       }));
     return 0;
   };
   auto maint = [&](cudaStream_t s) -> int {
     EpiNormTo en;
-    en.st = ds; en.v = B.x; en.len = M.n; en.what = 1;
+    en.st = ds; en.v = I->x; en.len = M.n; en.what = 1;
     TS_CHECK(vecpass(M, M.n, en, wk, s));
     EpiCtaRecheck er;
-    er.st = ds; er.b = B.b; er.r = B.kp.p[0];
-    return pass(M, 0, B.x, XS{}, er, wk, s);
+    er.st = ds; er.b = I->b; er.r = I->kp.p[0];
+    return pass(M, 0, I->x, XS{}, er, wk, s);
   };
   TS_CHECK(c.run(body, gbody, maint));
   if (!c.hs->trivial) {
     EpiFinalR efr;
-    efr.st = ds; efr.use_cond = 0; efr.b = B.b; efr.fr = B.fr;
-    TS_CHECK(pass(M, 0, B.x, XS{}, efr, wk, st));
+    efr.st = ds; efr.b = I->b; efr.fr = I->fr;
+    TS_CHECK(pass(M, 0, I->x, XS{}, efr, wk, st));
     EpiFinalNR enr;
-    enr.st = ds; enr.use_cond = 0; enr.out = nullptr;
-    TS_CHECK(pass(M, 1, B.fr, XS{}, enr, wk, st));
+    enr.st = ds; enr.out = nullptr;
+    TS_CHECK(pass(M, 1, I->fr, XS{}, enr, wk, st));
   }
   TS_CHECK(c.read_state());
-  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, B.x, M.n * sizeof(double), cudaMemcpyDefault, st));
+  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, M.n * sizeof(double), cudaMemcpyDefault, st));
   fill_result(*c.hs, res);
   TS_CHECK(c.finish_timing(res));
   TS_CUDA(cudaStreamSynchronize(st));
@@ -679,35 +790,36 @@ int ts_hankel_min_norm(const double* phi, int32_t t, int32_t order, double rcond
 int ts_moments(const ts_matrix* A, int32_t h_mode, const double* r, int32_t t, double* phi,
                double* krylov, double* transposed, void* stream) {
   TS_CHECK_HANDLE(A);
-  if (t < 1 || t > kTMax || t > A->m) TS_INVAL("order t=%d outside 1..%lld", t, (long long)std::min<int64_t>(A->m, kTMax));
+  if (t < 1 || t > kTMax || t > A->m)
+    TS_INVAL("order t=%d outside 1..%lld", t, (long long)std::min<int64_t>(A->m, kTMax));
   if (h_mode == 1 && A->m != A->n) TS_INVAL("symmetric mode requires a square matrix");
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
   const int gram = h_mode == 0;
-  {
-    SolveCtx c(*A, st);
-    SolveState s0;
-    memset(&s0, 0, sizeof(s0));
-    s0.mode = MODE_CTA;
-    s0.t = t;
-    s0.gram = gram;
-    TS_CHECK(c.init(s0, 16, nullptr, 0));
-    CtaBuffers B;
-    TS_CHECK(cta_alloc(c.ar, *A, t, gram, &B));
-    TS_CUDA(cudaMemcpyAsync(B.kp.p[0], r, A->m * sizeof(double), cudaMemcpyDefault, st));
-    TS_CHECK(cta_pairs(*A, c.ds, c.wk, B, t, gram, 0, st));
-    TS_CHECK(c.read_state());
-    memcpy(phi, c.hs->phi, 2 * t * sizeof(double));
-    if (krylov)
-      for (int i = 0; i <= t; ++i)
-        TS_CUDA(cudaMemcpyAsync(krylov + (size_t)i * A->m, B.kp.p[i], A->m * sizeof(double),
-                                cudaMemcpyDefault, st));
-    if (transposed && gram)
-      for (int i = 0; i < t; ++i)
-        TS_CUDA(cudaMemcpyAsync(transposed + (size_t)i * A->n, B.kp.q[i], A->n * sizeof(double),
-                                cudaMemcpyDefault, st));
-    TS_CUDA(cudaStreamSynchronize(st));
-  }
+  const int key[4] = {3, gram, kTMax, 0};
+  InstanceLease lease(*A);
+  TS_CHECK(acquire(*A, key, [&](Instance* I) { return cta_alloc(I, *A, kTMax, gram); }, &lease.I));
+  Instance* I = lease.I;
+  SolveCtx c(*A, st, I);
+  SolveState s0;
+  memset(&s0, 0, sizeof(s0));
+  s0.mode = MODE_CTA;
+  s0.t = t;
+  s0.gram = gram;
+  TS_CHECK(c.init(s0, nullptr, 0));
+  TS_CUDA(cudaMemcpyAsync(I->kp.p[0], r, A->m * sizeof(double), cudaMemcpyDefault, st));
+  TS_CHECK(cta_pairs(*A, I, t, gram, 0, st));
+  TS_CHECK(c.read_state());
+  memcpy(phi, c.hs->phi, 2 * t * sizeof(double));
+  if (krylov)
+    for (int i = 0; i <= t; ++i)
+      TS_CUDA(cudaMemcpyAsync(krylov + (size_t)i * A->m, I->kp.p[i], A->m * sizeof(double),
+                              cudaMemcpyDefault, st));
+  if (transposed && gram)
+    for (int i = 0; i < t; ++i)
+      TS_CUDA(cudaMemcpyAsync(transposed + (size_t)i * A->n, I->kp.q[i], A->n * sizeof(double),
+                              cudaMemcpyDefault, st));
+  TS_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
 
@@ -715,50 +827,48 @@ int ts_cta_step(const ts_matrix* A, int32_t h_mode, const double* x, const doubl
                 double rcond, double* x_out, double* r_out, int32_t* order_out,
                 double* atr_norm_out, int32_t* status_out, void* stream) {
   TS_CHECK_HANDLE(A);
-  if (t < 1 || t > kTMax || t > A->m) TS_INVAL("order t=%d outside 1..%lld", t, (long long)std::min<int64_t>(A->m, kTMax));
+  if (t < 1 || t > kTMax || t > A->m)
+    TS_INVAL("order t=%d outside 1..%lld", t, (long long)std::min<int64_t>(A->m, kTMax));
   if (h_mode == 1 && A->m != A->n) TS_INVAL("symmetric mode requires a square matrix");
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
   const int gram = h_mode == 0;
-  {
-    SolveCtx c(*A, st);
-    SolveState s0;
-    memset(&s0, 0, sizeof(s0));
-    s0.mode = MODE_CTA;
-    s0.t = t;
-    s0.t_max = t;
-    s0.gram = gram;
-    s0.known_solvable = 1;
-    s0.max_iters = (long long)1 << 60;
-    s0.rcond = rcond;
-    s0.eps_abs = -1.0;
-    TS_CHECK(c.init(s0, 16, nullptr, 0));
-    CtaBuffers B;
-    TS_CHECK(cta_alloc(c.ar, *A, t, gram, &B));
-    TS_CUDA(cudaMemcpyAsync(B.kp.p[0], r, A->m * sizeof(double), cudaMemcpyDefault, st));
-    TS_CUDA(cudaMemcpyAsync(B.x, x, A->n * sizeof(double), cudaMemcpyDefault, st));
-    // r_norm for the monotone test
-    double* rn;
-    TS_CHECK(c.ar.get(&rn, 1));
-    EpiDot e{B.kp.p[0], B.kp.p[0], &c.ds->r_norm, 1};
-    TS_CHECK(vecpass(*A, A->m, e, c.wk, st));
-    TS_CHECK(cta_step_kernels(*A, c.ds, c.wk, B, t, gram, st, 0, 0));
-    TS_CHECK(c.read_state());
-    const int nestatus = (c.hs->status == TS_NORMAL_EQ_SOLUTION) ? TS_NORMAL_EQ_SOLUTION : 0;
-    if (c.hs->status == TS_NUMERICAL_FAILURE) {
-      set_error("moment solve failed: SVD did not converge in Linear Least Squares");
-      return TS_EINVAL;
-    }
-    if (status_out) *status_out = nestatus;
-    if (!nestatus) {
-      if (order_out) *order_out = c.hs->sel_order;
-      if (atr_norm_out) *atr_norm_out = c.hs->atr_norm;
-      if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, B.x, A->n * sizeof(double), cudaMemcpyDefault, st));
-      if (r_out)
-        TS_CUDA(cudaMemcpyAsync(r_out, B.kp.p[0], A->m * sizeof(double), cudaMemcpyDefault, st));
-    }
-    TS_CUDA(cudaStreamSynchronize(st));
+  const int key[4] = {3, gram, kTMax, 0};
+  InstanceLease lease(*A);
+  TS_CHECK(acquire(*A, key, [&](Instance* I) { return cta_alloc(I, *A, kTMax, gram); }, &lease.I));
+  Instance* I = lease.I;
+  SolveCtx c(*A, st, I);
+  SolveState s0;
+  memset(&s0, 0, sizeof(s0));
+  s0.mode = MODE_CTA;
+  s0.t = t;
+  s0.t_max = t;
+  s0.gram = gram;
+  s0.known_solvable = 1;
+  s0.max_iters = (long long)1 << 60;
+  s0.rcond = rcond;
+  s0.eps_abs = -1.0;
+  TS_CHECK(c.init(s0, nullptr, 0));
+  TS_CUDA(cudaMemcpyAsync(I->kp.p[0], r, A->m * sizeof(double), cudaMemcpyDefault, st));
+  TS_CUDA(cudaMemcpyAsync(I->x, x, A->n * sizeof(double), cudaMemcpyDefault, st));
+  EpiDot e{I->kp.p[0], I->kp.p[0], &I->ds->r_norm, 1};  // ||r|| for the monotone test
+  TS_CHECK(vecpass(*A, A->m, e, I->wk, st));
+  TS_CHECK(cta_step_kernels(*A, I, t, gram, st, 0, 0));
+  TS_CHECK(c.read_state());
+  if (c.hs->status == TS_NUMERICAL_FAILURE) {
+    set_error("moment solve failed: SVD did not converge in Linear Least Squares");
+    return TS_EINVAL;
   }
+  const int nestatus = (c.hs->status == TS_NORMAL_EQ_SOLUTION) ? TS_NORMAL_EQ_SOLUTION : 0;
+  if (status_out) *status_out = nestatus;
+  if (!nestatus) {
+    if (order_out) *order_out = c.hs->sel_order;
+    if (atr_norm_out) *atr_norm_out = c.hs->atr_norm;
+    if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, A->n * sizeof(double), cudaMemcpyDefault, st));
+    if (r_out)
+      TS_CUDA(cudaMemcpyAsync(r_out, I->kp.p[0], A->m * sizeof(double), cudaMemcpyDefault, st));
+  }
+  TS_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
 

@@ -271,6 +271,8 @@ int ts_device_count(int* count) {
 int ts_matrix_destroy(ts_matrix* A) {
   if (!A) return 0;
   DeviceGuard g(A->dev);
+  cudaDeviceSynchronize();
+  destroy_instances(A);
   void* ps[] = {A->a, A->rp, A->ci, A->val, A->rpT, A->ciT, A->valT, A->planN.wrow, A->planT.wrow};
   for (void* p : ps)
     if (p) cudaFree(p);

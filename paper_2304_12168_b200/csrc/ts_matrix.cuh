@@ -16,6 +16,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdlib>
+#include <mutex>
 
 #include "ts_passes.cuh"
 
@@ -28,6 +29,8 @@ struct RowPlan {
   int P = 1;            // blocks
   int* wrow = nullptr;  // device [P * kWarps] (PLAN_FLAT)
 };
+
+struct Instance;  // cached solver instance (ts_drivers.cuh)
 
 struct Mat {
   int dev = 0;
@@ -43,6 +46,9 @@ struct Mat {
   double fro = 0.0;
   RowPlan planN, planT;
   int Pmax = 0;  // largest grid any pass of this matrix uses
+  // solver instances (buffers + instantiated graphs) cached per solver shape
+  std::mutex cache_mu;
+  std::vector<Instance*> cache;
 
   DenseRows dense() const { return DenseRows{a, lda, m, n}; }
   CsrRows csr() const { return CsrRows{rp, ci, val, m, nnz}; }
@@ -84,6 +90,7 @@ inline int64_t first_row_at(const int* rp, int64_t rows, int64_t s) {
 int plan_rows_csr(const int* rp_host, int64_t rows, int64_t nnz, int sms, RowPlan* out,
                   cudaStream_t st);
 int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t st);
+void destroy_instances(Mat* M);
 
 inline int vec_grid(int64_t len, int sms) {
   int64_t g = (len + kNT * 4 - 1) / (kNT * 4);
