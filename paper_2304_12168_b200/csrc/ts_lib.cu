@@ -118,8 +118,11 @@ int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* ou
   const int64_t pmax = resident_blocks(sms);
   const bool long_rows = rows > 0 && nnz / rows >= 32 && nnz >= (int64_t)kWarps * 256;
   if (!long_rows) {
-    p.kind = PLAN_SHORT;
-    int64_t g = (rows + kNT - 1) / kNT;
+    // warp-cooperative short rows (TS_CSR_SHORT=thread selects the
+    // thread-per-row kernel, kept for comparison)
+    static const bool thread_rows = getenv("TS_CSR_SHORT") && !strcmp(getenv("TS_CSR_SHORT"), "thread");
+    p.kind = thread_rows ? PLAN_SHORT : PLAN_WARP;
+    int64_t g = thread_rows ? (rows + kNT - 1) / kNT : (rows + kNT * 4 - 1) / (kNT * 4);
     p.P = (int)std::max<int64_t>(1, std::min(g, pmax));
     *out = p;
     return 0;

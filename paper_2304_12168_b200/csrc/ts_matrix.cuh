@@ -22,7 +22,7 @@
 
 namespace ts {
 
-enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2 };
+enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3 };
 
 struct RowPlan {
   int kind = PLAN_SHORT;
@@ -130,6 +130,8 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
     const CsrRows acc = trans ? M.csrT() : M.csr();
     if (pl.kind == PLAN_FLAT)
       k_rows_flat<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk, pl.wrow);
+    else if (pl.kind == PLAN_WARP)
+      k_rows_warp<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
     else
       k_rows_short<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
   }
