@@ -120,7 +120,13 @@ int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* ou
   if (!long_rows) {
     // warp-cooperative short rows (TS_CSR_SHORT=thread selects the
     // thread-per-row kernel, kept for comparison)
-    static const bool thread_rows = getenv("TS_CSR_SHORT") && !strcmp(getenv("TS_CSR_SHORT"), "thread");
+    // thread-per-row for small (L2-resident, latency-bound) matrices, the
+    // coalesced warp-cooperative kernel once the pass is HBM-bound.
+    // TS_CSR_SHORT=thread|warp forces one (kernel comparisons).
+    const char* force = getenv("TS_CSR_SHORT");
+    bool thread_rows = nnz < ((int64_t)1 << 21);
+    if (force && !strcmp(force, "thread")) thread_rows = true;
+    if (force && !strcmp(force, "warp")) thread_rows = false;
     p.kind = thread_rows ? PLAN_SHORT : PLAN_WARP;
     int64_t g = thread_rows ? (rows + kNT - 1) / kNT : (rows + kNT * 4 - 1) / (kNT * 4);
     p.P = (int)std::max<int64_t>(1, std::min(g, pmax));

@@ -126,15 +126,23 @@ struct CsrRows {
                                         const XS& xs, int lane) const {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int64_t k = k0 + lane;
-    for (; k + 96 < k1; k += 128) {
-      double v0 = ld_stream(val + k), v1 = ld_stream(val + k + 32);
-      double v2 = ld_stream(val + k + 64), v3 = ld_stream(val + k + 96);
-      int j0 = ld_stream_i(ci + k), j1 = ld_stream_i(ci + k + 32);
-      int j2 = ld_stream_i(ci + k + 64), j3 = ld_stream_i(ci + k + 96);
-      a0 = fma(v0, xs(__ldg(x + j0)), a0);
-      a1 = fma(v1, xs(__ldg(x + j1)), a1);
-      a2 = fma(v2, xs(__ldg(x + j2)), a2);
-      a3 = fma(v3, xs(__ldg(x + j3)), a3);
+    for (; k + 224 < k1; k += 256) {
+      double v[8], xv[8];
+      int j[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = ld_stream(val + k + 32 * u);
+        j[u] = ld_stream_i(ci + k + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = __ldg(x + j[u]);
+#pragma unroll
+      for (int u = 0; u < 8; u += 4) {
+        a0 = fma(v[u], xs(xv[u]), a0);
+        a1 = fma(v[u + 1], xs(xv[u + 1]), a1);
+        a2 = fma(v[u + 2], xs(xv[u + 2]), a2);
+        a3 = fma(v[u + 3], xs(xv[u + 3]), a3);
+      }
     }
     for (; k < k1; k += 32) a0 = fma(ld_stream(val + k), xs(__ldg(x + ld_stream_i(ci + k))), a0);
     return (a0 + a1) + (a2 + a3);
@@ -143,7 +151,21 @@ struct CsrRows {
   __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
     const int k0 = __ldg(rp + r), k1 = __ldg(rp + r + 1);
     double s = 0.0;
-    for (int k = k0; k < k1; ++k)
+    int k = k0;
+    for (; k + 4 <= k1; k += 4) {
+      double v[4], xv[4];
+      int j[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u] = ld_stream(val + k + u);
+        j[u] = ld_stream_i(ci + k + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = __ldg(x + j[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s = __dadd_rn(s, __dmul_rn(v[u], xs(xv[u])));
+    }
+    for (; k < k1; ++k)
       s = __dadd_rn(s, __dmul_rn(ld_stream(val + k), xs(__ldg(x + ld_stream_i(ci + k)))));
     return s;
   }
@@ -345,7 +367,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const dou
 // lane then adds ITS row's products left to right without FMA — the same
 // operation sequence as scipy's csr_matvec, so the result is bitwise the
 // reference's, with coalesced HBM traffic instead of per-thread strided rows.
-constexpr int kWCh = 128;  // products staged per warp per chunk
+constexpr int kWCh = 256;  // products staged per warp per chunk
 
 template <class Epi>
 __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const double* __restrict__ x,
@@ -381,13 +403,20 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
     const int ge = __ldg(A.rp + rlast);
     double sum = 0.0;
     for (int cs = gb; cs < ge; cs += kWCh) {
+      constexpr int J = kWCh / 32;
+      double vv[J], xv[J];
+      int cc[J];
 #pragma unroll
-      for (int j = 0; j < kWCh / 32; ++j) {
+      for (int j = 0; j < J; ++j) {  // independent loads first ...
         const int k = cs + j * 32 + lane;
-        double prod = 0.0;
-        if (k < ge) prod = __dmul_rn(ld_stream(A.val + k), xs(__ldg(x + ld_stream_i(A.ci + k))));
-        sb[j * 32 + lane] = prod;
+        const bool ok = k < ge;
+        vv[j] = ok ? ld_stream(A.val + k) : 0.0;
+        cc[j] = ok ? ld_stream_i(A.ci + k) : 0;
       }
+#pragma unroll
+      for (int j = 0; j < J; ++j) xv[j] = __ldg(x + cc[j]);  // ... then the gathers
+#pragma unroll
+      for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xs(xv[j]));
       __syncwarp();
       const int lo = kb > cs ? kb : cs;
       const int hi = ke < cs + kWCh ? ke : cs + kWCh;
