@@ -179,10 +179,6 @@ def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResul
         raise ValueError("symmetric mode requires a square matrix")
     if opts.t_max > DEVICE_T_MAX:
         raise ValueError(f"t_max={opts.t_max} exceeds the device limit {DEVICE_T_MAX}")
-    if opts.enhanced and not opts.known_solvable:
-        raise NotImplementedError(
-            "CenteringOptions(enhanced=True) (first_order_probe) is not implemented on the "
-            "device path yet")
     dm, gram = as_device_matrix(a)
     if gram:
         raise TypeError("centering_solve on a GramProduct operator is not supported on the device")

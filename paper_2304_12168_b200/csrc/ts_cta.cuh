@@ -237,6 +237,10 @@ struct EpiCtaP : EpiBase {
         return;
       }
       st->atr_norm = st->gram ? sqrt(st->atr2) : sqrt(st->phi[1]);
+      // enhanced probe: first step uses phi_1 = r.Hr, phi_2 = Hr.Hr (centering.py:241-245)
+      st->probe_hit = 0;
+      st->probe_done = !(st->enhanced && st->t >= 2);
+      if (!st->probe_done) st->probe_alpha = st->phi[0] / st->phi[1];
     }
   }
   // the last pass of the moments runs the order-1..t Hankel solves, one
@@ -378,12 +382,119 @@ struct EpiCtaUpd : EpiBase {
     SolveState* s = st;
     s->iterations += 1;
     s->r_norm = sqrt(red[0]);
-    if (s->recheck_every > 0 && (s->iterations % s->recheck_every) == 0) {
+    if (s->enhanced && s->probe_hit) {
+      s->maint = MAINT_PROBE;  // centering.py:335-343, finished by the host-driven passes
+    } else if (s->recheck_every > 0 && (s->iterations % s->recheck_every) == 0) {
       s->maint = MAINT_RECHECK;
     } else {
       cta_head(s);
     }
     tail();
+  }
+};
+
+// ---- enhanced probe (first_order_probe, centering.py:227-251) ------------
+struct ProbePtrs {
+  double *y, *hy, *aty, *xh, *fr2;
+};
+__device__ __forceinline__ bool probe_on(const SolveState* s, int j) {
+  return s->status == TS_RUNNING && s->maint == MAINT_NONE && !s->probe_done && j < s->t;
+}
+// x_hat += alpha (A^T y | y);  y = y - alpha H y     (step j)
+struct EpiProbeUpd : EpiBase {
+  static constexpr int K = 1;
+  KrylovPtrs kp;
+  ProbePtrs pp;
+  const double* x;
+  int64_t m, n;
+  int gram, j;
+  __device__ bool active() const { return probe_on(st, j); }
+  __device__ void elem(int64_t i, double (&)[K]) const {
+    const double al = st->probe_alpha;
+    double yo = 0.0;
+    if (i < m) yo = (j == 1) ? kp.p[0][i] : pp.y[i];
+    if (i < n) {
+      const double xo = (j == 1) ? x[i] : pp.xh[i];
+      const double dir = gram ? ((j == 1) ? kp.q[0][i] : pp.aty[i]) : yo;
+      pp.xh[i] = __dadd_rn(xo, __dmul_rn(al, dir));
+    }
+    if (i < m) {
+      const double hr = (j == 1) ? kp.p[1][i] : pp.hy[i];
+      pp.y[i] = __dsub_rn(yo, __dmul_rn(al, hr));
+    }
+  }
+  __device__ void finish(double (&)[K]) const {}
+};
+// Gram mode: aty = A^T y
+struct EpiProbeT : EpiBase {
+  static constexpr int K = 1;
+  double* aty;
+  int j;
+  __device__ bool active() const { return probe_on(st, j); }
+  __device__ void elem(int64_t i, double v, double (&)[K]) const { aty[i] = v; }
+  __device__ void finish(double (&)[K]) const {}
+};
+// hy = H y; hit test |y.Hy| <= eps_abs^2, else next alpha = y.Hy / Hy.Hy
+struct EpiProbeN : EpiBase {
+  static constexpr int K = 2;
+  const double* y;
+  double* hy;
+  int j;
+  __device__ bool active() const { return probe_on(st, j); }
+  __device__ void elem(int64_t r, double v, double (&acc)[K]) const {
+    hy[r] = v;
+    acc[0] = fma(y[r], v, acc[0]);
+    acc[1] = fma(v, v, acc[1]);
+  }
+  __device__ void finish(double (&red)[K]) const {
+    SolveState* s = st;
+    if (fabs(red[0]) <= s->quad) {
+      s->probe_hit = j;
+      s->probe_done = 1;
+    } else if (j + 1 >= s->t || red[1] == 0.0) {
+      s->probe_done = 1;  // orbit exhausted / terminated without triggering
+    } else {
+      s->probe_alpha = red[0] / red[1];
+    }
+  }
+};
+// post-step comparison: ||A^T (b - A x)|| vs ||A^T (b - A x_hat)||
+struct EpiProbeR : EpiBase {  // fr = b - A v
+  static constexpr int K = 1;
+  const double* b;
+  double* fr;
+  __device__ bool active() const { return true; }
+  __device__ void elem(int64_t i, double y, double (&)[K]) const { fr[i] = __dsub_rn(b[i], y); }
+  __device__ void finish(double (&)[K]) const {}
+};
+struct EpiProbeNR : EpiBase {  // ||A^T fr||
+  static constexpr int K = 1;
+  int which;  // 0 stepped, 1 refined
+  __device__ bool active() const { return true; }
+  __device__ void elem(int64_t, double y, double (&acc)[K]) const { acc[0] = fma(y, y, acc[0]); }
+  __device__ void finish(double (&red)[K]) const {
+    if (which == 0) {
+      st->probe_stepped = sqrt(red[0]);
+    } else {
+      st->probe_refined = sqrt(red[0]);
+      st->probe_take = st->probe_refined < st->probe_stepped;
+    }
+  }
+};
+struct EpiProbeTake : EpiBase {  // x = x_hat; r = b - A x_hat (when refined wins)
+  static constexpr int K = 1;
+  const double *xh, *fr2;
+  double *x, *r;
+  int64_t m, n;
+  __device__ bool active() const { return true; }
+  __device__ void elem(int64_t i, double (&)[K]) const {
+    if (!st->probe_take) return;
+    if (i < n) x[i] = xh[i];
+    if (i < m) r[i] = fr2[i];
+  }
+  __device__ void finish(double (&)[K]) const {
+    st->maint = MAINT_NONE;
+    st->status = TS_NORMAL_EQ_SOLUTION;
   }
 };
 

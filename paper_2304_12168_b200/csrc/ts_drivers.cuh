@@ -101,6 +101,7 @@ struct Instance {
   // CTA vectors
   double *xs = nullptr;
   KrylovPtrs kp;
+  ProbePtrs pp = {nullptr, nullptr, nullptr, nullptr, nullptr};
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -508,9 +509,10 @@ struct CtaArgs {
   int accel_patience = 3;
   double accel_ratio = 0.95;
   const double* x_start = nullptr;
+  int enhanced = 0;
 };
 
-static int cta_alloc(Instance* I, const Mat& M, int t_max, int gram) {
+static int cta_alloc(Instance* I, const Mat& M, int t_max, int gram, int enhanced = 0) {
   memset(&I->kp, 0, sizeof(I->kp));
   for (int i = 0; i <= t_max; ++i) TS_CHECK(I->alloc(&I->kp.p[i], M.m));
   if (gram)
@@ -519,7 +521,55 @@ static int cta_alloc(Instance* I, const Mat& M, int t_max, int gram) {
   TS_CHECK(I->alloc(&I->x, M.n));
   TS_CHECK(I->alloc(&I->xs, M.n));
   TS_CHECK(I->alloc(&I->fr, M.m));
+  if (enhanced) {
+    TS_CHECK(I->alloc(&I->pp.y, M.m));
+    TS_CHECK(I->alloc(&I->pp.hy, M.m));
+    TS_CHECK(I->alloc(&I->pp.aty, M.n));
+    TS_CHECK(I->alloc(&I->pp.xh, M.n));
+    TS_CHECK(I->alloc(&I->pp.fr2, M.m));
+  }
   return 0;
+}
+
+// enhanced probe steps 1..npairs-1 (centering.py:240-250), after the moments
+static int cta_probe_kernels(const Mat& M, const Instance* I, int npairs, int gram, cudaStream_t s) {
+  for (int j = 1; j < npairs; ++j) {
+    EpiProbeUpd eu;
+    eu.st = I->ds; eu.kp = I->kp; eu.pp = I->pp; eu.x = I->x; eu.m = M.m; eu.n = M.n;
+    eu.gram = gram; eu.j = j;
+    TS_CHECK(vecpass(M, std::max(M.m, M.n), eu, I->wk, s));
+    EpiProbeN en;
+    en.st = I->ds; en.y = I->pp.y; en.hy = I->pp.hy; en.j = j;
+    if (gram) {
+      EpiProbeT et;
+      et.st = I->ds; et.aty = I->pp.aty; et.j = j;
+      TS_CHECK(pass(M, 1, I->pp.y, XS{}, et, I->wk, s));
+      TS_CHECK(pass(M, 0, I->pp.aty, XS{}, en, I->wk, s));
+    } else {
+      TS_CHECK(pass(M, 0, I->pp.y, XS{}, en, I->wk, s));
+    }
+  }
+  return 0;
+}
+
+// stepped vs refined normal residual, adopt x_hat if it wins (centering.py:335-343)
+static int cta_probe_finish(const Mat& M, const Instance* I, cudaStream_t s) {
+  EpiProbeR r1;
+  r1.st = I->ds; r1.b = I->b; r1.fr = I->fr;
+  TS_CHECK(pass(M, 0, I->x, XS{}, r1, I->wk, s));
+  EpiProbeNR n1;
+  n1.st = I->ds; n1.which = 0;
+  TS_CHECK(pass(M, 1, I->fr, XS{}, n1, I->wk, s));
+  EpiProbeR r2;
+  r2.st = I->ds; r2.b = I->b; r2.fr = I->pp.fr2;
+  TS_CHECK(pass(M, 0, I->pp.xh, XS{}, r2, I->wk, s));
+  EpiProbeNR n2;
+  n2.st = I->ds; n2.which = 1;
+  TS_CHECK(pass(M, 1, I->pp.fr2, XS{}, n2, I->wk, s));
+  EpiProbeTake et;
+  et.st = I->ds; et.xh = I->pp.xh; et.fr2 = I->pp.fr2; et.x = I->x; et.r = I->kp.p[0];
+  et.m = M.m; et.n = M.n;
+  return vecpass(M, std::max(M.m, M.n), et, I->wk, s);
 }
 
 // moments pairs for orders 1..npairs (predicated on state t); `solve_last`
@@ -548,8 +598,9 @@ static int cta_pairs(const Mat& M, const Instance* I, int npairs, int gram, int 
 // one CTA step of at most `npairs` pairs: moments (+ Hankel in the last pair's
 // finisher), candidate norms / retry rule, fused r / x update (tail)
 static int cta_step_kernels(const Mat& M, const Instance* I, int npairs, int gram, cudaStream_t s,
-                            cudaGraphConditionalHandle h, int use) {
+                            cudaGraphConditionalHandle h, int use, int enhanced = 0) {
   TS_CHECK(cta_pairs(M, I, npairs, gram, 1, s));
+  if (enhanced) TS_CHECK(cta_probe_kernels(M, I, npairs, gram, s));
   EpiCtaCand ecd;
   ecd.st = I->ds; ecd.kp = I->kp; ecd.m = M.m;
   TS_CHECK(vecpass(M, M.m, ecd, I->wk, s));
@@ -561,9 +612,9 @@ static int cta_step_kernels(const Mat& M, const Instance* I, int npairs, int gra
 
 static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double* x_out,
                      ts_trace_row* trace, int64_t trace_cap, ts_result* res, cudaStream_t st) {
-  const int key[4] = {2, a.gram, a.t_max, 0};
+  const int key[4] = {2, a.gram, a.t_max, a.enhanced};
   InstanceLease lease(M);
-  TS_CHECK(acquire(M, key, [&](Instance* I) { return cta_alloc(I, M, a.t_max, a.gram); },
+  TS_CHECK(acquire(M, key, [&](Instance* I) { return cta_alloc(I, M, a.t_max, a.gram, a.enhanced); },
                    &lease.I));
   Instance* I = lease.I;
   SolveCtx c(M, st, I);
@@ -584,6 +635,8 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   s0.m_rows = M.m;
   s0.n_cols = M.n;
   s0.warm = 1;
+  s0.enhanced = a.enhanced;
+  s0.probe_done = 1;
   TS_CHECK(c.init(s0, trace, trace_cap));
   SolveState* ds = I->ds;
   const Work& wk = I->wk;
@@ -602,7 +655,7 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     TS_CHECK(vecpass(M, std::max(M.m, M.n), ei, wk, st));
   }
   BodyFn body = [&](cudaStream_t s) -> int {
-    return cta_step_kernels(M, I, a.t_max, a.gram, s, 0, 0);
+    return cta_step_kernels(M, I, a.t_max, a.gram, s, 0, 0, a.enhanced);
   };
   // graph body: [head: switch = t - 1] -> SWITCH{order 1 .. t_max}: each case
   // launches exactly its t pairs + candidate + update
@@ -618,11 +671,12 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     }));
     for (int k = 0; k < a.t_max; ++k)
       TS_CHECK(capture_into(cap, cases[k], [&](cudaStream_t s) -> int {
-        return cta_step_kernels(M, I, k + 1, a.gram, s, hw, 1);
+        return cta_step_kernels(M, I, k + 1, a.gram, s, hw, 1, a.enhanced);
       }));
     return 0;
   };
   auto maint = [&](cudaStream_t s) -> int {
+    if (c.hs->maint == MAINT_PROBE) return cta_probe_finish(M, I, s);
     EpiNormTo en;
     en.st = ds; en.v = I->x; en.len = M.n; en.what = 1;
     TS_CHECK(vecpass(M, M.n, en, wk, s));
@@ -912,8 +966,6 @@ int ts_cta_solve(const ts_matrix* A, const double* b, const ts_cta_options* o, d
   if (!(o->epsilon > 0.0 && o->epsilon < 1.0)) TS_INVAL("epsilon must lie in (0, 1)");
   if (o->t_max < 1) TS_INVAL("t_max must be at least 1");
   if (o->h_mode != 0 && o->h_mode != 1) TS_INVAL("unknown h_mode");
-  if (o->enhanced && !o->known_solvable)
-    TS_INVAL("enhanced probe (first_order_probe) is not implemented on the device path");
   int t_max = (int)std::min<int64_t>(o->t_max, A->m);
   if (t_max > kTMax) TS_INVAL("t_max=%d exceeds the device limit %d", t_max, kTMax);
   if (o->h_mode == 1 && A->m != A->n) TS_INVAL("symmetric mode requires a square matrix");
@@ -931,6 +983,7 @@ int ts_cta_solve(const ts_matrix* A, const double* b, const ts_cta_options* o, d
   a.accel_patience = o->accel_patience;
   a.accel_ratio = o->accel_ratio;
   a.x_start = o->x_start;
+  a.enhanced = (o->enhanced && !o->known_solvable) ? 1 : 0;  // centering.py:306
   return cta_solve(*A, b, a, x_out, trace, trace_cap, res, (cudaStream_t)stream);
 }
 

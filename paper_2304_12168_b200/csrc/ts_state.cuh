@@ -20,7 +20,7 @@ namespace ts {
 
 enum Mode : int { MODE_ADAPTIVE = 0, MODE_BALL = 1, MODE_LP = 2, MODE_CTA = 3 };
 enum Event : int { EV_NONE = 0, EV_PIVOT = 1, EV_EXPAND = 2 };
-enum Maint : int { MAINT_NONE = 0, MAINT_REVALIDATE = 1, MAINT_RECHECK = 2 };
+enum Maint : int { MAINT_NONE = 0, MAINT_REVALIDATE = 1, MAINT_RECHECK = 2, MAINT_PROBE = 3 };
 
 struct alignas(16) SolveState {
   // control
@@ -41,6 +41,9 @@ struct alignas(16) SolveState {
   // CTA
   double epsilon, eps_abs, quad, r_norm, atr_norm, atr2;
   double a_fro, x_norm, ratio, w_blend, accel_ratio, rcond;
+  // enhanced probe (first_order_probe, centering.py:227-251)
+  int probe_hit, probe_done, probe_take, pad1;
+  double probe_alpha, probe_stepped, probe_refined;
   double phi[2 * kTMax];
   double alpha_o[kTMax][kTMax];
   double cand[kTMax];

@@ -43,6 +43,14 @@ def _inball(seed):
     return a, b
 
 
+def _probe_case(seed):
+    # inconsistent systems on which the enhanced first-order probe triggers
+    rng = np.random.default_rng(seed)
+    m = int(rng.integers(10, 40))
+    n = int(rng.integers(3, m))
+    return rng.standard_normal((m, n)), rng.standard_normal(m)
+
+
 def _c(w):
     return (w.a, w.b)
 
@@ -68,6 +76,8 @@ CASES = [
      "cta", dict(epsilon=1e-10, h_mode="a", t_max=1, max_iters=20000, accelerate=True)),
     ("cta_enhanced", lambda: (lambda r: (r.standard_normal((8, 3)), r.standard_normal(8)))(
         np.random.default_rng(12)), "cta", dict(epsilon=1e-9, enhanced=True)),
+    ("cta_enhanced_probe31", lambda: _probe_case(31), "cta", dict(epsilon=1e-9, enhanced=True)),
+    ("cta_enhanced_probe38", lambda: _probe_case(38), "cta", dict(epsilon=1e-9, enhanced=True)),
     ("cta_known_solvable", lambda: (_poisson2d(8), _poisson2d(8).sum(axis=1)), "cta",
      dict(epsilon=1e-13, h_mode="a", known_solvable=True)),
     ("cta_rank1_ne", lambda: (np.outer([1.0, 0.0], [1.0, 1.0]), np.array([0.0, 1.0])), "cta",

@@ -52,8 +52,6 @@ def run_device(g: Golden):
 @pytest.mark.parametrize("name", golden_names())
 def test_golden_parity(name):
     g = Golden(name)
-    if g.solver == "cta" and g.kwargs.get("enhanced"):
-        pytest.skip("enhanced probe not implemented on the device path yet")
     res = run_device(g)
     assert res.status == g.status, (res, g.status, g.detail, res.detail)
     bn = float(np.linalg.norm(g.b))
