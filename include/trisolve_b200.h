@@ -47,6 +47,7 @@ extern "C" {
 #define TS_ABI_VERSION 1
 
 typedef struct ts_matrix ts_matrix; /* opaque; immutable after creation */
+typedef struct ts_comm ts_comm;     /* column-sharding communicator (one per rank) */
 
 /* ---- return codes -------------------------------------------------------- */
 enum {
@@ -213,6 +214,22 @@ TS_API int ts_cta_step(const ts_matrix* a, int32_t h_mode, const double* x, cons
  * device-resident vectors: average milliseconds per launch (kernel tuning and
  * the bench's cross-check of the in-solve kernel timers). */
 TS_API int ts_time_pass(const ts_matrix* a, int32_t trans, int32_t reps, double* avg_ms, void* stream);
+
+/* ---- column sharding over NVLink (BASELINE north_star) ---------
+ * One process per GPU.  Each rank creates a communicator, exports 128 bytes of
+ * IPC handles, all-gathers them (e.g. torch.distributed), connects, and
+ * attaches it to its column block A_p = A[:, off:off+n_p] (a normal matrix
+ * handle).  Solves on the attached handle then exchange one fixed-rank-order
+ * all-reduce of the m-vector A_p v_p per A-pass (fused into the pass
+ * epilogue, deterministic, identical on every rank) and one scalar
+ * all-reduce per n-space reduction.  b, b', r, gap, Krylov vectors are
+ * replicated; x, x0, x_start, c are the rank's LOCAL column slice. */
+TS_API int ts_comm_create(int device, int rank, int world, int64_t vec_capacity, ts_comm** out,
+                          void* ipc_handles_out /* 128 bytes */);
+TS_API int ts_comm_connect(ts_comm* comm, const void* all_handles /* world x 128 bytes */);
+TS_API int ts_comm_destroy(ts_comm* comm);
+TS_API int ts_matrix_set_shard(ts_matrix* a, ts_comm* comm, int64_t n_global, int64_t col_offset,
+                               double frobenius_global);
 
 /* ---- solvers --------------------------------------------------------------- */
 TS_API int ts_cta_solve(const ts_matrix* a, const double* b, const ts_cta_options* opts, double* x_out,

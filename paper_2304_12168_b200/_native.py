@@ -22,6 +22,7 @@ EXPORTS = (
     "ts_matvec", "ts_rmatvec", "ts_gram_matvec", "ts_norm2", "ts_dot",
     "ts_moments", "ts_hankel_min_norm", "ts_cta_step", "ts_time_pass",
     "ts_cta_solve", "ts_ta_adaptive", "ts_ta_in_ball", "ts_lp_feasibility",
+    "ts_comm_create", "ts_comm_connect", "ts_comm_destroy", "ts_matrix_set_shard",
 )
 
 # statuses (results.py:11-18)
@@ -110,6 +111,10 @@ def _declare(lib):
         "ts_cta_step": ([_P, _I32, _P, _P, _I32, _D, _P, _P, C.POINTER(_I32), C.POINTER(_D),
                          C.POINTER(_I32), _P], C.c_int),
         "ts_time_pass": ([_P, _I32, _I32, C.POINTER(_D), _P], C.c_int),
+        "ts_comm_create": ([C.c_int, C.c_int, C.c_int, _I64, C.POINTER(_P), _P], C.c_int),
+        "ts_comm_connect": ([_P, _P], C.c_int),
+        "ts_comm_destroy": ([_P], C.c_int),
+        "ts_matrix_set_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
         "ts_cta_solve": ([_P, _P, C.POINTER(CtaOptions), _P, _P, _I64, C.POINTER(Result), _P],
                          C.c_int),
         "ts_ta_adaptive": ([_P, _P, C.POINTER(TaOptions), _P, _P, _I64, C.POINTER(Result), _P],

@@ -23,6 +23,7 @@ from .linalg import (
     H_MODE_SYMMETRIC,
     HOperator,
     as_device_matrix,
+    local_slice,
     norm2,
     shape_of,
 )
@@ -182,9 +183,10 @@ def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResul
     dm, gram = as_device_matrix(a)
     if gram:
         raise TypeError("centering_solve on a GramProduct operator is not supported on the device")
+    n_local = dm.shape[1]  # == n unless `a` is a column-sharded ShardedMatrix
     x_start = None
     if opts.start == "random":
-        x_start = np.random.default_rng(opts.start_seed).standard_normal(n)
+        x_start = local_slice(a, np.random.default_rng(opts.start_seed).standard_normal(n), n_local)
     o = N.CtaOptions()
     o.epsilon = float(opts.epsilon)
     o.t_max = int(opts.t_max)
@@ -199,11 +201,11 @@ def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResul
     o.accel_ratio = float(opts.accel_ratio)
     o.x_start = x_start.ctypes.data if x_start is not None else None
     buf, cap = trace_buffer(opts.max_iters)
-    x = np.empty(n)
+    x = np.empty(n_local)
     res = N.Result()
     N.check(N.lib().ts_cta_solve(dm.handle, N.ptr(b), C.byref(o), x.ctypes.data,
                                  buf.ctypes.data, cap, C.byref(res), None))
     trace = rows_to_trace("cta", buf, res.trace_rows, CENTERING_TRACE_COLUMNS)
     if res.trivial:
-        return SolveResult(APPROX_SOLUTION, np.zeros(n), 0.0, 0.0, 0, trace)
+        return SolveResult(APPROX_SOLUTION, np.zeros(n_local), 0.0, 0.0, 0, trace)
     return build_result("cta", res, x, trace)

@@ -56,29 +56,56 @@ static SolveState* pinned_state() {
   return hs;
 }
 
-// count every launch we enqueue
+// count every launch we enqueue; on a column-sharded matrix, A v becomes
+// [local partial -> symmetric buffer] + [k_ar_vec with the epilogue] and A^T v
+// becomes [local pass, finisher deferred] + [k_ar_scalars]
+inline int ar_grid(int64_t len, int sms) {
+  int64_t g = (len + kNT * 4 - 1) / (kNT * 4);
+  const int64_t cap = (int64_t)sms * 2;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+template <int K>
+constexpr unsigned all_slots() { return (K >= 32) ? ~0u : ((1u << K) - 1u); }
+
 template <class Epi>
 static int pass(const Mat& M, int trans, const double* x, XS xs, const Epi& e, const Work& w,
                 cudaStream_t s) {
   ++g_launches;
-  if constexpr (std::is_base_of<EpiBase, Epi>::value) {
-    Epi e2 = e;
-    e2.tclass = trans ? 1 : 0;
-    return launch_pass(M, trans, x, xs, e2, w, s);
+  Epi e2 = e;
+  if constexpr (std::is_base_of<EpiBase, Epi>::value) e2.tclass = trans ? 1 : 0;
+  if (!M.comm) return launch_pass(M, trans, x, xs, e2, w, s);
+  const CommDev cd = M.comm->dev_view();
+  ++g_launches;
+  if (!trans) {
+    if (M.m > (int64_t)cd.vec_cap) TS_INVAL("communicator vector capacity too small");
+    EpiSymStore<Epi> ps{e2, cd};
+    TS_CHECK(launch_pass(M, 0, x, xs, ps, w, s));
+    k_ar_vec<Epi><<<ar_grid(M.m, M.sms), kNT, 0, s>>>(M.m, e2, w, cd);
   } else {
-    return launch_pass(M, trans, x, xs, e, w, s);
+    EpiDefer<Epi> d{e2, cd};
+    TS_CHECK(launch_pass(M, 1, x, xs, d, w, s));
+    k_ar_scalars<Epi><<<1, kNT, 0, s>>>(e2, cd, all_slots<Epi::K>());
   }
+  TS_CUDA(cudaGetLastError());
+  return 0;
 }
 template <class Epi>
 static int vecpass(const Mat& M, int64_t len, const Epi& e, const Work& w, cudaStream_t s) {
   ++g_launches;
+  Epi e2 = e;
+  unsigned mask = 0;
   if constexpr (std::is_base_of<EpiBase, Epi>::value) {
-    Epi e2 = e;
     e2.tclass = 2;
-    return launch_vec(len, M.sms, e2, w, s);
-  } else {
-    return launch_vec(len, M.sms, e, w, s);
+    mask = Epi::kShardMask;
   }
+  if (!M.comm || !mask) return launch_vec(len, M.sms, e2, w, s);
+  const CommDev cd = M.comm->dev_view();
+  ++g_launches;
+  EpiDefer<Epi> d{e2, cd};
+  TS_CHECK(launch_vec(len, M.sms, d, w, s));
+  k_ar_scalars<Epi><<<1, kNT, 0, s>>>(e2, cd, mask);
+  TS_CUDA(cudaGetLastError());
+  return 0;
 }
 
 // ----------------------------------------------------------- instances ----
@@ -436,7 +463,7 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
   s0.halvings_left = std::max(0, a.halvings);
   s0.a_fro = a.gram ? M.fro * M.fro : M.fro;
   s0.m_rows = mo;
-  s0.n_cols = no;
+  s0.n_cols = M.comm ? M.n_global : no;
   TS_CHECK(c.init(s0, trace, trace_cap));
   SolveState* ds = I->ds;
   const Work& wk = I->wk;
@@ -633,7 +660,7 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   s0.rcond = a.rcond;
   s0.a_fro = M.fro;
   s0.m_rows = M.m;
-  s0.n_cols = M.n;
+  s0.n_cols = M.comm ? M.n_global : M.n;
   s0.warm = 1;
   s0.enhanced = a.enhanced;
   s0.probe_done = 1;
@@ -847,6 +874,7 @@ int ts_moments(const ts_matrix* A, int32_t h_mode, const double* r, int32_t t, d
   if (t < 1 || t > kTMax || t > A->m)
     TS_INVAL("order t=%d outside 1..%lld", t, (long long)std::min<int64_t>(A->m, kTMax));
   if (h_mode == 1 && A->m != A->n) TS_INVAL("symmetric mode requires a square matrix");
+  if (A->comm) TS_INVAL("not supported on a column-sharded matrix");
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
   const int gram = h_mode == 0;
@@ -884,6 +912,7 @@ int ts_cta_step(const ts_matrix* A, int32_t h_mode, const double* x, const doubl
   if (t < 1 || t > kTMax || t > A->m)
     TS_INVAL("order t=%d outside 1..%lld", t, (long long)std::min<int64_t>(A->m, kTMax));
   if (h_mode == 1 && A->m != A->n) TS_INVAL("symmetric mode requires a square matrix");
+  if (A->comm) TS_INVAL("not supported on a column-sharded matrix");
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
   const int gram = h_mode == 0;
@@ -923,6 +952,107 @@ int ts_cta_step(const ts_matrix* A, int32_t h_mode, const double* x, const doubl
       TS_CUDA(cudaMemcpyAsync(r_out, I->kp.p[0], A->m * sizeof(double), cudaMemcpyDefault, st));
   }
   TS_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// ------------------------------------------------------- column sharding --
+int ts_comm_create(int device, int rank, int world, int64_t vec_capacity, ts_comm** out,
+                   void* ipc_handles_out) {
+  if (!out || !ipc_handles_out) TS_INVAL("null argument");
+  *out = nullptr;
+  if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
+    TS_INVAL("rank %d / world %d outside 0..%d", rank, world, kMaxRanks);
+  if (vec_capacity < 1) TS_INVAL("vector capacity must be positive");
+  DeviceGuard g(device);
+  Comm* c = new Comm();
+  c->dev = device;
+  c->rank = rank;
+  c->world = world;
+  c->vec_cap = (size_t)vec_capacity;
+  const size_t slot = c->vec_cap + kArScalars;
+  auto fail = [&](const char* what, cudaError_t e) {
+    set_error("%s failed: %s", what, cudaGetErrorString(e));
+    if (c->sym) cudaFree(c->sym);
+    if (c->flags) cudaFree(c->flags);
+    if (c->epoch) cudaFree(c->epoch);
+    delete c;
+    return TS_ECUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->sym, 2 * slot * sizeof(double))) != cudaSuccess) return fail("cudaMalloc(sym)", e);
+  if ((e = cudaMalloc(&c->flags, 256)) != cudaSuccess) return fail("cudaMalloc(flags)", e);
+  if ((e = cudaMalloc(&c->epoch, sizeof(unsigned long long))) != cudaSuccess) return fail("cudaMalloc(epoch)", e);
+  cudaMemset(c->sym, 0, 2 * slot * sizeof(double));
+  cudaMemset(c->flags, 0, 256);
+  cudaMemset(c->epoch, 0, sizeof(unsigned long long));
+  cudaIpcMemHandle_t hs, hf;
+  if ((e = cudaIpcGetMemHandle(&hs, c->sym)) != cudaSuccess) return fail("cudaIpcGetMemHandle(sym)", e);
+  if ((e = cudaIpcGetMemHandle(&hf, c->flags)) != cudaSuccess) return fail("cudaIpcGetMemHandle(flags)", e);
+  memcpy(ipc_handles_out, &hs, sizeof(hs));
+  memcpy(static_cast<char*>(ipc_handles_out) + 64, &hf, sizeof(hf));
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("comm init", e);
+  *out = reinterpret_cast<ts_comm*>(c);
+  return 0;
+}
+
+int ts_comm_connect(ts_comm* h, const void* all_handles) {
+  Comm* c = reinterpret_cast<Comm*>(h);
+  if (!c || !all_handles) TS_INVAL("null argument");
+  DeviceGuard g(c->dev);
+  std::vector<double*> psym(c->world);
+  std::vector<unsigned long long*> pflags(c->world);
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) {
+      psym[q] = c->sym;
+      pflags[q] = c->flags;
+      continue;
+    }
+    cudaIpcMemHandle_t hs, hf;
+    memcpy(&hs, static_cast<const char*>(all_handles) + 128 * q, sizeof(hs));
+    memcpy(&hf, static_cast<const char*>(all_handles) + 128 * q + 64, sizeof(hf));
+    void *ps = nullptr, *pf = nullptr;
+    TS_CUDA(cudaIpcOpenMemHandle(&ps, hs, cudaIpcMemLazyEnablePeerAccess));
+    c->opened.push_back(ps);
+    TS_CUDA(cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess));
+    c->opened.push_back(pf);
+    psym[q] = static_cast<double*>(ps);
+    pflags[q] = static_cast<unsigned long long*>(pf);
+  }
+  TS_CUDA(cudaMalloc(&c->psym_d, c->world * sizeof(double*)));
+  TS_CUDA(cudaMalloc(&c->pflags_d, c->world * sizeof(unsigned long long*)));
+  TS_CUDA(cudaMemcpy(c->psym_d, psym.data(), c->world * sizeof(double*), cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(c->pflags_d, pflags.data(), c->world * sizeof(unsigned long long*),
+                     cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int ts_comm_destroy(ts_comm* h) {
+  Comm* c = reinterpret_cast<Comm*>(h);
+  if (!c) return 0;
+  DeviceGuard g(c->dev);
+  cudaDeviceSynchronize();
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (void* p : {(void*)c->sym, (void*)c->flags, (void*)c->epoch, (void*)c->psym_d,
+                  (void*)c->pflags_d})
+    if (p) cudaFree(p);
+  delete c;
+  return 0;
+}
+
+int ts_matrix_set_shard(ts_matrix* A, ts_comm* h, int64_t n_global, int64_t col_offset,
+                        double fro_global) {
+  TS_CHECK_HANDLE(A);
+  Comm* c = reinterpret_cast<Comm*>(h);
+  if (c && c->dev != A->dev) TS_INVAL("communicator and matrix live on different devices");
+  if (c && (col_offset < 0 || col_offset + A->n > n_global))
+    TS_INVAL("shard columns [%lld, %lld) outside 0..%lld", (long long)col_offset,
+             (long long)(col_offset + A->n), (long long)n_global);
+  if (c && A->m > (int64_t)c->vec_cap) TS_INVAL("communicator vector capacity below m");
+  destroy_instances(A);  // instances bake the (un)sharded kernel sequence
+  A->comm = c;
+  A->n_global = c ? n_global : A->n;
+  A->col_off = c ? col_offset : 0;
+  if (c) A->fro = fro_global;
   return 0;
 }
 
@@ -969,6 +1099,7 @@ int ts_cta_solve(const ts_matrix* A, const double* b, const ts_cta_options* o, d
   int t_max = (int)std::min<int64_t>(o->t_max, A->m);
   if (t_max > kTMax) TS_INVAL("t_max=%d exceeds the device limit %d", t_max, kTMax);
   if (o->h_mode == 1 && A->m != A->n) TS_INVAL("symmetric mode requires a square matrix");
+  if (o->h_mode == 1 && A->comm) TS_INVAL("symmetric mode is not supported on a column-sharded matrix");
   memset(res, 0, sizeof(*res));
   DeviceGuard g(A->dev);
   CtaArgs a;
@@ -993,6 +1124,7 @@ int ts_ta_adaptive(const ts_matrix* A, const double* b, const ts_ta_options* o, 
   if (!o || !res || !b) TS_INVAL("null argument");
   memset(res, 0, sizeof(*res));
   DeviceGuard g(A->dev);
+  if (A->comm && o->gram) TS_INVAL("the Gram pair is not supported on a column-sharded matrix");
   TaArgs a;
   a.mode = MODE_ADAPTIVE;
   a.gram = o->gram ? 1 : 0;
@@ -1013,6 +1145,7 @@ int ts_ta_in_ball(const ts_matrix* A, const double* b, const ts_ball_options* o,
   if (!(o->rho > 0.0)) TS_INVAL("rho must be positive");
   memset(res, 0, sizeof(*res));
   DeviceGuard g(A->dev);
+  if (A->comm && o->gram) TS_INVAL("the Gram pair is not supported on a column-sharded matrix");
   TaArgs a;
   a.mode = MODE_BALL;
   a.gram = o->gram ? 1 : 0;
@@ -1033,6 +1166,7 @@ int ts_lp_feasibility(const ts_matrix* A, const double* b, const ts_lp_options* 
   if (o->rho_max >= 0.0 && !(o->rho_max > 0.0)) TS_INVAL("rho_max must be positive");
   memset(res, 0, sizeof(*res));
   DeviceGuard g(A->dev);
+  if (A->comm && o->gram) TS_INVAL("the Gram pair is not supported on a column-sharded matrix");
   TaArgs a;
   a.mode = MODE_LP;
   a.gram = o->gram ? 1 : 0;

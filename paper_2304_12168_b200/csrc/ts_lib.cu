@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "ts_cta.cuh"
+#include "ts_comm.cuh"
 
 namespace ts {
 

@@ -31,6 +31,7 @@ struct RowPlan {
 };
 
 struct Instance;  // cached solver instance (ts_drivers.cuh)
+struct Comm;      // column-sharding communicator (ts_comm.cuh)
 
 struct Mat {
   int dev = 0;
@@ -46,6 +47,9 @@ struct Mat {
   double fro = 0.0;
   RowPlan planN, planT;
   int Pmax = 0;  // largest grid any pass of this matrix uses
+  // column shard of a matrix split over ranks (nullptr: unsharded)
+  Comm* comm = nullptr;
+  int64_t n_global = 0, col_off = 0;
   // solver instances (buffers + instantiated graphs) cached per solver shape
   std::mutex cache_mu;
   std::vector<Instance*> cache;

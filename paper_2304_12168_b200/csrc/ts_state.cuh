@@ -202,6 +202,8 @@ struct EpiBase {
   int use_cond = 0;
   int use_sw = 0;
   int tclass = -1;  // live accounting class (set by the launch helper)
+  // vector passes: reduction slots that sum over n-space (column-sharded)
+  static constexpr unsigned kShardMask = 0;
   __device__ __forceinline__ void count_launch() const {
     if (st) atomicAdd(reinterpret_cast<unsigned long long*>(&st->launches), 1ull);
   }
@@ -272,6 +274,7 @@ struct EpiTaBp : EpiBase {
 // norm of a vector into the state (x0 warm start): sums v.v
 struct EpiNormTo : EpiBase {
   static constexpr int K = 1;
+  static constexpr unsigned kShardMask = 1u;  // ||v||^2 over n-space
   const double* v;
   int64_t len;
   int what;  // 0: ta x0 (rho / warm flag), 1: cta x norm (recheck)
@@ -352,6 +355,7 @@ struct EpiTaV : EpiBase {
 // sums: gap.gap, gap.b, min(x)
 struct EpiTaUpd : EpiBase {
   static constexpr int K = 3;
+  static constexpr unsigned kShardMask = 1u << 2;  // min(x) over n-space
   const double *b, *d, *c;
   double *bp, *gap, *x;
   int64_t m, n;

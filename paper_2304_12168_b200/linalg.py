@@ -147,6 +147,8 @@ def as_device_matrix(a):
         return a, False
     if isinstance(a, GramProduct):
         return a.device_matrix, True
+    if type(a).__name__ == "ShardedMatrix":
+        return a.device_matrix, False
     if isinstance(a, np.ndarray) or sparse.issparse(a) or _is_torch(a):
         return DeviceMatrix(a), False
     if hasattr(a, "shape") and not hasattr(a, "matvec"):
@@ -154,6 +156,15 @@ def as_device_matrix(a):
     raise TypeError(
         f"operator of type {type(a).__name__} cannot run on the device path; pass an ndarray, "
         "a scipy sparse matrix, a DeviceMatrix or a GramProduct")
+
+
+def local_slice(a, v, n_local: int):
+    """For a column-sharded matrix, this rank's slice of an n-vector given
+    either globally or already locally; identity otherwise."""
+    if v is None or type(a).__name__ != "ShardedMatrix":
+        return v
+    arr = np.asarray(v, dtype=np.float64)
+    return a.local(arr) if arr.shape == (a.n_global,) else arr
 
 
 def matvec(a, v) -> np.ndarray:

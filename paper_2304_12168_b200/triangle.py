@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as N
 from ._solve import build_result, host_vec, rows_to_trace, trace_buffer
-from .linalg import as_device_matrix, dot, matvec, matvec_transpose, norm2, shape_of
+from .linalg import as_device_matrix, dot, local_slice, matvec, matvec_transpose, norm2, shape_of
 from .results import APPROX_SOLUTION, TRIANGLE_TRACE_COLUMNS, SolveResult, Trace
 
 _REVALIDATE_EVERY = 512   # triangle.py:37 (device cadence)
@@ -83,7 +83,7 @@ def solve_in_ball(a, b, rho, eps, eps_prime=None, max_iters=100_000, x0=None) ->
     o.eps = float(eps)
     o.eps_prime = float(eps if eps_prime is None else eps_prime)
     o.max_iters = int(max_iters)
-    x0v = host_vec(x0, nn, "x0 has wrong shape") if x0 is not None else None
+    x0v = host_vec(local_slice(a, x0, nn), nn, "x0 has wrong shape") if x0 is not None else None
     o.x0 = N.ptr(x0v) if x0v is not None else None
     o.gram = int(gram)
     buf, cap = trace_buffer(max_iters)
@@ -112,7 +112,7 @@ def solve_adaptive(a, b, eps, eps_prime=None, rho_cap=None, max_iters=100_000,
     o.max_iters = int(max_iters)
     o.restart_halvings = int(max(0, restart_halvings))
     o.gram = int(gram)
-    x0v = host_vec(x0, nn, "x0 has wrong shape") if x0 is not None else None
+    x0v = host_vec(local_slice(a, x0, nn), nn, "x0 has wrong shape") if x0 is not None else None
     o.x0 = N.ptr(x0v) if x0v is not None else None
     buf, cap = trace_buffer(max_iters)
     x = np.empty(nn)

@@ -1,0 +1,112 @@
+"""World-size-2 gloo tests of the column-sharded path's host logic (CPU only).
+
+Two processes each hold one column block; the sharded iteration model
+(tests/sharded_model.py, the decomposition csrc/ts_comm.cuh implements) must
+reproduce the unsharded reference oracle: same status, iteration count and
+pivot/expand sequence, x and residuals to rounding.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    import sharded_model as SM
+    from paper_2304_12168_b200 import workloads as W
+    from paper_2304_12168_b200.shard import column_range, local_block
+
+    if case == "cta_dense":
+        w = W.dense_lowrank(60, 240, 24, seed=3)
+        c0, c1 = column_range(w.a.shape[1], world, rank)
+        out = SM.cta_sharded(local_block(w.a, c0, c1), w.b, 1e-8, 200)
+    elif case == "ta_dense":
+        w = W.dense_gaussian(40, 90, seed=4)
+        c0, c1 = column_range(w.a.shape[1], world, rank)
+        out = SM.ta_adaptive_sharded(local_block(w.a, c0, c1), w.b,
+                                     1e-8 * np.linalg.norm(w.b), 30)
+    else:  # lp_sparse: the C5 family (cone stall)
+        w = W.lp_columns(60, 3000, 10, seed=5)
+        c0, c1 = column_range(w.a.shape[1], world, rank)
+        out = SM.ta_adaptive_sharded(local_block(w.a, c0, c1), w.b,
+                                     1e-6 * np.linalg.norm(w.b), 1000, lp=True)
+    np.savez(os.path.join(outdir, f"{case}_{rank}.npz"), x=out["x"], c0=c0, c1=c1,
+             iterations=out["iterations"], status=out["status"],
+             residual_norm=out["residual_norm"], events=np.array(out.get("events", [])))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["cta_dense", "ta_dense", "lp_sparse"])
+def test_sharded_decomposition_matches_oracle(case, tmp_path):
+    import torch.multiprocessing as mp
+
+    from oracle import port
+    from paper_2304_12168_b200 import workloads as W
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    parts = [np.load(os.path.join(tmp_path, f"{case}_{r}.npz")) for r in range(world)]
+    x = np.concatenate([p["x"] for p in parts])
+    if case == "cta_dense":
+        w = W.dense_lowrank(60, 240, 24, seed=3)
+        ref = port.cta_solve(w.a, w.b, epsilon=1e-8, max_iters=200)
+    elif case == "ta_dense":
+        w = W.dense_gaussian(40, 90, seed=4)
+        ref = port.ta_adaptive(w.a, w.b, eps=1e-8 * np.linalg.norm(w.b), max_iters=30)
+    else:
+        w = W.lp_columns(60, 3000, 10, seed=5)
+        ref = port.lp_feasibility(w.a, w.b, eps=1e-6 * np.linalg.norm(w.b), max_iters=1000)
+    for p in parts:  # every rank takes identical decisions
+        assert str(p["status"]) == ref["status"]
+        assert int(p["iterations"]) == ref["iterations"]
+        assert float(p["residual_norm"]) == pytest.approx(ref["residual_norm"], rel=1e-9)
+    if "trace" in ref and case != "cta_dense":
+        assert list(parts[0]["events"]) == [row[4] for row in ref["trace"]]
+    assert np.linalg.norm(x - ref["x"]) <= 1e-9 * max(np.linalg.norm(ref["x"]), 1e-300)
+
+
+def test_column_partition_covers_all_columns():
+    from paper_2304_12168_b200.shard import column_range
+
+    for n in (1, 7, 1000, 1_000_000):
+        for world in (1, 2, 3, 8):
+            ranges = [column_range(n, world, r) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+            assert max(b - a for a, b in ranges) - min(b - a for a, b in ranges) <= 1
+
+
+def test_local_block_dense_and_sparse():
+    import scipy.sparse as sp
+
+    from paper_2304_12168_b200.shard import local_block
+
+    rng = np.random.default_rng(0)
+    dense = rng.standard_normal((7, 11)) * (rng.random((7, 11)) < 0.4)
+    csr = sp.csr_array(dense)
+    for c0, c1 in ((0, 4), (4, 11), (3, 3)):
+        assert np.array_equal(local_block(dense, c0, c1), dense[:, c0:c1])
+        blk = local_block(csr, c0, c1)
+        assert blk.format == "csr"
+        assert np.array_equal(blk.toarray(), dense[:, c0:c1])
