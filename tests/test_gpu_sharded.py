@@ -69,11 +69,14 @@ def test_sharded_ta_and_lp_sparse(group):
         assert (r1.status, r1.iterations) == (r0.status, r0.iterations)
         assert [row[4] for row in r1.trace.rows] == [row[4] for row in r0.trace.rows]
         assert rel_l2(r1.x, r0.x) <= 1e-11
-    # random start + recheck cadence on the sharded CTA (sparse)
+    # random start + a short recheck cadence on the sharded CTA (sparse,
+    # ill-conditioned: compare inside the parity window)
     w3 = W.clement_variant(301, seed=3)
     dm3, sh3 = _pair(w3.a)
-    opts = ts.CenteringOptions(epsilon=1e-8, max_iters=300, start="random", start_seed=4)
+    opts = ts.CenteringOptions(epsilon=1e-8, max_iters=40, start="random", start_seed=4,
+                               recheck_every=16)
     r0 = ts.centering_solve(dm3, w3.b, opts)
     r1 = ts.centering_solve(sh3, w3.b, opts)
     assert (r1.status, r1.iterations) == (r0.status, r0.iterations)
+    assert rel_l2(r1.x, r0.x) <= 1e-9
     assert r1.residual_norm == pytest.approx(r0.residual_norm, rel=1e-6)
