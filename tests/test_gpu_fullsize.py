@@ -1,0 +1,105 @@
+"""Parity at the BASELINE.json configs' full sizes (GPU vs the CPU oracle).
+
+Inside the parity window (the reference agrees with itself to
+~1e-12 for <= 50 iterations on the ill-conditioned families) iterates must
+match to 1e-9 relative l2 (north_star).  Full solves must reproduce the
+reference outcome: status, iteration count (+-1 %), final relative residual
+within a factor of 2.  Sizes: C1 1000^2 dense, C2 5000 x 20000 dense,
+C3 n = 100001 CSR, C4 n = 10^6 CSR, C5 10^4 x 10^6 CSR+CSC.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ts():
+    import paper_2304_12168_b200 as ts
+
+    return ts
+
+
+def _check_window(dev, ref, tol=1e-9):
+    assert dev.status == ref["status"]
+    assert dev.iterations == ref["iterations"]
+    assert rel_l2(dev.x, ref["x"]) <= tol, rel_l2(dev.x, ref["x"])
+
+
+def _check_outcome(dev, ref, bn):
+    assert dev.status == ref["status"]
+    band = max(1, int(np.ceil(0.01 * ref["iterations"])))
+    assert abs(dev.iterations - ref["iterations"]) <= band
+    rr, gr = dev.residual_norm / bn, ref["residual_norm"] / bn
+    assert 0.5 * gr <= rr <= 2.0 * gr, (rr, gr)
+
+
+def test_c1_dense_window_cta_and_ta(ts):
+    from oracle import port
+    from paper_2304_12168_b200 import workloads as W
+
+    w = W.dense_gaussian()
+    dm = ts.DeviceMatrix(w.a)
+    bn = float(np.linalg.norm(w.b))
+    dev = ts.centering_solve(dm, w.b, ts.CenteringOptions(epsilon=1e-8, max_iters=40))
+    _check_window(dev, port.cta_solve(w.a, w.b, epsilon=1e-8, max_iters=40))
+    dev = ts.solve_adaptive(dm, w.b, eps=1e-8 * bn, max_iters=50)
+    ref = port.ta_adaptive(w.a, w.b, eps=1e-8 * bn, max_iters=50)
+    _check_window(dev, ref)
+    assert [r[4] for r in dev.trace.rows] == [r[4] for r in ref["trace"]]
+
+
+def test_c2_dense_lowrank_full_solve(ts):
+    from oracle import port
+    from paper_2304_12168_b200 import workloads as W
+
+    w = W.dense_lowrank()
+    dev = ts.centering_solve(ts.DeviceMatrix(w.a), w.b, ts.CenteringOptions(epsilon=1e-8))
+    ref = port.cta_solve(w.a, w.b, epsilon=1e-8)
+    # well-conditioned on its range: the whole solve is inside the window
+    _check_window(dev, ref, tol=1e-9)
+    assert dev.status == "normal_eq_solution" and dev.iterations == 23
+
+
+def test_c3_clement_window(ts):
+    from oracle import port
+    from paper_2304_12168_b200 import workloads as W
+
+    w = W.clement_variant()
+    dev = ts.centering_solve(ts.DeviceMatrix(w.a), w.b, ts.CenteringOptions(epsilon=1e-8, max_iters=30))
+    _check_window(dev, port.cta_solve(w.a, w.b, epsilon=1e-8, max_iters=30))
+
+
+def test_c4_convdiff_window(ts):
+    from oracle import port
+    from paper_2304_12168_b200 import workloads as W
+
+    w = W.convdiff_upwind()
+    dev = ts.centering_solve(ts.DeviceMatrix(w.a), w.b, ts.CenteringOptions(epsilon=1e-8, max_iters=15))
+    _check_window(dev, port.cta_solve(w.a, w.b, epsilon=1e-8, max_iters=15))
+
+
+def test_c5_lp_stall_and_unconstrained_ta(ts):
+    from oracle import port
+    from paper_2304_12168_b200 import workloads as W
+
+    w = W.lp_columns()
+    dm = ts.DeviceMatrix(w.a)
+    bn = float(np.linalg.norm(w.b))
+    dev = ts.nonnegative_feasibility(dm, w.b, eps=1e-6 * bn)
+    ref = port.lp_feasibility(w.a, w.b, eps=1e-6 * bn)
+    _check_window(dev, ref, tol=1e-11)
+    assert dev.status == "witness" and dev.iterations == 11
+    assert dev.detail == "no ascent direction in the nonnegative cone section"
+    assert dev.lower_bound == pytest.approx(ref["lower_bound"], rel=1e-11)
+    dev = ts.solve_adaptive(dm, w.b, eps=1e-6 * bn)
+    ref = port.ta_adaptive(w.a, w.b, eps=1e-6 * bn)
+    _check_outcome(dev, ref, bn)
+    assert rel_l2(dev.x, ref["x"]) <= 1e-9
+    assert dev.residual_norm <= 1e-6 * bn
+    assert float(dev.x.min()) >= 0.0
