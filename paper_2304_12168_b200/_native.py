@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtrisolve_b200.so")
+LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(_HERE, "_lib", "libtrisolve_b200.so")
 
 EXPORTS = (
     "ts_abi_version", "ts_last_error", "ts_device_count",

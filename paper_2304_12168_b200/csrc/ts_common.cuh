@@ -56,7 +56,7 @@ constexpr int kNT = 256;          // threads per block for every pass kernel
 constexpr int kMinBlocks = 4;     // __launch_bounds__ min blocks/SM (<= 64 registers)
 constexpr int kWarps = kNT / 32;  // warps per block
 constexpr int kKMax = 8;          // max reduction slots per pass
-constexpr int kCW = 2 * kNT;      // dense A^T tile width (columns): 2 per thread
+constexpr int kCW = 4 * kNT;      // max dense A^T tile width (columns): up to 4 per thread
 constexpr int kTMax = 8;          // max CTA order supported on device
 
 enum RedOp : int { RED_SUM = 0, RED_MIN = 1 };
@@ -74,11 +74,54 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+// 256-bit streaming load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
+__device__ __forceinline__ void ld_stream4(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ldg4(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
 __device__ __forceinline__ int ld_stream_i(const int* p) {
   int v;
   asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+// ---- TMA 1-D bulk copies (cp.async.bulk) + mbarrier helpers ---------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{ .reg .pred p; TS_WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; "
+      "@!p bra TS_WAIT_%=; }" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, both ends 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -146,6 +189,7 @@ struct Work {
   double* facc;     // [pmax * kKMax] split-row / split-tile epilogue partials
   double* bpart;    // [pmax * 2] block boundary row-piece sums (first, last)
   double* tpart;    // [pmax * 2 * kCW] block boundary tile pieces
+  double* npart;    // [ntiles * m] dense A v per-(tile,row) partials (k_rows_tile)
   unsigned* cnt;    // [pmax] split counters (self-resetting)
   unsigned* done;   // [4] completion counters (self-resetting)
   int pmax;

@@ -86,8 +86,9 @@ struct Arena {
   }
 };
 
-static int make_work(Arena& ar, int pmax, Work* w) {
+static int make_work(Arena& ar, int pmax, Work* w, int64_t npart = 0) {
   w->pmax = pmax;
+  TS_CHECK(ar.get(&w->npart, (size_t)std::max<int64_t>(npart, 1)));
   TS_CHECK(ar.get(&w->bacc, (size_t)pmax * kKMax));
   TS_CHECK(ar.get(&w->facc, (size_t)pmax * kKMax));
   TS_CHECK(ar.get(&w->bpart, (size_t)pmax * 2));
@@ -304,7 +305,7 @@ int ts_matrix_info(const ts_matrix* A, int64_t* m, int64_t* n, int64_t* nnz, int
 static int finish_create(ts_matrix* A, cudaStream_t st, Arena& ar) {
   // Frobenius norm once (linalg.py:64-69); cached on the immutable handle
   Work wk;
-  TS_CHECK(make_work(ar, work_blocks(A->sms), &wk));
+  TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->kind == 0 ? npart_elems(A->m, A->n) : 0));
   double* dfro;
   TS_CHECK(ar.get(&dfro, 1));
   if (A->kind == 0) {
@@ -337,7 +338,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
   A->m = m;
   A->n = n;
   A->nnz = m * n;
-  A->lda = n >= 64 ? (n + 15) / 16 * 16 : (n + 1) / 2 * 2;
+  A->lda = n >= 64 ? (n + 15) / 16 * 16 : (n + 3) / 4 * 4;
   int rc = 0;
   {
     Arena ar(st);
@@ -357,8 +358,25 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
     }
     if (!rc) rc = plan_rows_dense(m, n, A->sms, &A->planN, st);
     if (!rc) {
+      // 128-bit loads; TS_DENSE_VW=4 selects the 256-bit variants (measured slower)
+      const char* e = getenv("TS_DENSE_VW");
+      const int vw = (e && atoi(e) == 4) ? 4 : 2;
+      A->planN.vw = vw;
       A->planT.kind = PLAN_TILE;
-      A->planT.P = tile_grid(m, n, A->sms);
+      A->planT.vw = vw;
+      A->planT.P = tile_grid(m, n, A->sms, vw);
+      // TMA-streamed A^T v (TS_DENSE_T=ldg keeps the register-staged tile kernel)
+      const char* te = getenv("TS_DENSE_T");
+      if (!(te && !strcmp(te, "ldg")) && vw == 2) {
+        A->planT.kind = PLAN_TMA;
+        A->planT.P = std::max(1, std::min(tile_grid(m, n, A->sms, 2), A->sms * 2));
+      }
+      // A v in the A^T v tile geometry: TS_DENSE_N=tile (measured slower than the flat split)
+      const char* fe = getenv("TS_DENSE_N");
+      if (A->planN.kind == PLAN_FLAT && fe && !strcmp(fe, "tile")) {
+        A->planN.kind = PLAN_TILE;
+        A->planN.P = tile_grid(m, n, A->sms, 2);
+      }
     }
     if (!rc) rc = finish_create(A, st, ar);
   }

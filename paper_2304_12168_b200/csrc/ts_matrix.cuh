@@ -22,12 +22,16 @@
 
 namespace ts {
 
-enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3 };
+enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4 };
+
+// elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans)
+inline int64_t npart_elems(int64_t m, int64_t n) { return ((n + 2 * kNT - 1) / (2 * kNT)) * m; }
 
 struct RowPlan {
   int kind = PLAN_SHORT;
   int P = 1;            // blocks
   int* wrow = nullptr;  // device [P * kWarps] (PLAN_FLAT)
+  int vw = 2;           // dense: columns per 128/256-bit load
 };
 
 struct Instance;  // cached solver instance (ts_drivers.cuh)
@@ -54,7 +58,7 @@ struct Mat {
   std::mutex cache_mu;
   std::vector<Instance*> cache;
 
-  DenseRows dense() const { return DenseRows{a, lda, m, n}; }
+  DenseRows dense(int vw = 2) const { return DenseRows{a, lda, m, n, vw}; }
   CsrRows csr() const { return CsrRows{rp, ci, val, m, nnz}; }
   CsrRows csrT() const { return CsrRows{rpT, ciT, valT, n, nnz}; }
 };
@@ -104,8 +108,9 @@ inline int vec_grid(int64_t len, int sms) {
   return (int)g;
 }
 
-inline int tile_grid(int64_t m, int64_t n, int sms) {
-  const int64_t nct = (n + kCW - 1) / kCW;
+inline int tile_grid(int64_t m, int64_t n, int sms, int vw) {
+  const int64_t tw = (int64_t)vw * kNT;
+  const int64_t nct = (n + tw - 1) / tw;
   const int64_t U = nct * m;
   int64_t g = U / 32;  // >= 32 rows of a tile per block
   const int64_t pmax = resident_blocks(sms);
@@ -121,13 +126,29 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
                 cudaStream_t st) {
   if (M.kind == 0) {
     if (!trans) {
-      if (M.planN.kind == PLAN_FLAT)
+      if (M.planN.kind == PLAN_TILE) {
+        const int64_t nct = (M.n + 2 * kNT - 1) / (2 * kNT);
+        k_rows_tile<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk.npart);
+        k_tile_combine<Epi><<<vec_grid(M.m, M.sms), kNT, 0, st>>>(M.m, nct, wk.npart, epi, wk);
+      } else if (M.planN.kind == PLAN_FLAT && M.planN.vw == 4)
+        k_rows_flat<DenseRows4, Epi><<<M.planN.P, kNT, 0, st>>>(DenseRows4{M.dense()}, x, xs, epi,
+                                                                  wk, M.planN.wrow);
+      else if (M.planN.kind == PLAN_FLAT)
         k_rows_flat<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk,
                                                                  M.planN.wrow);
       else
         k_rows_short<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+    } else if (M.planT.kind == PLAN_TMA) {
+      static bool attr_set = false;  // per process; the attribute is per function
+      if (!attr_set) {
+        cudaFuncSetAttribute(k_cols_tma<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+        attr_set = true;
+      }
+      k_cols_tma<Epi><<<M.planT.P, kNT, kTmaSmem, st>>>(M.dense(), x, xs, epi, wk);
+    } else if (M.planT.vw == 4) {
+      k_cols_tile<Epi, 4><<<M.planT.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
     } else {
-      k_cols_tile<Epi><<<M.planT.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+      k_cols_tile<Epi, 2><<<M.planT.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
     }
   } else {
     const RowPlan& pl = trans ? M.planT : M.planN;

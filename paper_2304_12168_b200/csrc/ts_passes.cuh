@@ -61,6 +61,7 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 struct DenseRows {
   const double* a;
   int64_t lda, m, n;
+  int vw = 2;  // 4: 256-bit loads in the flat A v (requires lda % 4 == 0); see DenseRows4
   __device__ __forceinline__ int64_t rbeg(int64_t r) const { return r * n; }
   __device__ __forceinline__ int64_t rend(int64_t r) const { return (r + 1) * n; }
   __device__ __forceinline__ int64_t total() const { return m * n; }
@@ -87,8 +88,13 @@ struct DenseRows {
       double2 v[8], xv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = ld_stream2(rp + 2 * (p + 32 * u));
+#ifdef TS_EXP_NOX
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = make_double2(1.0 + u, 2.0 - u);
+#else
 #pragma unroll
       for (int u = 0; u < 8; ++u) xv[u] = ldg2(xp + 2 * (p + 32 * u));
+#endif
 #pragma unroll
       for (int u = 0; u < 8; u += 4) {
         a0 = fma(v[u].x, xs(xv[u].x), a0); a0 = fma(v[u].y, xs(xv[u].y), a0);
@@ -104,12 +110,62 @@ struct DenseRows {
     }
     return ((a0 + a1) + (a2 + a3)) + (h + t);
   }
+  // 256-bit variant: quads of 4 columns, kQ quads of A + kQ of x per lane in flight
+  static constexpr int kQ = 2;
+  __device__ __forceinline__ double seg4(int64_t r, int64_t k0, int64_t k1, const double* x,
+                                         const XS& xs, int lane) const {
+    const int64_t c0 = k0 - r * n, c1 = k1 - r * n;
+    const double* row = a + r * lda;
+    double h = 0.0, t = 0.0;
+    int64_t c = (c0 + 3) & ~(int64_t)3;
+    if (c > c1) c = c1;
+    if (lane < c - c0) h = row[c0 + lane] * xs(__ldg(x + c0 + lane));  // <= 3 head elements
+    const int64_t nq = (c1 - c) >> 2;
+    const int64_t cend = c + 4 * nq;
+    if (lane < c1 - cend) t = row[cend + lane] * xs(__ldg(x + cend + lane));  // <= 3 tail
+    const double* rp = row + c;
+    const double* xp = x + c;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t q = lane;
+    for (; q + 32 * (kQ - 1) < nq; q += 32 * kQ) {
+      double v[kQ][4], xv[kQ][4];
+#pragma unroll
+      for (int u = 0; u < kQ; ++u) ld_stream4(rp + 4 * (q + 32 * u), v[u]);
+#pragma unroll
+      for (int u = 0; u < kQ; ++u) ldg4(xp + 4 * (q + 32 * u), xv[u]);
+#pragma unroll
+      for (int u = 0; u < kQ; ++u) {
+        a0 = fma(v[u][0], xs(xv[u][0]), a0);
+        a1 = fma(v[u][1], xs(xv[u][1]), a1);
+        a2 = fma(v[u][2], xs(xv[u][2]), a2);
+        a3 = fma(v[u][3], xs(xv[u][3]), a3);
+      }
+    }
+    for (; q < nq; q += 32) {
+      double v[4], xv[4];
+      ld_stream4(rp + 4 * q, v);
+      ldg4(xp + 4 * q, xv);
+      a0 = fma(v[0], xs(xv[0]), a0);
+      a1 = fma(v[1], xs(xv[1]), a1);
+      a2 = fma(v[2], xs(xv[2]), a2);
+      a3 = fma(v[3], xs(xv[3]), a3);
+    }
+    return ((a0 + a1) + (a2 + a3)) + (h + t);
+  }
   // whole row, one thread, column order (short-row path)
   __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
     const double* row = a + r * lda;
     double s = 0.0;
     for (int64_t c = 0; c < n; ++c) s = fma(row[c], xs(__ldg(x + c)), s);
     return s;
+  }
+};
+
+// A v with 256-bit loads: same geometry, seg() -> seg4()
+struct DenseRows4 : DenseRows {
+  __device__ __forceinline__ double seg(int64_t r, int64_t k0, int64_t k1, const double* x,
+                                        const XS& xs, int lane) const {
+    return seg4(r, k0, k1, x, xs, lane);
   }
 };
 
@@ -443,11 +499,13 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
 }
 
 // ----------------------------------------------------------- k_cols_tile ----
-template <class Epi>
+// VW columns per thread (2: 128-bit loads, 4: 256-bit loads); tile = VW * kNT
+template <class Epi, int VW>
 __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, const double* __restrict__ x,
-                                                   XS xs, Epi epi, Work wk) {
+                                                             XS xs, Epi epi, Work wk) {
   constexpr int K = Epi::K;
-  constexpr int RU = 8;  // rows in flight per thread
+  constexpr int TW = VW * kNT;       // tile width (columns)
+  constexpr int RU = VW == 4 ? 4 : 8;  // rows in flight per thread
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
@@ -459,7 +517,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
   KTimer* kt = epi.timer();
   ktimer_begin(kt);
   const int64_t m = A.m, n = A.n, lda = A.lda;
-  const int64_t nct = (n + kCW - 1) / kCW;
+  const int64_t nct = (n + TW - 1) / TW;
   const int64_t U = nct * m;
   const int64_t P = gridDim.x, b = blockIdx.x;
   const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
@@ -470,46 +528,57 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
   for (int64_t u = U0; u < U1;) {
     const int64_t ct = u / m, r0 = u - ct * m;
     const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
-    const int64_t c = ct * kCW + 2 * threadIdx.x;
-    const bool two = c + 1 < n, one = c < n;
-    double ax[RU], ay[RU];
+    const int64_t c = ct * TW + VW * threadIdx.x;
+    const int64_t nv = n - c < VW ? (n - c > 0 ? n - c : 0) : VW;  // valid columns of this thread
+    double ac[2][VW];
 #pragma unroll
-    for (int i = 0; i < RU; ++i) ax[i] = ay[i] = 0.0;
+    for (int j = 0; j < VW; ++j) ac[0][j] = ac[1][j] = 0.0;
     const double* base = A.a + c;
     int64_t r = r0;
-    if (two) {
+    if (nv == VW) {
       for (; r + RU <= r1; r += RU) {
-        double2 v[RU];
+        double v[RU][VW];
         double xr[RU];
 #pragma unroll
-        for (int i = 0; i < RU; ++i) v[i] = ld_stream2(base + (r + i) * lda);
+        for (int i = 0; i < RU; ++i) {
+          if constexpr (VW == 4) {
+            ld_stream4(base + (r + i) * lda, v[i]);
+          } else {
+            const double2 t2 = ld_stream2(base + (r + i) * lda);
+            v[i][0] = t2.x;
+            v[i][1] = t2.y;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < RU; ++i) xr[i] = xs(__ldg(x + r + i));
 #pragma unroll
-        for (int i = 0; i < RU; ++i) {
-          ax[i] = fma(v[i].x, xr[i], ax[i]);
-          ay[i] = fma(v[i].y, xr[i], ay[i]);
-        }
+        for (int i = 0; i < RU; ++i)
+#pragma unroll
+          for (int j = 0; j < VW; ++j) ac[i & 1][j] = fma(v[i][j], xr[i], ac[i & 1][j]);
       }
       for (; r < r1; ++r) {
-        const double2 v = ld_stream2(base + r * lda);
         const double xr = xs(__ldg(x + r));
-        ax[0] = fma(v.x, xr, ax[0]);
-        ay[0] = fma(v.y, xr, ay[0]);
+#pragma unroll
+        for (int j = 0; j < VW; ++j) ac[0][j] = fma(ld_stream(base + r * lda + j), xr, ac[0][j]);
       }
-    } else if (one) {
-      for (; r < r1; ++r) ax[0] = fma(ld_stream(base + r * lda), xs(__ldg(x + r)), ax[0]);
+    } else if (nv > 0) {
+      for (; r < r1; ++r) {
+        const double xr = xs(__ldg(x + r));
+        for (int j = 0; j < nv; ++j) ac[0][j] = fma(ld_stream(base + r * lda + j), xr, ac[0][j]);
+      }
     }
-    const double sx = ((ax[0] + ax[1]) + (ax[2] + ax[3])) + ((ax[4] + ax[5]) + (ax[6] + ax[7]));
-    const double sy = ((ay[0] + ay[1]) + (ay[2] + ay[3])) + ((ay[4] + ay[5]) + (ay[6] + ay[7]));
+    double sv[VW];
+#pragma unroll
+    for (int j = 0; j < VW; ++j) sv[j] = ac[0][j] + ac[1][j];
     if (r0 == 0 && r1 == m) {
-      if (one) epi.elem(c, sx, acc);
-      if (two) epi.elem(c + 1, sy, acc);
+#pragma unroll
+      for (int j = 0; j < VW; ++j)
+        if (j < nv) epi.elem(c + j, sv[j], acc);
     } else {
       const int which = (r0 > 0) ? 0 : 1;  // 0: tile began in an earlier block
-      double* dst = wk.tpart + ((size_t)b * 2 + which) * kCW + 2 * threadIdx.x;
-      dst[0] = sx;
-      dst[1] = sy;
+      double* dst = wk.tpart + ((size_t)b * 2 + which) * kCW + VW * threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < VW; ++j) dst[j] = sv[j];
       if (which == 0) ct_first = ct; else ct_last = ct;
     }
     u += r1 - r0;
@@ -531,7 +600,181 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
     __syncthreads();
     if (sflag) {
       __threadfence();
-      const int64_t c = ct * kCW + 2 * threadIdx.x;
+      const int64_t c = ct * TW + VW * threadIdx.x;
+      double y[VW];
+#pragma unroll
+      for (int j = 0; j < VW; ++j) y[j] = __ldcg(wk.tpart + ((size_t)ba * 2 + 1) * kCW + VW * threadIdx.x + j);
+      for (int64_t q = ba + 1; q <= bb; ++q)
+#pragma unroll
+        for (int j = 0; j < VW; ++j) y[j] += __ldcg(wk.tpart + ((size_t)q * 2) * kCW + VW * threadIdx.x + j);
+      double facc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) facc[k] = red_identity(epi.op(k));
+#pragma unroll
+      for (int j = 0; j < VW; ++j)
+        if (c + j < n) epi.elem(c + j, y[j], facc);
+      block_reduce<K>(facc, sm, epi);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) wk.facc[bb * kKMax + k] = facc[k];
+        wk.cnt[bb] = 0u;
+      }
+    }
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      wk.bacc[b * kKMax + k] = acc[k];
+      if (!end_block) wk.facc[b * kKMax + k] = red_identity(epi.op(k));
+    }
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
+    if (threadIdx.x == 0) {
+      ktimer_end(kt);
+      epi.finish(red);
+    }
+    __syncthreads();
+    epi.finish_block();
+  }
+}
+
+// ------------------------------------------------------------ k_cols_tma ----
+// Dense A^T v streamed by the Tensor Memory Accelerator: the block's (tile,
+// row) units are fetched as 4 KB row chunks with cp.async.bulk into a ring of
+// kTmaStages stages x kTmaRows rows in shared memory (one producer thread,
+// mbarrier transaction counts), so the memory system sees deep, contiguous
+// per-block streams with no register staging; 256 consumer threads own two
+// columns each and accumulate from shared memory.  Partial tiles at block
+// boundaries are merged exactly like k_cols_tile (same reduction order).
+constexpr int kTmaRows = 4;
+constexpr int kTmaStages = 6;
+constexpr int kTmaTW = 2 * kNT;  // tile width (columns)
+constexpr int kTmaSmem = kTmaStages * kTmaRows * kTmaTW * 8;
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, 2) k_cols_tma(DenseRows A, const double* __restrict__ x, XS xs,
+                                                    Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  extern __shared__ __align__(128) double ring[];  // [stage][row][kTmaTW]
+  __shared__ __align__(8) unsigned long long full[kTmaStages];
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  xs.load();
+  KTimer* kt = epi.timer();
+  ktimer_begin(kt);
+  const int64_t m = A.m, n = A.n, lda = A.lda;
+  const int64_t nct = (n + kTmaTW - 1) / kTmaTW;
+  const int64_t U = nct * m;
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // The unit range is consumed as groups of <= kTmaRows rows that never cross a
+  // tile boundary; group g covers units [gstart(g), gstart(g) + grows(g)).
+  // Producer state walks the same sequence ahead of the consumers.
+  auto group_at = [&](int64_t u, int64_t* ct, int64_t* r, int* rows) {
+    *ct = u / m;
+    *r = u - *ct * m;
+    int64_t left = m - *r;
+    if (U1 - u < left) left = U1 - u;
+    *rows = (int)(left < kTmaRows ? left : kTmaRows);
+  };
+  auto issue = [&](int64_t u, int stage) {
+    int64_t ct, r;
+    int rows;
+    group_at(u, &ct, &r, &rows);
+    const int64_t cb = ct * kTmaTW;
+    const int64_t cols = (n - cb < kTmaTW) ? n - cb : kTmaTW;
+    const unsigned bytes = (unsigned)(((cols * 8) + 15) & ~15);  // tail rounds into the lda padding
+    mbar_expect_tx(&full[stage], bytes * rows);
+    for (int i = 0; i < rows; ++i)
+      bulk_g2s(ring + ((size_t)stage * kTmaRows + i) * kTmaTW, A.a + (r + i) * lda + cb, bytes,
+               &full[stage]);
+    return (int64_t)rows;
+  };
+  int64_t pu = U0;  // producer position
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kTmaStages && pu < U1; ++s) pu += issue(pu, s);
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  long long ct_first = -1, ct_last = -1;
+  int64_t cu = U0;  // consumer position
+  int g = 0;
+  while (cu < U1) {
+    // one segment = one tile, rows r0..r1 of this block's range
+    const int64_t ct = cu / m, r0 = cu - ct * m;
+    const int64_t r1 = (m < r0 + (U1 - cu)) ? m : r0 + (U1 - cu);
+    const int64_t c = ct * kTmaTW + 2 * threadIdx.x;
+    const bool two = c + 1 < n, one = c < n;
+    double ax0 = 0.0, ay0 = 0.0, ax1 = 0.0, ay1 = 0.0;
+    for (int64_t r = r0; r < r1;) {
+      const int stage = g % kTmaStages;
+      const unsigned phase = (unsigned)((g / kTmaStages) & 1);
+      const int rows = (int)((r1 - r < kTmaRows) ? r1 - r : kTmaRows);
+      mbar_wait(&full[stage], phase);
+      const double* sbuf = ring + (size_t)stage * kTmaRows * kTmaTW + 2 * threadIdx.x;
+#pragma unroll
+      for (int i = 0; i < kTmaRows; ++i) {
+        if (i < rows) {
+          const double xr = xs(__ldg(x + r + i));
+          const double2 v = *reinterpret_cast<const double2*>(sbuf + (size_t)i * kTmaTW);
+          if (i & 1) {
+            if (one) ax1 = fma(v.x, xr, ax1);
+            if (two) ay1 = fma(v.y, xr, ay1);
+          } else {
+            if (one) ax0 = fma(v.x, xr, ax0);
+            if (two) ay0 = fma(v.y, xr, ay0);
+          }
+        }
+      }
+      __syncthreads();  // stage consumed: refill it
+      if (threadIdx.x == 0 && pu < U1) pu += issue(pu, stage);
+      r += rows;
+      ++g;
+    }
+    const double sx = ax0 + ax1, sy = ay0 + ay1;
+    if (r0 == 0 && r1 == m) {
+      if (one) epi.elem(c, sx, acc);
+      if (two) epi.elem(c + 1, sy, acc);
+    } else {
+      const int which = (r0 > 0) ? 0 : 1;  // 0: tile began in an earlier block
+      double* dst = wk.tpart + ((size_t)b * 2 + which) * kCW + 2 * threadIdx.x;
+      dst[0] = sx;
+      dst[1] = sy;
+      if (which == 0) ct_first = ct; else ct_last = ct;
+    }
+    cu += r1 - r0;
+  }
+  // split-tile merges (as k_cols_tile)
+  bool end_block = false;
+  if (ct_first >= 0 && ct_first * m + m <= U1) end_block = true;
+  for (int which = 0; which < 2; ++which) {
+    const long long ct = which == 0 ? ct_first : ct_last;
+    if (ct < 0) continue;
+    const int64_t ba = blk_of(ct * m, U, P), bb = blk_of(ct * m + m - 1, U, P);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned prev = atomicAdd(wk.cnt + bb, 1u);
+      sflag = (prev == (unsigned)(bb - ba));
+    }
+    __syncthreads();
+    if (sflag) {
+      __threadfence();
+      const int64_t c = ct * kTmaTW + 2 * threadIdx.x;
       double y0 = __ldcg(wk.tpart + ((size_t)ba * 2 + 1) * kCW + 2 * threadIdx.x);
       double y1 = __ldcg(wk.tpart + ((size_t)ba * 2 + 1) * kCW + 2 * threadIdx.x + 1);
       for (int64_t q = ba + 1; q <= bb; ++q) {
@@ -564,6 +807,103 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
     reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
     if (threadIdx.x == 0) {
       ktimer_end(kt);
+      epi.finish(red);
+    }
+    __syncthreads();
+    epi.finish_block();
+  }
+}
+
+// ----------------------------------------------------------- k_rows_tile ----
+// Dense A v in the A^T v kernel's geometry: 512-column tiles, the (tile, row)
+// unit space split evenly over blocks, so both passes stream A with the same
+// coalesced 4 KB row chunks.  A warp keeps its tile's slice of v in registers
+// (loaded once per segment) and reduces one row chunk per step; the per-(tile,
+// row) sums go to `part` and k_tile_combine adds them in tile order.
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, const double* __restrict__ x,
+                                                             XS xs, Epi epi, double* __restrict__ part) {
+  constexpr int TW = 2 * kNT;  // 512 columns: 16 per lane, 8 x 128-bit loads per row chunk
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) return;  // k_tile_combine owns idle()
+  xs.load();
+  ktimer_begin(epi.timer());
+  const int64_t m = A.m, n = A.n, lda = A.lda;
+  const int64_t nct = (n + TW - 1) / TW;
+  const int64_t U = nct * m;
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t u = U0; u < U1;) {
+    const int64_t ct = u / m, r0 = u - ct * m;
+    const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
+    const int64_t cb = ct * TW;
+    const bool full = cb + TW <= n;
+    double2 xv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t c = cb + 64 * k + 2 * lane;
+      xv[k].x = (c < n) ? xs(__ldg(x + c)) : 0.0;
+      xv[k].y = (c + 1 < n) ? xs(__ldg(x + c + 1)) : 0.0;
+    }
+    for (int64_t r = r0 + wid; r < r1; r += kWarps) {
+      const double* row = A.a + r * lda + cb + 2 * lane;
+      double a0 = 0.0, a1 = 0.0;
+      if (full) {
+        double2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = ld_stream2(row + 64 * k);
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          a0 = fma(v[k].x, xv[k].x, a0); a0 = fma(v[k].y, xv[k].y, a0);
+          a1 = fma(v[k + 1].x, xv[k + 1].x, a1); a1 = fma(v[k + 1].y, xv[k + 1].y, a1);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t c = cb + 64 * k + 2 * lane;
+          if (c < n) a0 = fma(ld_stream(row + 64 * k), xv[k].x, a0);
+          if (c + 1 < n) a1 = fma(ld_stream(row + 64 * k + 1), xv[k].y, a1);
+        }
+      }
+      const double sum = warp_reduce(a0 + a1, RED_SUM);
+      if (lane == 0) part[ct * m + r] = sum;
+    }
+    u += r1 - r0;
+  }
+}
+
+// y_r = sum over tiles (fixed order) of part[tile][r]; then the pass epilogue
+template <class Epi>
+__global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, const double* __restrict__ part,
+                                                     Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  const int64_t stride = (int64_t)gridDim.x * kNT;
+  for (int64_t r = (int64_t)blockIdx.x * kNT + threadIdx.x; r < m; r += stride) {
+    double y = __ldcg(part + r);
+    for (int64_t t = 1; t < nct; ++t) y += __ldcg(part + t * m + r);
+    epi.elem(r, y, acc);
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+  }
+  if (arrive_last(wk.done, gridDim.x, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, nullptr, (int)gridDim.x, red, sm, epi);
+    if (threadIdx.x == 0) {
+      ktimer_end(epi.timer());
       epi.finish(red);
     }
     __syncthreads();
