@@ -365,11 +365,13 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
       A->planT.kind = PLAN_TILE;
       A->planT.vw = vw;
       A->planT.P = tile_grid(m, n, A->sms, vw);
-      // TMA-streamed A^T v (TS_DENSE_T=ldg keeps the register-staged tile kernel)
+      // TMA-streamed A^T v: TS_DENSE_T=tma (measured ~4 % slower than the
+      // register-staged tile kernel on C2, kept for experiments)
       const char* te = getenv("TS_DENSE_T");
-      if (!(te && !strcmp(te, "ldg")) && vw == 2) {
+      if (te && !strcmp(te, "tma") && vw == 2) {
         A->planT.kind = PLAN_TMA;
-        A->planT.P = std::max(1, std::min(tile_grid(m, n, A->sms, 2), A->sms * 2));
+        const int per_sm = std::max(1, std::min(2, (227 * 1024 - 4096) / kTmaSmem));
+        A->planT.P = std::max(1, std::min(tile_grid(m, n, A->sms, 2), A->sms * per_sm));
       }
       // A v in the A^T v tile geometry: TS_DENSE_N=tile (measured slower than the flat split)
       const char* fe = getenv("TS_DENSE_N");

@@ -649,8 +649,14 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
 // per-block streams with no register staging; 256 consumer threads own two
 // columns each and accumulate from shared memory.  Partial tiles at block
 // boundaries are merged exactly like k_cols_tile (same reduction order).
-constexpr int kTmaRows = 4;
-constexpr int kTmaStages = 6;
+#ifndef TS_TMA_ROWS
+#define TS_TMA_ROWS 8
+#endif
+#ifndef TS_TMA_STAGES
+#define TS_TMA_STAGES 3
+#endif
+constexpr int kTmaRows = TS_TMA_ROWS;
+constexpr int kTmaStages = TS_TMA_STAGES;
 constexpr int kTmaTW = 2 * kNT;  // tile width (columns)
 constexpr int kTmaSmem = kTmaStages * kTmaRows * kTmaTW * 8;
 
@@ -723,12 +729,15 @@ __global__ void __launch_bounds__(kNT, 2) k_cols_tma(DenseRows A, const double* 
       const int stage = g % kTmaStages;
       const unsigned phase = (unsigned)((g / kTmaStages) & 1);
       const int rows = (int)((r1 - r < kTmaRows) ? r1 - r : kTmaRows);
+      double xr_[kTmaRows];  // x for this group, fetched before waiting on the data
+#pragma unroll
+      for (int i = 0; i < kTmaRows; ++i) xr_[i] = (i < rows) ? xs(__ldg(x + r + i)) : 0.0;
       mbar_wait(&full[stage], phase);
       const double* sbuf = ring + (size_t)stage * kTmaRows * kTmaTW + 2 * threadIdx.x;
 #pragma unroll
       for (int i = 0; i < kTmaRows; ++i) {
         if (i < rows) {
-          const double xr = xs(__ldg(x + r + i));
+          const double xr = xr_[i];
           const double2 v = *reinterpret_cast<const double2*>(sbuf + (size_t)i * kTmaTW);
           if (i & 1) {
             if (one) ax1 = fma(v.x, xr, ax1);
