@@ -153,7 +153,7 @@ struct Instance {
     TS_CHECK(alloc(&wk.facc, (size_t)pmax * kKMax));
     TS_CHECK(alloc(&wk.bpart, (size_t)pmax * 2));
     TS_CHECK(alloc(&wk.tpart, (size_t)pmax * 2 * kCW));
-    TS_CHECK(alloc(&wk.npart, (size_t)std::max<int64_t>(M.kind == 0 ? npart_elems(M.m, M.n) : 0, 1)));
+    TS_CHECK(alloc(&wk.npart, (size_t)std::max<int64_t>(M.npart, 1)));
     TS_CHECK(alloc(&wk.cnt, (size_t)pmax));
     TS_CHECK(alloc(&wk.done, 4));
     wk.pmax = pmax;
@@ -750,7 +750,7 @@ int ts_matvec(const ts_matrix* A, const double* x, double* y, void* stream) {
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->kind == 0 ? npart_elems(A->m, A->n) : 0));
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
     double *dx, *dy;
     TS_CHECK(stage_in(ar, x, A->n, &dx));
     TS_CHECK(ar.get(&dy, A->m));
@@ -770,7 +770,7 @@ int ts_rmatvec(const ts_matrix* A, const double* x, double* y, void* stream) {
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->kind == 0 ? npart_elems(A->m, A->n) : 0));
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
     double *dx, *dy;
     TS_CHECK(stage_in(ar, x, A->m, &dx));
     TS_CHECK(ar.get(&dy, A->n));
@@ -790,7 +790,7 @@ int ts_gram_matvec(const ts_matrix* A, const double* x, double* y, void* stream)
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->kind == 0 ? npart_elems(A->m, A->n) : 0));
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
     double *dx, *dt, *dy;
     TS_CHECK(stage_in(ar, x, A->n, &dx));
     TS_CHECK(ar.get(&dt, A->m));
@@ -1066,7 +1066,7 @@ int ts_time_pass(const ts_matrix* A, int32_t trans, int32_t reps, double* avg_ms
   {
     Arena ar(st);
     Work wk;
-    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->kind == 0 ? npart_elems(A->m, A->n) : 0));
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
     double *dx, *dy;
     const int64_t nin = trans ? A->m : A->n, nout = trans ? A->n : A->m;
     TS_CHECK(ar.get(&dx, nin));

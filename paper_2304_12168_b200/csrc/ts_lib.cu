@@ -258,6 +258,24 @@ __global__ void k_rowptr_from_keys(const int* keys, int64_t nnz, int64_t ncols, 
   }
 }
 
+__global__ void k_tile_keys(const int* ci, int64_t nnz, int* tkey) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    tkey[k] = ci[k] / kCtTW;
+}
+__global__ void k_gather_ctile(const int* perm, const int* rowid, const int* ci, const double* val,
+                               int64_t nnz, int64_t m, double* tval, uint16_t* tci, int* qkey) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int k = perm[j];
+    const int c = ci[k];
+    const int t = c / kCtTW;
+    tval[j] = val[k];
+    tci[j] = (uint16_t)(c - t * kCtTW);
+    qkey[j] = (int)(t * m + rowid[k]);
+  }
+}
+
 static int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4096));
@@ -284,7 +302,8 @@ int ts_matrix_destroy(ts_matrix* A) {
   DeviceGuard g(A->dev);
   cudaDeviceSynchronize();
   destroy_instances(A);
-  void* ps[] = {A->a, A->rp, A->ci, A->val, A->rpT, A->ciT, A->valT, A->planN.wrow, A->planT.wrow};
+  void* ps[] = {A->a,    A->rp,   A->ci,  A->val,        A->rpT,       A->ciT, A->valT,
+                A->tval, A->tci,  A->trp, A->tblk, A->planN.wrow, A->planT.wrow};
   for (void* p : ps)
     if (p) cudaFree(p);
   delete A;
@@ -305,7 +324,7 @@ int ts_matrix_info(const ts_matrix* A, int64_t* m, int64_t* n, int64_t* nnz, int
 static int finish_create(ts_matrix* A, cudaStream_t st, Arena& ar) {
   // Frobenius norm once (linalg.py:64-69); cached on the immutable handle
   Work wk;
-  TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->kind == 0 ? npart_elems(A->m, A->n) : 0));
+  TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
   double* dfro;
   TS_CHECK(ar.get(&dfro, 1));
   if (A->kind == 0) {
@@ -356,6 +375,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
       set_error("dense upload failed: %s", cudaGetErrorString(e));
       rc = TS_ECUDA;
     }
+    A->npart = npart_elems(m, n);
     if (!rc) rc = plan_rows_dense(m, n, A->sms, &A->planN, st);
     if (!rc) {
       // 128-bit loads; TS_DENSE_VW=4 selects the 256-bit variants (measured slower)
@@ -476,6 +496,40 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       }
       k_gather_T<<<grid_for(nnz), 256, 0, st>>>(perm_out, rowid, A->val, A->ciT, A->valT, nnz);
       k_rowptr_from_keys<<<grid_for(nnz + 1), 256, 0, st>>>(keys_out, nnz, n, A->rpT);
+      // column-tiled copy for wide long-row A v (C5-like: x does not fit a cache)
+      const char* ce = getenv("TS_CSR_CTILE");
+      const int64_t nct = (n + kCtTW - 1) / kCtTW;
+      const bool want_ct = !(ce && !strcmp(ce, "0")) && m > 0 && nnz / m >= 32 &&
+                           n > 2 * (int64_t)kCtTW && nct * m + 1 < (int64_t)INT32_MAX;
+      if (want_ct) {
+        int *tkey, *qkey;
+        if ((rc = ar.get(&tkey, nz)) || (rc = ar.get(&qkey, nz))) return fail(rc);
+        if (cudaMalloc(&A->tval, nz * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&A->tci, nz * sizeof(uint16_t)) != cudaSuccess ||
+            cudaMalloc(&A->trp, (nct * m + 1) * sizeof(int)) != cudaSuccess) {
+          set_error("cudaMalloc for the column-tiled CSR failed");
+          return fail(TS_ENOMEM);
+        }
+        k_tile_keys<<<grid_for(nnz), 256, 0, st>>>(A->ci, nnz, tkey);
+        k_iota<<<grid_for(nnz), 256, 0, st>>>(perm_in, nnz);
+        int tbits = 1;
+        while (tbits < 31 && ((int64_t)1 << tbits) < nct) ++tbits;
+        size_t tb2 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey, keys_out, perm_in, perm_out, (int)nnz, 0,
+                                        tbits, st);
+        void* tmp2 = tmp;
+        if (tb2 > tmp_bytes && (rc = ar.get((char**)&tmp2, tb2))) return fail(rc);
+        size_t tb3 = std::max(tb2, tmp_bytes);
+        if (cub::DeviceRadixSort::SortPairs(tmp2, tb3, tkey, keys_out, perm_in, perm_out, (int)nnz, 0,
+                                            tbits, st) != cudaSuccess) {
+          set_error("radix sort for the column-tiled CSR failed");
+          return fail(TS_ECUDA);
+        }
+        k_gather_ctile<<<grid_for(nnz), 256, 0, st>>>(perm_out, rowid, A->ci, A->val, nnz, m, A->tval,
+                                                     A->tci, qkey);
+        k_rowptr_from_keys<<<grid_for(nnz + 1), 256, 0, st>>>(qkey, nnz, nct * m, A->trp);
+        A->ct_nct = (int)nct;
+      }
     } else {
       cudaMemsetAsync(A->rpT, 0, (n + 1) * sizeof(int), st);
     }
@@ -491,6 +545,30 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
     }
     if ((rc = plan_rows_csr(rp_h.data(), m, nnz, A->sms, &A->planN, st))) return fail(rc);
     if ((rc = plan_rows_csr(rpT_h.data(), n, nnz, A->sms, &A->planT, st))) return fail(rc);
+    if (A->ct_nct > 0) {
+      // nnz-balanced (tile, row) unit ranges, one per block
+      const int64_t U = (int64_t)A->ct_nct * m;
+      std::vector<int> trp_h((size_t)U + 1);
+      cudaMemcpy(trp_h.data(), A->trp, (U + 1) * sizeof(int), cudaMemcpyDeviceToHost);
+      const int P = A->sms * kCtBlocksPerSM;
+      std::vector<int> blk((size_t)P + 1);
+      for (int b = 0; b <= P; ++b) {
+        const int64_t target = nnz * b / P;
+        blk[b] = b == P ? (int)U
+                        : (int)(std::lower_bound(trp_h.begin(), trp_h.end() - 1, (int)target) -
+                                trp_h.begin());
+      }
+      for (int b = 1; b <= P; ++b) blk[b] = std::max(blk[b], blk[b - 1]);
+      if (cudaMalloc(&A->tblk, (P + 1) * sizeof(int)) != cudaSuccess ||
+          cudaMemcpy(A->tblk, blk.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice) !=
+              cudaSuccess) {
+        set_error("column-tiled CSR plan upload failed");
+        return fail(TS_ECUDA);
+      }
+      A->planN.kind = PLAN_CTILE;
+      A->planN.P = P;
+      A->npart = U;
+    }
     if (nnz > 0) {
       if ((rc = finish_create(A, st, ar))) return fail(rc);
     } else {

@@ -22,7 +22,9 @@
 
 namespace ts {
 
-enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4 };
+enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4,
+                      PLAN_CTILE = 5 };
+
 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans)
 inline int64_t npart_elems(int64_t m, int64_t n) { return ((n + 2 * kNT - 1) / (2 * kNT)) * m; }
@@ -51,6 +53,15 @@ struct Mat {
   double fro = 0.0;
   RowPlan planN, planT;
   int Pmax = 0;  // largest grid any pass of this matrix uses
+  // per-(tile,row) partials a solve's Work needs (dense tile A v, column-tiled CSR)
+  int64_t npart = 0;
+  // column-tiled CSR for wide sparse A v (PLAN_CTILE): entries grouped by
+  // column tile (stable: row-major inside a tile), 16-bit in-tile column index
+  int ct_nct = 0;
+  double* tval = nullptr;
+  uint16_t* tci = nullptr;
+  int* trp = nullptr;   // [ct_nct * m + 1] start of (tile, row) in tval/tci
+  int* tblk = nullptr;  // [P + 1] first (tile,row) unit of each block (nnz-balanced)
   // column shard of a matrix split over ranks (nullptr: unsharded)
   Comm* comm = nullptr;
   int64_t n_global = 0, col_off = 0;
@@ -153,7 +164,17 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
   } else {
     const RowPlan& pl = trans ? M.planT : M.planN;
     const CsrRows acc = trans ? M.csrT() : M.csr();
-    if (pl.kind == PLAN_FLAT)
+    if (pl.kind == PLAN_CTILE) {
+      static bool attr_set = false;
+      if (!attr_set) {
+        cudaFuncSetAttribute(k_csr_ctile<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kCtTW * (int)sizeof(double));
+        attr_set = true;
+      }
+      k_csr_ctile<Epi><<<pl.P, kNT, kCtTW * sizeof(double), st>>>(
+          CtileRows{M.tval, M.tci, M.trp, M.tblk, M.m, M.n, M.ct_nct}, x, xs, epi, wk.npart);
+      k_tile_combine<Epi><<<vec_grid(M.m, M.sms), kNT, 0, st>>>(M.m, M.ct_nct, wk.npart, epi, wk);
+    } else if (pl.kind == PLAN_FLAT)
       k_rows_flat<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk, pl.wrow);
     else if (pl.kind == PLAN_WARP)
       k_rows_warp<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);

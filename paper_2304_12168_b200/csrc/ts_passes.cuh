@@ -823,6 +823,83 @@ __global__ void __launch_bounds__(kNT, 2) k_cols_tma(DenseRows A, const double* 
   }
 }
 
+// ----------------------------------------------------------- k_csr_ctile ----
+// Wide CSR A v (C5: 10^4 rows x 10^6 columns, ~1000 nnz per row) over a
+// column-tiled copy of A: the entries of column tile t (kCtTW columns) form a
+// CSR of their own, rows in order, 16-bit in-tile column indices.  A block
+// owns an nnz-balanced run of (tile, row) units; per tile it stages the tile's
+// slice of v in shared memory once, so every gather is a shared-memory read
+// instead of a random L2 sector (the untiled kernel's limiter).  Each warp
+// streams 32 rows' entries coalesced, stages the exact products, and lane l
+// adds row l's products left to right.  part[t * m + r] is then summed over
+// tiles in order by k_tile_combine.
+struct CtileRows {
+  const double* val;
+  const uint16_t* ci;
+  const int* rp;    // [nct * m + 1]
+  const int* blk;   // [P + 1]
+  int64_t m, n;
+  int nct;
+};
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kCtBlocksPerSM) k_csr_ctile(CtileRows A, const double* __restrict__ x,
+                                                                 XS xs, Epi epi, double* __restrict__ part) {
+  extern __shared__ __align__(16) double xsm[];  // [kCtTW] tile slice of v
+  __shared__ double buf[kWarps][kWCh];
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) return;  // k_tile_combine owns idle()
+  xs.load();
+  ktimer_begin(epi.timer());
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t m = A.m;
+  const int64_t q0 = A.blk[blockIdx.x], q1 = A.blk[blockIdx.x + 1];
+  double* sb = buf[wid];
+  for (int64_t q = q0; q < q1;) {
+    const int64_t t = q / m;
+    const int64_t ra = q - t * m;
+    const int64_t rb = (q1 - t * m < m) ? q1 - t * m : m;  // rows [ra, rb) of tile t
+    const int64_t cb = t * (int64_t)kCtTW;
+    const int64_t cw = (A.n - cb < kCtTW) ? A.n - cb : kCtTW;
+    __syncthreads();  // previous tile's slice fully consumed
+    for (int64_t i = threadIdx.x; i < cw; i += kNT) xsm[i] = xs(__ldg(x + cb + i));
+    __syncthreads();
+    const int* rp = A.rp + t * m;
+    const int64_t ngroups = (rb - ra + 31) / 32;
+    for (int64_t g = wid; g < ngroups; g += kWarps) {
+      const int64_t r = ra + g * 32 + lane;
+      const bool live = r < rb;
+      const int64_t rlast = (ra + g * 32 + 32 < rb) ? ra + g * 32 + 32 : rb;
+      const int kb = live ? __ldg(rp + r) : 0;
+      const int ke = live ? __ldg(rp + r + 1) : 0;
+      const int gb = __shfl_sync(0xffffffffu, kb, 0);
+      const int ge = __ldg(rp + rlast);
+      double sum = 0.0;
+      for (int cs = gb; cs < ge; cs += kWCh) {
+        constexpr int J = kWCh / 32;
+        double vv[J];
+        int cc[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int k = cs + j * 32 + lane;
+          const bool ok = k < ge;
+          vv[j] = ok ? ld_stream(A.val + k) : 0.0;
+          cc[j] = ok ? (int)__ldg(A.ci + k) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xsm[cc[j]]);
+        __syncwarp();
+        const int lo = kb > cs ? kb : cs;
+        const int hi = ke < cs + kWCh ? ke : cs + kWCh;
+        for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, sb[k - cs]);
+        __syncwarp();
+      }
+      if (live) part[t * m + r] = sum;
+    }
+    q = t * m + rb;
+  }
+}
+
 // ----------------------------------------------------------- k_rows_tile ----
 // Dense A v in the A^T v kernel's geometry: 512-column tiles, the (tile, row)
 // unit space split evenly over blocks, so both passes stream A with the same
