@@ -119,6 +119,13 @@ inline int vec_grid(int64_t len, int sms) {
   return (int)g;
 }
 
+// warp-per-row combine: enough warps for the rows, at most one resident wave
+inline int combine_grid(int64_t m, int sms) {
+  int64_t g = (m + kWarps - 1) / kWarps;
+  const int64_t cap = resident_blocks(sms);
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
 inline int tile_grid(int64_t m, int64_t n, int sms, int vw) {
   const int64_t tw = (int64_t)vw * kNT;
   const int64_t nct = (n + tw - 1) / tw;
@@ -140,7 +147,7 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
       if (M.planN.kind == PLAN_TILE) {
         const int64_t nct = (M.n + 2 * kNT - 1) / (2 * kNT);
         k_rows_tile<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk.npart);
-        k_tile_combine<Epi><<<vec_grid(M.m, M.sms), kNT, 0, st>>>(M.m, nct, wk.npart, epi, wk);
+        k_tile_combine<Epi><<<combine_grid(M.m, M.sms), kNT, 0, st>>>(M.m, nct, wk.npart, epi, wk);
       } else if (M.planN.kind == PLAN_FLAT && M.planN.vw == 4)
         k_rows_flat<DenseRows4, Epi><<<M.planN.P, kNT, 0, st>>>(DenseRows4{M.dense()}, x, xs, epi,
                                                                   wk, M.planN.wrow);
@@ -173,7 +180,7 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
       }
       k_csr_ctile<Epi><<<pl.P, kNT, kCtTW * sizeof(double), st>>>(
           CtileRows{M.tval, M.tci, M.trp, M.tblk, M.m, M.n, M.ct_nct}, x, xs, epi, wk.npart);
-      k_tile_combine<Epi><<<vec_grid(M.m, M.sms), kNT, 0, st>>>(M.m, M.ct_nct, wk.npart, epi, wk);
+      k_tile_combine<Epi><<<combine_grid(M.m, M.sms), kNT, 0, st>>>(M.m, M.ct_nct, wk.npart, epi, wk);
     } else if (pl.kind == PLAN_FLAT)
       k_rows_flat<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk, pl.wrow);
     else if (pl.kind == PLAN_WARP)

@@ -845,8 +845,9 @@ struct CtileRows {
 template <class Epi>
 __global__ void __launch_bounds__(kNT, kCtBlocksPerSM) k_csr_ctile(CtileRows A, const double* __restrict__ x,
                                                                  XS xs, Epi epi, double* __restrict__ part) {
-  extern __shared__ __align__(16) double xsm[];  // [kCtTW] tile slice of v
+  extern __shared__ __align__(128) double xsm[];  // [kCtTW] raw tile slice of v (TMA)
   __shared__ double buf[kWarps][kWCh];
+  __shared__ __align__(8) unsigned long long xbar;
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) return;  // k_tile_combine owns idle()
   xs.load();
@@ -854,47 +855,66 @@ __global__ void __launch_bounds__(kNT, kCtBlocksPerSM) k_csr_ctile(CtileRows A, 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t m = A.m;
   const int64_t q0 = A.blk[blockIdx.x], q1 = A.blk[blockIdx.x + 1];
+  if (threadIdx.x == 0) {
+    mbar_init(&xbar, 1);
+    fence_mbar_init();
+  }
   double* sb = buf[wid];
+  unsigned phase = 0;
   for (int64_t q = q0; q < q1;) {
     const int64_t t = q / m;
     const int64_t ra = q - t * m;
     const int64_t rb = (q1 - t * m < m) ? q1 - t * m : m;  // rows [ra, rb) of tile t
     const int64_t cb = t * (int64_t)kCtTW;
     const int64_t cw = (A.n - cb < kCtTW) ? A.n - cb : kCtTW;
-    __syncthreads();  // previous tile's slice fully consumed
-    for (int64_t i = threadIdx.x; i < cw; i += kNT) xsm[i] = xs(__ldg(x + cb + i));
-    __syncthreads();
+    __syncthreads();  // previous slice fully consumed (and barrier init visible)
+    if (threadIdx.x == 0) {  // one bulk copy brings the whole slice
+      const unsigned bytes = (unsigned)((cw * 8 + 15) & ~15);
+      mbar_expect_tx(&xbar, bytes);
+      bulk_g2s(xsm, x + cb, bytes, &xbar);
+    }
     const int* rp = A.rp + t * m;
     const int64_t ngroups = (rb - ra + 31) / 32;
-    for (int64_t g = wid; g < ngroups; g += kWarps) {
+    // row pointers of the warp's first group while the slice is in flight
+    int64_t g = wid;
+    int kb = 0, ke = 0, ge = 0;
+    auto fetch = [&](int64_t gg) {
+      const int64_t r = ra + gg * 32 + lane;
+      const int64_t rlast = (ra + gg * 32 + 32 < rb) ? ra + gg * 32 + 32 : rb;
+      kb = (r < rb) ? __ldg(rp + r) : 0;
+      ke = (r < rb) ? __ldg(rp + r + 1) : 0;
+      ge = __ldg(rp + rlast);
+    };
+    if (g < ngroups) fetch(g);
+    mbar_wait(&xbar, phase);
+    phase ^= 1u;
+    for (; g < ngroups; g += kWarps) {
       const int64_t r = ra + g * 32 + lane;
       const bool live = r < rb;
-      const int64_t rlast = (ra + g * 32 + 32 < rb) ? ra + g * 32 + 32 : rb;
-      const int kb = live ? __ldg(rp + r) : 0;
-      const int ke = live ? __ldg(rp + r + 1) : 0;
       const int gb = __shfl_sync(0xffffffffu, kb, 0);
-      const int ge = __ldg(rp + rlast);
+      const int my_kb = kb, my_ke = ke, my_ge = ge;
+      if (g + kWarps < ngroups) fetch(g + kWarps);  // next group's pointers in flight
       double sum = 0.0;
-      for (int cs = gb; cs < ge; cs += kWCh) {
+      for (int cs = gb; cs < my_ge; cs += kWCh) {
         constexpr int J = kWCh / 32;
         double vv[J];
         int cc[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) {
           const int k = cs + j * 32 + lane;
-          const bool ok = k < ge;
+          const bool ok = k < my_ge;
           vv[j] = ok ? ld_stream(A.val + k) : 0.0;
           cc[j] = ok ? (int)__ldg(A.ci + k) : 0;
         }
 #pragma unroll
-        for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xsm[cc[j]]);
+        for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xs(xsm[cc[j]]));
         __syncwarp();
-        const int lo = kb > cs ? kb : cs;
-        const int hi = ke < cs + kWCh ? ke : cs + kWCh;
+        const int lo = my_kb > cs ? my_kb : cs;
+        const int hi = my_ke < cs + kWCh ? my_ke : cs + kWCh;
         for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, sb[k - cs]);
         __syncwarp();
       }
-      if (live) part[t * m + r] = sum;
+      if (live) part[r * A.nct + t] = sum;
     }
     q = t * m + rb;
   }
@@ -953,37 +973,55 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, cons
         }
       }
       const double sum = warp_reduce(a0 + a1, RED_SUM);
-      if (lane == 0) part[ct * m + r] = sum;
+      if (lane == 0) part[r * nct + ct] = sum;
     }
     u += r1 - r0;
   }
 }
 
-// y_r = sum over tiles (fixed order) of part[tile][r]; then the pass epilogue
+// y_r = sum over tiles of part[r][tile] (row-major partials): one warp per
+// row, lane-strided sums then the fixed xor tree; then the pass epilogue
 template <class Epi>
 __global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, const double* __restrict__ part,
                                                      Epi epi, Work wk) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
+  __shared__ double wacc[kWarps][K];
   __shared__ int sflag;
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  const int64_t stride = (int64_t)gridDim.x * kNT;
-  for (int64_t r = (int64_t)blockIdx.x * kNT + threadIdx.x; r < m; r += stride) {
-    double y = __ldcg(part + r);
-    for (int64_t t = 1; t < nct; ++t) y += __ldcg(part + t * m + r);
-    epi.elem(r, y, acc);
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  for (int64_t r = (int64_t)blockIdx.x * kWarps + wid; r < m; r += W) {
+    const double* pr = part + r * nct;
+    double y0 = 0.0, y1 = 0.0;
+    int64_t t = lane;
+    for (; t + 32 < nct; t += 64) {
+      y0 += __ldcg(pr + t);
+      y1 += __ldcg(pr + t + 32);
+    }
+    if (t < nct) y0 += __ldcg(pr + t);
+    const double y = warp_reduce(y0 + y1, RED_SUM);
+    if (lane == 0) epi.elem(r, y, acc);
   }
-  block_reduce<K>(acc, sm, epi);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wacc[wid][k] = acc[k];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+    for (int k = 0; k < K; ++k) {
+      double v = wacc[0][k];
+      for (int j = 1; j < kWarps; ++j) v = red_combine(epi.op(k), v, wacc[j][k]);
+      wk.bacc[blockIdx.x * kKMax + k] = v;
+    }
   }
   if (arrive_last(wk.done, gridDim.x, &sflag)) {
     double red[K];
