@@ -498,9 +498,12 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       k_gather_T<<<grid_for(nnz), 256, 0, st>>>(perm_out, rowid, A->val, A->ciT, A->valT, nnz);
       k_rowptr_from_keys<<<grid_for(nnz + 1), 256, 0, st>>>(keys_out, nnz, n, A->rpT);
       // column-tiled copy for wide long-row A v (C5-like: x does not fit a cache)
+      // opt-in (TS_CSR_CTILE=1): on C5 it measured 101 us vs 64 us for the flat
+      // long-row kernel (partials + combine + 64 KB smem occupancy outweigh the
+      // shared-memory gathers); kept for further work
       const char* ce = getenv("TS_CSR_CTILE");
       const int64_t nct = (n + kCtTW - 1) / kCtTW;
-      const bool want_ct = !(ce && !strcmp(ce, "0")) && m > 0 && nnz / m >= 32 &&
+      const bool want_ct = (ce && !strcmp(ce, "1")) && m > 0 && nnz / m >= 32 &&
                            n > 2 * (int64_t)kCtTW && nct * m + 1 < (int64_t)INT32_MAX;
       if (want_ct) {
         int *tkey, *qkey;
