@@ -124,6 +124,8 @@ typedef struct {
    * [2] fused vector passes, [3] small scalar kernels */
   double kernel_ms[4];
   int64_t kernel_count[4];
+  double gap_norm;             /* TA family: ||b - b'|| of the final iterate pair */
+  double x_norm;               /* ||x|| of the returned iterate */
 } ts_result;
 
 typedef struct {
@@ -194,6 +196,10 @@ TS_API int ts_matvec(const ts_matrix* a, const double* x, double* y, void* strea
 TS_API int ts_rmatvec(const ts_matrix* a, const double* x, double* y, void* stream);  /* y = A^T x */
 TS_API int ts_gram_matvec(const ts_matrix* a, const double* x, double* y, void* stream); /* y = A^T (A x) */
 TS_API int ts_norm2(const double* v, int64_t len, double* out, void* stream);
+/* r = b - A x (r_out optional), ||r||, and ||A^T r|| (atr_norm optional):
+ * the honest-residual step of every driver (triangle.py:84-89, hybrid.py:102-104) */
+TS_API int ts_residual(const ts_matrix* a, const double* x, const double* b, double* r_out,
+                       double* r_norm, double* atr_norm, void* stream);
 TS_API int ts_dot(const double* u, const double* v, int64_t len, double* out, void* stream);
 
 /* ---- CTA pieces ------------------------------------------------------------ */

@@ -484,3 +484,90 @@ def lp_feasibility(a, b, eps, rho_max=None, max_iters=100_000):
     return dict(status=status, detail=detail, x=x, iterations=it, trace=trace, rho=rho,
                 lower_bound=lb, min_x_entry=float(x.min()) if n else 0.0,
                 residual_norm=nrm(fr), normal_residual_norm=nrm(rmv(a, fr)))
+
+
+# --------------------------------------------------------------------------
+# next rows: min-norm bisection (triangle.py:254-330) and hybrid (hybrid.py)
+# --------------------------------------------------------------------------
+def min_norm_solve(a, b, eps, x_eps, inner_cap=250_000, max_iters=4_000_000):
+    """min_norm_solve (triangle.py:254-330); the outer trace rows carry the
+    bracket events 'shrink' / 'expand'."""
+    b = np.asarray(b, dtype=np.float64)
+    if nrm(b) == 0.0:
+        raise ValueError("b must be nonzero")
+    x_eps = np.asarray(x_eps, dtype=np.float64)
+    start_gap = nrm(b - mv(a, x_eps))
+    if start_gap > eps * (1.0 + 1e-9):
+        raise ValueError("x_eps is not an eps-approximate solution")
+    floor = 1e-14 * fro(a) * nrm(b)
+    hi, lo = nrm(x_eps), 0.0
+    best = x_eps.copy()
+    warm = None
+    trace, it, status, detail = [], 0, MIN_NORM, ""
+    budget = max(8, int(math.ceil(math.log2(max(hi / eps, 2.0)))) + 8)
+    for _ in range(budget):
+        if hi - lo <= eps or it >= max_iters:
+            break
+        rho = 0.5 * (hi + lo)
+        if rho <= 0.0:
+            break
+        inner = ta_in_ball(a, b, rho, 0.25 * eps, eps_prime=floor,
+                           max_iters=min(inner_cap, max_iters - it), x0=warm)
+        for row in inner["trace"]:
+            trace.append((it + row[0],) + tuple(row[1:]))
+        it += inner["iterations"]
+        gap = nrm(b - inner["b_prime"])
+        if inner["status"] == APPROX:
+            best = inner["x"]
+            hi = min(rho, nrm(inner["x"]))
+            warm = inner["x"]
+            trace.append((it, hi, gap, 0.0, "shrink"))
+        elif inner["status"] == WITNESS:
+            lo = min(max(lo, inner["lower_bound"]), hi)
+            warm = inner["x"]
+            trace.append((it, lo, gap, 0.0, "expand"))
+        elif inner["status"] == NORMAL_EQ:
+            out = dict(status=NORMAL_EQ, iterations=it, trace=trace, rho=rho,
+                       rho_interval=(lo, hi), detail="pivot direction vanished during bisection")
+            return _finish(out, a, b, inner["x"])
+        else:
+            status = inner["status"]
+            detail = ("inner membership test exhausted its budget" if status == CAP
+                      else "non-finite iterate")
+            break
+    if status == MIN_NORM and hi - lo > eps:
+        status, detail = CAP, "bisection budget exhausted"
+    out = dict(status=status, iterations=it, trace=trace, rho=hi, rho_interval=(lo, hi),
+               detail=detail)
+    return _finish(out, a, b, best)
+
+
+def hybrid_solve(a, b, eps_cta=1e-8, eps_ta=1e-15, want_min_norm=False, t_max=5, h_mode="aat",
+                 max_iters_stage1=100_000, max_iters_stage2=400_000, min_norm_inner_cap=250_000):
+    """hybrid_solve (hybrid.py:59-111)."""
+    b = np.asarray(b, dtype=np.float64)
+    bn = nrm(b)
+    n = a.shape[1]
+    if bn == 0.0:
+        return dict(status=APPROX, x=np.zeros(n), residual_norm=0.0, normal_residual_norm=0.0,
+                    iterations=0, trace=[], detail="")
+    s1 = cta_solve(a, b, epsilon=eps_cta, t_max=t_max, h_mode=h_mode, max_iters=max_iters_stage1)
+    if s1["status"] == APPROX and want_min_norm:
+        eps2 = max(eps_ta * bn, 1.01 * s1["residual_norm"])
+        s2 = min_norm_solve(a, b, eps2, s1["x"], inner_cap=min_norm_inner_cap,
+                            max_iters=max_iters_stage2)
+        status, x = s2["status"], s2["x"]
+    elif s1["status"] == APPROX:
+        s2 = ta_adaptive(a, b, eps=eps_ta * bn, max_iters=max_iters_stage2, x0=s1["x"])
+        status = s2["status"]
+        x = s2["x"] if s2["residual_norm"] <= s1["residual_norm"] else s1["x"]
+    else:
+        g = rmv(a, b)
+        s2 = ta_adaptive(Gram(a), g, eps=eps_ta * nrm(g), max_iters=max_iters_stage2, x0=s1["x"])
+        x = s2["x"] if s2["normal_residual_norm"] <= s1["normal_residual_norm"] else s1["x"]
+        status = NORMAL_EQ if s2["status"] == APPROX else s2["status"]
+    fr = b - mv(a, x)
+    return dict(status=status, x=x, residual_norm=nrm(fr), normal_residual_norm=nrm(rmv(a, fr)),
+                iterations=s1["iterations"] + s2["iterations"], detail=s2.get("detail", ""),
+                trace=[], stage_status=(s1["status"], s2["status"]),
+                stage_iterations=(s1["iterations"], s2["iterations"]))

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(_HERE, "_lib", "libtris
 EXPORTS = (
     "ts_abi_version", "ts_last_error", "ts_device_count",
     "ts_matrix_create_dense", "ts_matrix_create_csr", "ts_matrix_destroy", "ts_matrix_info",
-    "ts_matvec", "ts_rmatvec", "ts_gram_matvec", "ts_norm2", "ts_dot",
+    "ts_matvec", "ts_rmatvec", "ts_gram_matvec", "ts_norm2", "ts_dot", "ts_residual",
     "ts_moments", "ts_hankel_min_norm", "ts_cta_step", "ts_time_pass",
     "ts_cta_solve", "ts_ta_adaptive", "ts_ta_in_ball", "ts_lp_feasibility",
     "ts_comm_create", "ts_comm_connect", "ts_comm_destroy", "ts_matrix_set_shard",
@@ -53,7 +53,8 @@ class Result(C.Structure):
                 ("detail_value", C.c_double), ("trace_rows", C.c_int64),
                 ("has_lower_bound", C.c_int32), ("trivial", C.c_int32),
                 ("elapsed_ms", C.c_double), ("kernel_launches", C.c_int64),
-                ("kernel_ms", C.c_double * 4), ("kernel_count", C.c_int64 * 4)]
+                ("kernel_ms", C.c_double * 4), ("kernel_count", C.c_int64 * 4),
+                ("gap_norm", C.c_double), ("x_norm", C.c_double)]
 
 
 class CtaOptions(C.Structure):
@@ -106,6 +107,7 @@ def _declare(lib):
         "ts_gram_matvec": ([_P, _P, _P, _P], C.c_int),
         "ts_norm2": ([_P, _I64, _P, _P], C.c_int),
         "ts_dot": ([_P, _P, _I64, _P, _P], C.c_int),
+        "ts_residual": ([_P, _P, _P, _P, C.POINTER(_D), C.POINTER(_D), _P], C.c_int),
         "ts_moments": ([_P, _I32, _P, _I32, _P, _P, _P, _P], C.c_int),
         "ts_hankel_min_norm": ([_P, _I32, _I32, _D, _P, _P], C.c_int),
         "ts_cta_step": ([_P, _I32, _P, _P, _I32, _D, _P, _P, C.POINTER(_I32), C.POINTER(_D),

@@ -88,6 +88,8 @@ def build_result(kind, res: N.Result, x, trace: Trace, **extra) -> SolveResult:
     out.kernel_launches = int(res.kernel_launches)
     out.kernel_ms = tuple(float(v) for v in res.kernel_ms)
     out.kernel_count = tuple(int(v) for v in res.kernel_count)
+    out.gap_norm = float(res.gap_norm)
+    out.x_norm = float(res.x_norm)
     return out
 
 

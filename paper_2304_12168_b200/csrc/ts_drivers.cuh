@@ -358,6 +358,8 @@ static void fill_result(const SolveState& s, ts_result* r) {
     r->kernel_ms[i] = s.kt[i].total_ns * 1e-6;
     r->kernel_count[i] = s.kt[i].count;
   }
+  r->gap_norm = s.gap_norm;
+  r->x_norm = s.x_norm;
 }
 
 // ================================================================== TA ====
@@ -514,6 +516,9 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
     EpiFinalNR enr;
     enr.st = ds; enr.out = nullptr;
     TS_CHECK(K.op_apply_t(st, I->fr, enr, 0));
+    EpiXNorm en;  // ||x|| for the min-norm bisection (triangle.py:306)
+    en.st = ds; en.v = I->x;
+    TS_CHECK(vecpass(M, no, en, wk, st));
   }
   TS_CHECK(c.read_state());
   if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, no * sizeof(double), cudaMemcpyDefault, st));
@@ -804,6 +809,60 @@ int ts_gram_matvec(const ts_matrix* A, const double* x, double* y, void* stream)
     TS_CUDA(cudaMemcpyAsync(y, dy, A->n * sizeof(double), cudaMemcpyDefault, st));
   }
   TS_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+struct EpiResid {
+  static constexpr int K = 1;
+  const double* b;
+  double* r;
+  double* out;
+  __device__ int op(int) const { return RED_SUM; }
+  __device__ bool active() const { return true; }
+  __device__ void idle() const {}
+  __device__ KTimer* timer() const { return nullptr; }
+  __device__ void finish_block() const {}
+  __device__ void count_launch() const {}
+  __device__ void elem(int64_t i, double y, double (&acc)[K]) const {
+    const double f = __dsub_rn(b[i], y);
+    r[i] = f;
+    acc[0] = fma(f, f, acc[0]);
+  }
+  __device__ void finish(double (&red)[K]) const { *out = sqrt(red[0]); }
+};
+
+int ts_residual(const ts_matrix* A, const double* x, const double* b, double* r_out,
+                double* r_norm, double* atr_norm, void* stream) {
+  TS_CHECK_HANDLE(A);
+  if (!x || !b) TS_INVAL("null argument");
+  if (A->comm) TS_INVAL("not supported on a column-sharded matrix");
+  DeviceGuard g(A->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  double hn[2] = {0.0, 0.0};
+  {
+    Arena ar(st);
+    Work wk;
+    TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
+    double *dx, *db, *dr, *dn, *dt;
+    TS_CHECK(stage_in(ar, x, A->n, &dx));
+    TS_CHECK(stage_in(ar, b, A->m, &db));
+    TS_CHECK(ar.get(&dr, A->m));
+    TS_CHECK(ar.get(&dt, A->n));
+    TS_CHECK(ar.get(&dn, 2));
+    EpiResid er{db, dr, dn};
+    TS_CHECK(pass(*A, 0, dx, XS{}, er, wk, st));
+    if (atr_norm) {
+      EpiStore es;
+      es.y = dt;
+      es.sq = dn + 1;
+      TS_CHECK(pass(*A, 1, dr, XS{}, es, wk, st));
+    }
+    if (r_out) TS_CUDA(cudaMemcpyAsync(r_out, dr, A->m * sizeof(double), cudaMemcpyDefault, st));
+    TS_CUDA(cudaMemcpyAsync(hn, dn, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    TS_CUDA(cudaStreamSynchronize(st));
+  }
+  if (r_norm) *r_norm = hn[0];
+  if (atr_norm) *atr_norm = sqrt(hn[1]);
   return 0;
 }
 

@@ -298,6 +298,16 @@ struct EpiNormTo : EpiBase {
   }
 };
 
+// ||x|| of the final iterate (always active; after the loop)
+struct EpiXNorm : EpiBase {
+  static constexpr int K = 1;
+  static constexpr unsigned kShardMask = 1u;
+  const double* v;
+  __device__ bool active() const { return true; }
+  __device__ void elem(int64_t i, double (&acc)[K]) const { acc[0] = fma(v[i], v[i], acc[0]); }
+  __device__ void finish(double (&r)[K]) const { st->x_norm = sqrt(r[0]); }
+};
+
 // x = warm ? x0 : 0
 struct EpiCopyWarm : EpiBase {
   static constexpr int K = 1;

@@ -200,6 +200,24 @@ def norm2(v) -> float:
     return float(out.value)
 
 
+def residual(a, x, b, want_normal: bool = True, want_vector: bool = False):
+    """``r = b - A x`` on the device: returns ``(||r||, ||A^T r||)`` (and ``r``
+    with ``want_vector``) — the honest-residual step of the drivers
+    (triangle.py:84-89, hybrid.py:102-104)."""
+    dm, gram = as_device_matrix(a)
+    if gram:
+        raise TypeError("residual() expects a matrix, not a GramProduct")
+    m, n = dm.shape
+    x = _as_vec(x, n, "x has length {got}, expected {want}")
+    b = _as_vec(b, m, "b has length {got}, expected {want}")
+    rn, an = C.c_double(), C.c_double()
+    r = np.empty(m) if want_vector else None
+    N.check(N.lib().ts_residual(dm.handle, N.ptr(x), N.ptr(b), r.ctypes.data if r is not None else None,
+                                C.byref(rn), C.byref(an) if want_normal else None, None))
+    out = (float(rn.value), float(an.value) if want_normal else None)
+    return out + (r,) if want_vector else out
+
+
 def dot(u, v) -> float:
     u = np.ascontiguousarray(np.asarray(u, dtype=np.float64)).ravel()
     v = np.ascontiguousarray(np.asarray(v, dtype=np.float64)).ravel()

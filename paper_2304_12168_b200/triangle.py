@@ -13,13 +13,25 @@ operator layer.
 from __future__ import annotations
 
 import ctypes as C
+import math
+import time
 
 import numpy as np
 
 from . import _native as N
 from ._solve import build_result, host_vec, rows_to_trace, trace_buffer
-from .linalg import as_device_matrix, dot, local_slice, matvec, matvec_transpose, norm2, shape_of
-from .results import APPROX_SOLUTION, TRIANGLE_TRACE_COLUMNS, SolveResult, Trace
+from .linalg import (as_device_matrix, dot, local_slice, matvec, matvec_transpose, norm2, residual,
+                     shape_of)
+from .results import (
+    APPROX_SOLUTION,
+    ITERATION_CAP,
+    MIN_NORM_SOLUTION,
+    NORMAL_EQ_SOLUTION,
+    TRIANGLE_TRACE_COLUMNS,
+    WITNESS,
+    SolveResult,
+    Trace,
+)
 
 _REVALIDATE_EVERY = 512   # triangle.py:37 (device cadence)
 _INNER_EPS_FACTOR = 0.25  # triangle.py:43
@@ -124,3 +136,81 @@ def solve_adaptive(a, b, eps, eps_prime=None, rho_cap=None, max_iters=100_000,
         return SolveResult(APPROX_SOLUTION, np.zeros(nn), 0.0, 0.0, 0,
                            Trace(TRIANGLE_TRACE_COLUMNS), rho=0.0)
     return build_result("ta", res, x, trace, rho=float(res.rho))
+
+
+def min_norm_solve(a, b, eps, x_eps, inner_cap=250_000, max_iters=4_000_000) -> SolveResult:
+    """Approximate minimum-norm solution by bisection on the ellipsoid radius
+    (triangle.py:254-330).  Each bisection step is one warm-started device
+    membership loop (``solve_in_ball`` on the cached instance, CUDA-graph
+    WHILE loop); the host keeps only the bracket ``[rho_lo, rho_hi]`` and the
+    outer trace rows, exactly like the reference's driver."""
+    m, n = shape_of(a)
+    b = host_vec(b, m, f"b has shape {np.shape(b)}, expected ({m},)")
+    if norm2(b) == 0.0:
+        raise ValueError("b must be nonzero")
+    dm, gram = as_device_matrix(a)
+    if gram:
+        raise TypeError("min_norm_solve expects a matrix, not a GramProduct")
+    x_eps = host_vec(local_slice(a, x_eps, dm.shape[1]), dm.shape[1], "x_eps has wrong shape")
+    start_gap, _ = residual(dm, x_eps, b, want_normal=False)
+    if start_gap > eps * (1.0 + 1e-9):
+        raise ValueError(
+            f"x_eps is not an eps-approximate solution: ||Ax-b|| = {start_gap:.3e} > {eps:.3e}")
+    zero_floor = 1e-14 * dm.frobenius_norm() * norm2(b)  # floating floor for "||c|| > 0"
+
+    rho_hi = norm2(x_eps)
+    rho_lo = 0.0
+    best_x = np.array(x_eps, copy=True)
+    warm = None
+    trace = Trace(TRIANGLE_TRACE_COLUMNS)
+    t0 = time.perf_counter_ns()
+    iterations = 0
+    status = MIN_NORM_SOLUTION
+    detail = ""
+    device_ms = 0.0
+    launches = 0
+
+    def finish(st, x, **extra):
+        rn, an = residual(dm, x, b)
+        out = SolveResult(st, x, rn, an, iterations, trace, **extra)
+        out.device_ms = device_ms
+        out.kernel_launches = launches
+        return out
+
+    outer_budget = max(8, int(math.ceil(math.log2(max(rho_hi / eps, 2.0)))) + 8)
+    for _ in range(outer_budget):
+        if rho_hi - rho_lo <= eps or iterations >= max_iters:
+            break
+        rho = 0.5 * (rho_hi + rho_lo)
+        if rho <= 0.0:
+            break
+        inner = solve_in_ball(dm, b, rho, 0.25 * eps, eps_prime=zero_floor,
+                              max_iters=min(inner_cap, max_iters - iterations), x0=warm)
+        device_ms += inner.device_ms or 0.0
+        launches += inner.kernel_launches or 0
+        for row in inner.trace.rows:  # iteration_offset (triangle.py:300)
+            trace.rows.append((iterations + row[0],) + tuple(row[1:]))
+        iterations += inner.iterations
+        wall = time.perf_counter_ns() - t0
+        gap = inner.gap_norm
+        if inner.status == APPROX_SOLUTION:
+            best_x = inner.x
+            rho_hi = min(rho, inner.x_norm)
+            warm = inner.x
+            trace.append(iterations, rho_hi, gap, 0.0, "shrink", wall)
+        elif inner.status == WITNESS:
+            rho_lo = min(max(rho_lo, inner.lower_bound), rho_hi)
+            warm = inner.x
+            trace.append(iterations, rho_lo, gap, 0.0, "expand", wall)
+        elif inner.status == NORMAL_EQ_SOLUTION:
+            return finish(NORMAL_EQ_SOLUTION, inner.x, rho=rho, rho_interval=(rho_lo, rho_hi),
+                          detail="pivot direction vanished during bisection")
+        else:
+            status = inner.status
+            detail = ("inner membership test exhausted its budget"
+                      if inner.status == ITERATION_CAP else "non-finite iterate")
+            break
+
+    if status == MIN_NORM_SOLUTION and rho_hi - rho_lo > eps:
+        status, detail = ITERATION_CAP, "bisection budget exhausted"
+    return finish(status, best_x, rho=rho_hi, rho_interval=(rho_lo, rho_hi), detail=detail)

@@ -23,7 +23,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-EVENTS = ("pivot", "expand", "witness")
+EVENTS = ("pivot", "expand", "witness", "shrink")
 
 
 def pytest_configure(config):
@@ -60,6 +60,11 @@ class Golden:
         self.trace_columns = tuple(str(c) for c in z["trace_columns"])
         self.extras = {k: (z[k] if z[k].ndim else float(z[k]))
                        for k in ("rho", "lower_bound", "min_x_entry", "b_prime") if k in z.files}
+        self.x_eps = z["x_eps"] if "x_eps" in z.files else None
+        self.rho_interval = tuple(z["rho_interval"]) if "rho_interval" in z.files else None
+        self.stage_status = [str(v) for v in z["stage_status"]] if "stage_status" in z.files else None
+        self.stage_iterations = ([int(v) for v in z["stage_iterations"]]
+                                 if "stage_iterations" in z.files else None)
 
 
 @pytest.fixture(params=golden_names())
@@ -76,7 +81,12 @@ def trace_rows_numeric(rows, columns):
         for col, v in zip(columns, row):
             if col == "wall_ns":
                 continue
-            vals.append(float(EVENTS.index(v)) if col == "event" else float(v))
+            if col == "event":
+                vals.append(float(EVENTS.index(v)))
+            elif col == "stage":
+                vals.append(1.0 if v == "stage1" else 2.0)
+            else:
+                vals.append(float(v))
         out.append(vals)
     return np.array(out, dtype=np.float64).reshape(len(rows), len(columns) - 1)
 

@@ -51,6 +51,15 @@ def _probe_case(seed):
     return rng.standard_normal((m, n)), rng.standard_normal(m)
 
 
+def _mn_under(seed):
+    rng = np.random.default_rng(seed)
+    m = int(rng.integers(2, 6))
+    n = int(rng.integers(m + 1, 12))
+    a = rng.standard_normal((m, n))
+    x0 = rng.standard_normal(n)
+    return a, a @ x0, x0
+
+
 def _c(w):
     return (w.a, w.b)
 
@@ -120,6 +129,28 @@ CASES = [
     ("lp_random_feasible", lambda: _rand_feasible_lp(1), "lp", dict(eps=1e-8, max_iters=400000)),
     ("lp_sparse_feasible", lambda: (lambda w: (w.a, w.b))(W.lp_columns(8, 40, 3, seed=11)), "lp",
      dict(eps_rel=1e-6, max_iters=200000)),
+    # --- min-norm bisection (min_norm_solve) -------------------------------------
+    ("mn_identity", lambda: (np.eye(2), np.array([1.0, 0.0]), np.array([1.0, 0.0])), "mn",
+     dict(eps=1e-6)),
+    ("mn_wide_row", lambda: (np.array([[1.0, 1.0]]), np.array([2.0]), np.array([2.0, 0.0])), "mn",
+     dict(eps=1e-6)),
+    ("mn_underdetermined", lambda: _mn_under(6), "mn", dict(eps=1e-6)),
+    ("mn_bisection", lambda: (lambda r: (lambda a, x0: (a, a @ x0, x0))(
+        r.standard_normal((3, 7)), r.standard_normal(7)))(np.random.default_rng(7)), "mn",
+     dict(eps=1e-7)),
+    ("mn_ne_branch", lambda: (np.array([[1.0, 0.0], [0.0, 0.0]]), np.array([1.0, 0.5]),
+                              np.array([1.0, 0.0])), "mn", dict(eps=0.6)),
+    # --- hybrid CTA -> TA (hybrid_solve) --------------------------------------
+    ("hy_min_norm", lambda: (lambda r: (lambda a: (a, a @ r.standard_normal(5)))(
+        r.standard_normal((2, 5))))(np.random.default_rng(0)), "hybrid",
+     dict(eps_cta=1e-8, eps_ta=1e-8, want_min_norm=True)),
+    ("hy_overdetermined", lambda: (lambda r: (r.standard_normal((5, 2)), r.standard_normal(5)))(
+        np.random.default_rng(1)), "hybrid", dict(eps_cta=1e-8, eps_ta=1e-9)),
+    ("hy_consistent", lambda: (lambda r: (lambda a: (a, a @ r.standard_normal(6)))(
+        r.standard_normal((3, 6))))(np.random.default_rng(2)), "hybrid",
+     dict(eps_cta=1e-6, eps_ta=1e-12)),
+    ("hy_c2_lowrank", lambda: _c(W.dense_lowrank(60, 200, 20, seed=9)), "hybrid",
+     dict(eps_cta=1e-8, eps_ta=1e-10)),
 ]
 
 

@@ -70,15 +70,29 @@ def _call(solver, a, b, kw):
         return trisolve.solve_in_ball(a, b, **kw), kw
     if solver == "lp":
         return trisolve.nonnegative_feasibility(a, b, **kw), kw
+    if solver == "hybrid":
+        return trisolve.hybrid_solve(a, b, trisolve.HybridOptions(**kw)), kw
     raise KeyError(solver)
 
 
 def record_case(name, builder, solver, kw):
-    a, b = builder()
-    res, resolved = _call(solver, a, b, kw)
+    built = builder()
+    a, b = built[0], built[1]
+    if solver == "mn":
+        res = trisolve.min_norm_solve(a, b, x_eps=built[2], **kw)
+        resolved = dict(kw)
+    else:
+        res, resolved = _call(solver, a, b, kw)
     d = {}
     _store_matrix(d, a)
     d["b"] = np.asarray(b, dtype=np.float64)
+    if len(built) > 2:
+        d["x_eps"] = np.asarray(built[2], dtype=np.float64)
+    if res.rho_interval is not None:
+        d["rho_interval"] = np.asarray(res.rho_interval, dtype=np.float64)
+    if res.stage_results:
+        d["stage_status"] = np.array([r.status for r in res.stage_results])
+        d["stage_iterations"] = np.array([r.iterations for r in res.stage_results])
     d["solver"] = solver
     d["kwargs"] = json.dumps(resolved)
     d["status"] = res.status
@@ -102,7 +116,12 @@ def record_case(name, builder, solver, kw):
         for col, v in zip(cols, row):
             if col == "wall_ns":
                 continue
-            vals.append(EVENT[v] if col == "event" else float(v))
+            if col == "event":
+                vals.append(float(EVENT.get(v, {"shrink": 3}.get(v, 4))))
+            elif col == "stage":
+                vals.append(1.0 if v == "stage1" else 2.0)
+            else:
+                vals.append(float(v))
         num.append(vals)
     d["trace"] = np.array(num, dtype=np.float64).reshape(len(rows), len(cols) - 1)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)

@@ -27,6 +27,10 @@ def run_oracle(g):
         return port.ta_in_ball(g.a, g.b, **kw)
     if g.solver == "lp":
         return port.lp_feasibility(g.a, g.b, **kw)
+    if g.solver == "mn":
+        return port.min_norm_solve(g.a, g.b, x_eps=g.x_eps, **kw)
+    if g.solver == "hybrid":
+        return port.hybrid_solve(g.a, g.b, **kw)
     raise KeyError(g.solver)
 
 
@@ -40,8 +44,14 @@ def test_oracle_matches_reference(golden):
     # last-ulp allowance only for BLAS kernel selection differences
     assert rel_l2(out["x"], g.x) <= 1e-14
     assert out["residual_norm"] == pytest.approx(g.residual_norm, rel=1e-12, abs=1e-300)
+    if g.solver == "hybrid":  # merged trace is host bookkeeping; check the stages instead
+        assert list(out["stage_status"]) == g.stage_status
+        assert list(out["stage_iterations"]) == g.stage_iterations
+        return
+    if g.rho_interval is not None:
+        np.testing.assert_allclose(out["rho_interval"], g.rho_interval, rtol=1e-12, atol=1e-300)
     tr = np.array([[float(v) if not isinstance(v, str) else
-                    float(("pivot", "expand", "witness").index(v)) for v in row]
+                    float(("pivot", "expand", "witness", "shrink").index(v)) for v in row]
                    for row in out["trace"]], dtype=np.float64).reshape(len(out["trace"]), g.trace.shape[1])
     assert tr.shape == g.trace.shape
     np.testing.assert_allclose(tr, g.trace, rtol=1e-12, atol=0)
