@@ -24,9 +24,14 @@ from conftest import EVENTS, Golden, golden_names, rel_l2, trace_rows_numeric
 pytestmark = pytest.mark.gpu
 
 CHAOTIC = {"cta_c1_cap", "ta_c1_500", "ta_c1_revalidate", "cta_c3_clement", "ta_sparse_c3",
-           "cta_c4_convdiff",
-           # long warm-started bisections / staged solves: outcome-level parity
-           "mn_underdetermined", "mn_bisection", "hy_min_norm", "hy_c2_lowrank"}
+           "cta_c4_convdiff"}
+# Warm-started bisections / staged solves whose iteration count is not stable
+# even for the reference: perturbing the inputs by 1e-15 moves the oracle's
+# totals over 289..512 (mn_underdetermined), 363..567 (mn_bisection),
+# 192..234 (hy_c2_lowrank), 70..1266 (hy_min_norm).  Parity there is the
+# outcome: status (and stage statuses), the certified bracket, ||x|| and the
+# residual against the tolerance the solve certifies.
+OUTCOME = {"mn_underdetermined", "mn_bisection", "hy_min_norm", "hy_c2_lowrank"}
 # cases whose tolerances are looser than the window but still tight
 LOOSE_X = {"cta_sym_diag": 1e-7, "ta_diag": 1e-7, "ta_restart": 1e-6, "ta_gram": 1e-6,
            "ball_random_inside": 1e-7, "lp_random_feasible": 1e-6, "lp_sparse_feasible": 1e-6,
@@ -61,6 +66,22 @@ def test_golden_parity(name):
     res = run_device(g)
     assert res.status == g.status, (res, g.status, g.detail, res.detail)
     bn = float(np.linalg.norm(g.b))
+    if name in OUTCOME:
+        if g.stage_status is not None:
+            assert [r.status for r in res.stage_results] == g.stage_status
+        if g.status == "min_norm_solution":
+            eps = g.kwargs.get("eps")
+            if eps is None:  # hybrid: eps2 = max(eps_ta ||b||, 1.01 stage-1 residual)
+                eps = max(g.kwargs["eps_ta"] * bn, 1.01 * res.stage_results[0].residual_norm)
+            lo, hi = res.rho_interval
+            assert hi - lo <= eps * (1 + 1e-9)
+            assert abs(np.linalg.norm(res.x) - np.linalg.norm(g.x)) <= 2 * eps
+            assert res.residual_norm <= eps
+        else:  # normal-equation outcome of the hybrid: certified normal residual
+            g_norm = float(np.linalg.norm(g.a.T @ g.b))
+            assert res.normal_residual_norm <= max(2 * g.normal_residual_norm,
+                                                   g.kwargs["eps_ta"] * g_norm * (1 + 1e-9))
+        return
     # final relative residual within a factor of 2 (north_star), floor at the
     # cancellation level of b - A x
     floor = 1e-11 * bn
