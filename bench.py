@@ -47,16 +47,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "TA/CTA iterations/s & time to rel. residual 1e-8; matvec-pair HBM GB/s"
 CONFIGS = {
-    "c1": dict(gen="c1", solver="cta", eps=1e-8, max_iters=10000,
+    "c1": dict(gen="c1", solver="cta", eps=1e-8, max_iters=10000, cpu_max_iters=2000,
                desc="C1 dense gaussian 1000x1000, CTA eps=1e-8, cap 10000"),
-    "c2": dict(gen="c2", solver="cta", eps=1e-8, max_iters=100000,
+    "c2": dict(gen="c2", solver="cta", eps=1e-8, max_iters=100000, cpu_max_iters=100000,
                desc="C2 dense rank-2000 5000x20000 (variance reading), CTA eps=1e-8"),
-    "c3": dict(gen="c3", solver="cta", eps=1e-8, max_iters=2000,
+    "c3": dict(gen="c3", solver="cta", eps=1e-8, max_iters=2000, cpu_max_iters=2000,
                desc="C3 Clement variant n=100001 CSR, CTA eps=1e-8, fixed budget 2000 iterations"),
-    "c4": dict(gen="c4", solver="cta", eps=1e-8, max_iters=600,
+    "c4": dict(gen="c4", solver="cta", eps=1e-8, max_iters=600, cpu_max_iters=100,
                desc="C4 upwind conv-diff n=1e6 CSR, CTA eps=1e-8, fixed budget 600 iterations"),
-    "c5": dict(gen="c5", solver="lp", eps=1e-6, max_iters=100000,
+    "c5": dict(gen="c5", solver="lp", eps=1e-6, max_iters=100000, cpu_max_iters=100000,
                desc="C5 LP 1e4 x 1e6 CSR+CSC, TA non-negativity eps=1e-6*||b|| (stalls @11)"),
+    "c5ta": dict(gen="c5", solver="ta", eps=1e-6, max_iters=100000, cpu_max_iters=100000,
+                 desc="C5 LP matrix, unconstrained TA (solve_adaptive) eps=1e-6*||b||"),
 }
 
 
@@ -177,13 +179,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- reference ---
-def run_oracle_step(cfg, w):
+def run_oracle_step(cfg, w, bounded=False):
     from oracle import port
 
     bn = float(np.linalg.norm(w.b))
+    cap = cfg["cpu_max_iters"] if bounded else cfg["max_iters"]
     if cfg["solver"] == "cta":
-        return port.cta_solve(w.a, w.b, epsilon=cfg["eps"], max_iters=cfg["max_iters"])
-    return port.lp_feasibility(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cfg["max_iters"])
+        return port.cta_solve(w.a, w.b, epsilon=cfg["eps"], max_iters=cap)
+    if cfg["solver"] == "ta":
+        return port.ta_adaptive(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
+    return port.lp_feasibility(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
 
 
 def reference_arm(args, cfg):
@@ -191,12 +196,12 @@ def reference_arm(args, cfg):
     if rank != 0:
         return 0
     w = make_workload(cfg)
-    for _ in range(args.warmup):
-        run_oracle_step(cfg, w)
+    for _ in range(min(args.warmup, 1)):
+        run_oracle_step(cfg, w, bounded=True)
     iters = 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        out = run_oracle_step(cfg, w)
+        out = run_oracle_step(cfg, w, bounded=True)
         iters += out["iterations"]
     dt = time.perf_counter() - t0
     val = iters / dt
@@ -210,8 +215,9 @@ def reference_arm(args, cfg):
         "config": {"workload": cfg["desc"], "step": "one full solve, reference stopping rule",
                    "status": out["status"], "iterations_per_step": out["iterations"]},
         "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full solves (oracle/port.py, numpy+OpenBLAS "
-                                   f"{cores} threads; same calls as the reference)"},
+                         "sample": f"{args.steps} solves capped at {cfg['cpu_max_iters']} "
+                                   f"iterations (oracle/port.py, numpy+OpenBLAS {cores} threads; "
+                                   "same calls as the reference)"},
         "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -224,6 +230,8 @@ def solve_once(ts, cfg, dm, b, bn):
     if cfg["solver"] == "cta":
         return ts.centering_solve(dm, b, ts.CenteringOptions(epsilon=cfg["eps"],
                                                              max_iters=cfg["max_iters"]))
+    if cfg["solver"] == "ta":
+        return ts.solve_adaptive(dm, b, eps=cfg["eps"] * bn, max_iters=cfg["max_iters"])
     return ts.nonnegative_feasibility(dm, b, eps=cfg["eps"] * bn, max_iters=cfg["max_iters"])
 
 
@@ -429,7 +437,7 @@ def e2e_measure(ts, cfg, w, bn, args, dev, world):
 
 def cpu_baseline(cfg, w):
     t0 = time.perf_counter()
-    out = run_oracle_step(cfg, w)
+    out = run_oracle_step(cfg, w, bounded=True)
     dt = time.perf_counter() - t0
     cores = blas_threads()
     return {"value": out["iterations"] / dt, "unit": "iterations/s", "cores": cores,
