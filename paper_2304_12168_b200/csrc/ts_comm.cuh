@@ -111,6 +111,7 @@ struct EpiSymStore {
   __device__ KTimer* timer() const { return e.timer(); }
   __device__ void finish_block() const {}
   __device__ void count_launch() const { e.count_launch(); }
+  __device__ void prepare(double* smem) { e.prepare(smem); }
   __device__ void elem(int64_t i, double v, double (&)[K]) const {
     c.sym[slot_base(c, *c.epoch + 1) + i] = v;
   }
@@ -129,6 +130,7 @@ struct EpiDefer {
   __device__ KTimer* timer() const { return e.timer(); }
   __device__ void finish_block() const {}
   __device__ void count_launch() const { e.count_launch(); }
+  __device__ void prepare(double* smem) { e.prepare(smem); }
   __device__ void elem(int64_t i, double y, double (&acc)[K]) const { e.elem(i, y, acc); }
   __device__ void elem(int64_t i, double (&acc)[K]) const { e.elem(i, acc); }
   __device__ void finish(double (&red)[K]) const {
@@ -187,7 +189,9 @@ __global__ void __launch_bounds__(kNT) k_ar_vec(int64_t len, Epi epi, Work wk, C
     return;
   }
   const unsigned long long e = *c.epoch + 1;
-  comm_barrier(c, e);
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  comm_barrier(c, e);  // (its __syncthreads also publishes epi_smem)
   const size_t base = slot_base(c, e);
   double acc[K];
 #pragma unroll

@@ -58,6 +58,7 @@ constexpr int kWarps = kNT / 32;  // warps per block
 constexpr int kKMax = 8;          // max reduction slots per pass
 constexpr int kCW = 4 * kNT;      // max dense A^T tile width (columns): up to 4 per thread
 constexpr int kTMax = 8;          // max CTA order supported on device
+constexpr int kEpiSmem = kTMax * kTMax + 16;  // per-block scratch for Epi::prepare
 constexpr int kCtTW = 8192;       // column-tiled CSR: tile width (x slice 64 KB in smem)
 constexpr int kCtBlocksPerSM = 3; // 3 x 64 KB x slices per SM
 

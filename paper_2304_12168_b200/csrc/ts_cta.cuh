@@ -285,9 +285,16 @@ struct EpiCtaCand : EpiBase {
   static constexpr int K = kTMax;
   KrylovPtrs kp;
   int64_t m;
+  int t_c = 0;
+  const double* al_s = nullptr;  // block copy of alpha_o (shared memory)
   __device__ bool active() const { return running(st); }
+  __device__ void prepare(double* smem) {
+    t_c = st->t;
+    for (int k = threadIdx.x; k < kTMax * kTMax; k += kNT) smem[k] = (&st->alpha_o[0][0])[k];
+    al_s = smem;
+  }
   __device__ void elem(int64_t j, double (&acc)[K]) const {
-    const int t = st->t;
+    const int t = t_c;
     const double rj = kp.p[0][j];
     double pv[kTMax];
 #pragma unroll
@@ -298,7 +305,7 @@ struct EpiCtaCand : EpiBase {
       double cv = rj;
 #pragma unroll
       for (int i = 0; i < kTMax; ++i)
-        if (i < o) cv = __dsub_rn(cv, __dmul_rn(st->alpha_o[o - 1][i], pv[i]));
+        if (i < o) cv = __dsub_rn(cv, __dmul_rn(al_s[(o - 1) * kTMax + i], pv[i]));
       acc[o - 1] = fma(cv, cv, acc[o - 1]);
     }
   }
@@ -349,12 +356,23 @@ struct EpiCtaUpd : EpiBase {
   double* x;
   int64_t m, n;
   int gram;
+  int o_c = 0, blend_c = 0;
+  double w_c = 0.0;
+  const double* al_s = nullptr;
   __device__ bool active() const { return running(st); }
+  __device__ void prepare(double* smem) {
+    o_c = st->sel_order;
+    blend_c = st->blend;
+    w_c = st->w_blend;
+    if (o_c >= 1)
+      for (int k = threadIdx.x; k < kTMax; k += kNT) smem[k] = st->alpha_o[o_c - 1][k];
+    al_s = smem;
+  }
   __device__ void elem(int64_t j, double (&acc)[K]) const {
-    const int o = st->sel_order;
-    const double* al = st->alpha_o[o - 1];
-    const int blend = st->blend;
-    const double w = st->w_blend;
+    const int o = o_c;
+    const double* al = al_s;
+    const int blend = blend_c;
+    const double w = w_c;
     double rold = 0.0, rnew = 0.0;
     if (j < m) {
       rold = kp.p[0][j];
@@ -408,9 +426,11 @@ struct EpiProbeUpd : EpiBase {
   const double* x;
   int64_t m, n;
   int gram, j;
+  double pal_c = 0.0;
   __device__ bool active() const { return probe_on(st, j); }
+  __device__ void prepare(double*) { pal_c = st->probe_alpha; }
   __device__ void elem(int64_t i, double (&)[K]) const {
-    const double al = st->probe_alpha;
+    const double al = pal_c;
     double yo = 0.0;
     if (i < m) yo = (j == 1) ? kp.p[0][i] : pp.y[i];
     if (i < n) {
@@ -486,9 +506,11 @@ struct EpiProbeTake : EpiBase {  // x = x_hat; r = b - A x_hat (when refined win
   const double *xh, *fr2;
   double *x, *r;
   int64_t m, n;
+  int take_c = 0;
   __device__ bool active() const { return true; }
+  __device__ void prepare(double*) { take_c = st->probe_take; }
   __device__ void elem(int64_t i, double (&)[K]) const {
-    if (!st->probe_take) return;
+    if (!take_c) return;
     if (i < n) x[i] = xh[i];
     if (i < m) r[i] = fr2[i];
   }

@@ -189,6 +189,7 @@ struct EpiFroDense {
   __device__ KTimer* timer() const { return nullptr; }
   __device__ void finish_block() const {}
   __device__ void count_launch() const {}
+  __device__ void prepare(double*) {}
   __device__ void elem(int64_t i, double (&acc)[K]) const {
     const double v = a[(i / n) * lda + (i % n)];
     acc[0] = fma(v, v, acc[0]);
@@ -205,6 +206,7 @@ struct EpiFroVals {
   __device__ KTimer* timer() const { return nullptr; }
   __device__ void finish_block() const {}
   __device__ void count_launch() const {}
+  __device__ void prepare(double*) {}
   __device__ void elem(int64_t i, double (&acc)[K]) const { acc[0] = fma(v[i], v[i], acc[0]); }
   __device__ void finish(double (&r)[K]) const { *out = sqrt(r[0]); }
 };
@@ -219,6 +221,7 @@ struct EpiIdxRange {
   __device__ KTimer* timer() const { return nullptr; }
   __device__ void finish_block() const {}
   __device__ void count_launch() const {}
+  __device__ void prepare(double*) {}
   __device__ void elem(int64_t i, double (&acc)[K]) const {
     const double v = (double)ci[i];
     acc[0] = py_min(acc[0], v);

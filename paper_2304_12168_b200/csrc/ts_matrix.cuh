@@ -130,7 +130,7 @@ inline int tile_grid(int64_t m, int64_t n, int sms, int vw) {
   const int64_t tw = (int64_t)vw * kNT;
   const int64_t nct = (n + tw - 1) / tw;
   const int64_t U = nct * m;
-  int64_t g = U / 32;  // >= 32 rows of a tile per block
+  int64_t g = U / 8;  // >= 8 rows of a tile per block (latency-bound sizes want more blocks)
   const int64_t pmax = resident_blocks(sms);
   if (g > pmax) g = pmax;
   if (g < 1) g = 1;

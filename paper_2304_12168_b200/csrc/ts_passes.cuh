@@ -30,6 +30,9 @@
 //   __device__ KTimer* timer() const;       live accounting slot or nullptr
 //   __device__ void finish_block() const;   whole last block, after finish()
 //   __device__ void count_launch() const;   block 0 / thread 0 at entry
+//   __device__ void prepare(double* smem);   all threads at entry: cache device-state
+//                                            scalars (registers / block smem) so
+//                                            elem() never chains on global loads
 #pragma once
 
 #include "ts_common.cuh"
@@ -252,6 +255,9 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_flat(Acc A, const doub
   xs.load();
   KTimer* kt = epi.timer();
   ktimer_begin(kt);
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int64_t P = gridDim.x, b = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t E = A.total();
@@ -393,6 +399,9 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const dou
   xs.load();
   KTimer* kt = epi.timer();
   ktimer_begin(kt);
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int64_t P = gridDim.x, b = blockIdx.x, m = A.rows();
   const int64_t R0 = m * b / P, R1 = m * (b + 1) / P;
   double acc[K];
@@ -440,6 +449,9 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
   xs.load();
   KTimer* kt = epi.timer();
   ktimer_begin(kt);
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t m = A.m;
   const int64_t ngroups = (m + 31) / 32;
@@ -516,6 +528,9 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
   xs.load();
   KTimer* kt = epi.timer();
   ktimer_begin(kt);
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int64_t m = A.m, n = A.n, lda = A.lda;
   const int64_t nct = (n + TW - 1) / TW;
   const int64_t U = nct * m;
@@ -676,6 +691,9 @@ __global__ void __launch_bounds__(kNT, 2) k_cols_tma(DenseRows A, const double* 
   xs.load();
   KTimer* kt = epi.timer();
   ktimer_begin(kt);
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int64_t m = A.m, n = A.n, lda = A.lda;
   const int64_t nct = (n + kTmaTW - 1) / kTmaTW;
   const int64_t U = nct * m;
@@ -852,6 +870,9 @@ __global__ void __launch_bounds__(kNT, kCtBlocksPerSM) k_csr_ctile(CtileRows A, 
   if (!epi.active()) return;  // k_tile_combine owns idle()
   xs.load();
   ktimer_begin(epi.timer());
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t m = A.m;
   const int64_t q0 = A.blk[blockIdx.x], q1 = A.blk[blockIdx.x + 1];
@@ -934,6 +955,9 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, cons
   if (!epi.active()) return;  // k_tile_combine owns idle()
   xs.load();
   ktimer_begin(epi.timer());
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int64_t m = A.m, n = A.n, lda = A.lda;
   const int64_t nct = (n + TW - 1) / TW;
   const int64_t U = nct * m;
@@ -993,6 +1017,9 @@ __global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, co
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double acc[K];
 #pragma unroll
@@ -1048,6 +1075,9 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_vec(int64_t len, Epi epi, W
   }
   KTimer* kt = epi.timer();
   ktimer_begin(kt);
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));

@@ -224,6 +224,7 @@ struct EpiBase {
     }
   }
   __device__ __forceinline__ void finish_block() const {}
+  __device__ __forceinline__ void prepare(double*) {}
 };
 
 __device__ __forceinline__ bool running(const SolveState* s) {
@@ -314,7 +315,9 @@ struct EpiCopyWarm : EpiBase {
   const double* src;
   double* dst;
   __device__ bool active() const { return st->status == TS_RUNNING; }
-  __device__ void elem(int64_t i, double (&acc)[K]) const { dst[i] = st->warm ? src[i] : 0.0; }
+  int warm_c = 0;
+  __device__ void prepare(double*) { warm_c = st->warm; }
+  __device__ void elem(int64_t i, double (&acc)[K]) const { dst[i] = warm_c ? src[i] : 0.0; }
   __device__ void finish(double (&)[K]) const {}
 };
 
@@ -370,10 +373,15 @@ struct EpiTaUpd : EpiBase {
   double *bp, *gap, *x;
   int64_t m, n;
   int relu;
+  double al_c = 0.0, scale_c = 0.0;
   __device__ int op(int k) const { return k == 2 ? RED_MIN : RED_SUM; }
   __device__ bool active() const { return st->status == TS_RUNNING && st->event == EV_PIVOT; }
+  __device__ void prepare(double*) {
+    al_c = st->alpha;
+    scale_c = st->scale;
+  }
   __device__ void elem(int64_t i, double (&acc)[K]) const {
-    const double al = st->alpha;
+    const double al = al_c;
     if (i < m) {
       const double nb = __dadd_rn(bp[i], __dmul_rn(al, d[i]));
       const double bi = b[i];
@@ -386,7 +394,7 @@ struct EpiTaUpd : EpiBase {
     if (i < n) {
       double cv = c[i];
       if (relu) cv = (cv >= 0.0 || cv != cv) ? cv : 0.0;
-      const double pre = __dmul_rn(st->scale, cv);
+      const double pre = __dmul_rn(scale_c, cv);
       const double nx = __dadd_rn(__dmul_rn(1.0 - al, x[i]), __dmul_rn(al, pre));
       x[i] = nx;
       acc[2] = py_min(acc[2], nx);
@@ -479,6 +487,7 @@ struct EpiDot {
   __device__ KTimer* timer() const { return nullptr; }
   __device__ void finish_block() const {}
   __device__ void count_launch() const {}
+  __device__ void prepare(double*) {}
   __device__ void elem(int64_t i, double (&acc)[K]) const { acc[0] = fma(u[i], v[i], acc[0]); }
   __device__ void finish(double (&r)[K]) const { *out = sqrt_out ? sqrt(r[0]) : r[0]; }
 };
