@@ -85,7 +85,8 @@ enum {
   TS_DETAIL_CONE_STALL = 9,         /* "no ascent direction in the nonnegative cone section" feasibility.py:433 */
   TS_DETAIL_LEFT_CONE = 10,         /* "iterate left the nonnegative cone"         feasibility.py:447 */
   TS_DETAIL_RADIUS_BUDGET = 11,     /* "radius budget %.3e exhausted"              feasibility.py:460 */
-  TS_DETAIL_ITER_BUDGET = 12        /* "iteration budget exhausted"                feasibility.py:411 */
+  TS_DETAIL_ITER_BUDGET = 12,       /* "iteration budget exhausted"                feasibility.py:411 */
+  TS_DETAIL_DEVICE_WATCHDOG = 13    /* device loop barrier watchdog (library-side; never expected) */
 };
 
 /* trace events (TA / LP `event` column) */

@@ -28,6 +28,7 @@ _DETAILS = {
     10: lambda v: "iterate left the nonnegative cone",                   # feasibility.py:447
     11: lambda v: f"radius budget {v:.3e} exhausted",                    # feasibility.py:460
     12: lambda v: "iteration budget exhausted",                          # feasibility.py:411
+    13: lambda v: "device loop watchdog tripped",                        # library-side
 }
 
 TRACE_ROW_CAP = 1 << 24

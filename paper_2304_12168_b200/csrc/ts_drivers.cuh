@@ -129,6 +129,8 @@ struct Instance {
   double *xs = nullptr;
   KrylovPtrs kp;
   ProbePtrs pp = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // persistent loop barrier (lazily allocated)
+  GridBar* gbar = nullptr;
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -311,13 +313,15 @@ struct SolveCtx {
   }
 
   int run(const BodyFn& body, const GraphFn& gbody,
-          const std::function<int(cudaStream_t)>& maint) {
+          const std::function<int(cudaStream_t)>& maint, const BodyFn* persist = nullptr) {
     TS_CHECK(read_state());
     TS_CHECK(flush());
     static const bool no_graph = getenv("TS_NO_GRAPH") != nullptr;
     while (hs->status == TS_RUNNING) {
       if (hs->maint != MAINT_NONE) {
         TS_CHECK(maint(st));
+      } else if (persist && !no_graph) {
+        TS_CHECK((*persist)(st));
       } else if (!no_graph) {
         if (!I->exec) TS_CHECK(I->build(gbody));
         TS_CUDA(cudaGraphLaunch(I->exec, st));
@@ -643,6 +647,104 @@ static int cta_step_kernels(const Mat& M, const Instance* I, int npairs, int gra
   return vecpass(M, std::max(M.m, M.n), eu, I->wk, s);
 }
 
+// ---- persistent CTA loop (csrc/ts_persist.cuh) ------------------------------
+// TS_PERSIST=1 runs the CTA loop as one cooperative kernel where the plans
+// allow it (opt-in: measured slower than the graph path, see ts_persist.cuh).
+static int persist_mode() {
+  static const int v = [] {
+    const char* e = getenv("TS_PERSIST");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+static bool pdir_from(const Mat& M, int trans, int Pg, PDir* D) {
+  if (M.kind == 0) {
+    D->d = M.dense();
+    if (trans) {
+      if (M.planT.kind != PLAN_TILE || M.planT.vw != 2) return false;
+      D->kind = PK_COLS;
+      D->P = std::min(M.planT.P, Pg);
+    } else {
+      if (M.planN.kind != PLAN_TILE) return false;
+      D->kind = PK_TILE;
+      D->P = std::min(M.planN.P, Pg);
+      D->Pc = std::min(combine_grid(M.m, M.sms), Pg);
+      D->nct = (M.n + 2 * kNT - 1) / (2 * kNT);
+    }
+    return true;
+  }
+  const RowPlan& pl = trans ? M.planT : M.planN;
+  D->c = trans ? M.csrT() : M.csr();
+  if (pl.kind == PLAN_SHORT) D->kind = PK_SHORT;
+  else if (pl.kind == PLAN_WARP) D->kind = PK_WARP;
+  else return false;
+  D->P = std::min(pl.P, Pg);
+  return true;
+}
+
+// co-resident grid of the persistent kernel (cooperative launch requirement)
+static int persist_grid(const Mat& M) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cta_loop, kNT, 0) != cudaSuccess) nb = 0;
+    per_sm = std::min(nb, blocks_per_sm());
+  }
+  return per_sm * M.sms;
+}
+
+// the loop's stack frame (epilogue objects, the kernel-argument copy) must fit
+// the per-thread stack limit: size it explicitly for the cooperative launch
+static int persist_stack() {
+  static int rc = -1;
+  if (rc < 0) {
+    cudaFuncAttributes fa;
+    size_t cur = 0;
+    rc = 0;
+    if (cudaFuncGetAttributes(&fa, k_cta_loop) != cudaSuccess ||
+        cudaDeviceGetLimit(&cur, cudaLimitStackSize) != cudaSuccess) {
+      rc = 1;
+    } else if (cur < fa.localSizeBytes + 512) {
+      if (cudaDeviceSetLimit(cudaLimitStackSize, fa.localSizeBytes + 512) != cudaSuccess) rc = 1;
+    }
+  }
+  return rc;
+}
+
+static bool cta_persist_setup(const Mat& M, Instance* I, const CtaArgs& a, CtaLoop* L) {
+  const int mode = persist_mode();
+  if (mode != 1 || a.enhanced || M.comm || a.t_max > kTMax) return false;
+  const int Pg = persist_grid(M);
+  if (Pg <= 0 || persist_stack() != 0) return false;
+  PDir T, N;
+  if (a.gram && !pdir_from(M, 1, Pg, &T)) return false;
+  if (!pdir_from(M, 0, Pg, &N)) return false;
+  if (!I->gbar && I->alloc(&I->gbar, 1)) return false;
+  L->st = I->ds;
+  L->kp = I->kp;
+  L->x = I->x;
+  L->m = M.m;
+  L->n = M.n;
+  L->gram = a.gram;
+  L->T = T;
+  L->N = N;
+  L->Pm = std::min(vec_grid(M.m, M.sms), Pg);
+  L->Pmn = std::min(vec_grid(std::max(M.m, M.n), M.sms), Pg);
+  L->wk = I->wk;
+  L->wk.gbar = I->gbar;
+  return true;
+}
+
+static int cta_persist_launch(const Mat& M, Instance* I, CtaLoop& L, cudaStream_t s) {
+  ++g_launches;
+  TS_CUDA(cudaMemsetAsync(I->gbar, 0, sizeof(GridBar), s));
+  void* args[] = {&L};
+  TS_CUDA(cudaLaunchCooperativeKernel((const void*)k_cta_loop, dim3(persist_grid(M)), dim3(kNT), args,
+                                      0, s));
+  return 0;
+}
+
 static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double* x_out,
                      ts_trace_row* trace, int64_t trace_cap, ts_result* res, cudaStream_t st) {
   const int key[4] = {2, a.gram, a.t_max, a.enhanced};
@@ -717,7 +819,10 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     er.st = ds; er.b = I->b; er.r = I->kp.p[0];
     return pass(M, 0, I->x, XS{}, er, wk, s);
   };
-  TS_CHECK(c.run(body, gbody, maint));
+  CtaLoop loop;
+  const bool use_persist = cta_persist_setup(M, I, a, &loop);
+  BodyFn persist = [&](cudaStream_t s) -> int { return cta_persist_launch(M, I, loop, s); };
+  TS_CHECK(c.run(body, gbody, maint, use_persist ? &persist : nullptr));
   if (!c.hs->trivial) {
     EpiFinalR efr;
     efr.st = ds; efr.b = I->b; efr.fr = I->fr;

@@ -15,6 +15,7 @@
 
 #include "ts_cta.cuh"
 #include "ts_comm.cuh"
+#include "ts_persist.cuh"
 
 namespace ts {
 

@@ -156,10 +156,11 @@ struct DenseRows {
     return ((a0 + a1) + (a2 + a3)) + (h + t);
   }
   // whole row, one thread, column order (short-row path)
+  template <bool kCoh = false>
   __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
     const double* row = a + r * lda;
     double s = 0.0;
-    for (int64_t c = 0; c < n; ++c) s = fma(row[c], xs(__ldg(x + c)), s);
+    for (int64_t c = 0; c < n; ++c) s = fma(row[c], xs(ldx<kCoh>(x + c)), s);
     return s;
   }
 };
@@ -207,6 +208,7 @@ struct CsrRows {
     return (a0 + a1) + (a2 + a3);
   }
   // scipy csr_matvec order: sum = 0; sum += A_ij * x_j left to right; no FMA
+  template <bool kCoh = false>
   __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
     const int k0 = __ldg(rp + r), k1 = __ldg(rp + r + 1);
     double s = 0.0;
@@ -220,12 +222,12 @@ struct CsrRows {
         j[u] = ld_stream_i(ci + k + u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = __ldg(x + j[u]);
+      for (int u = 0; u < 4; ++u) xv[u] = ldx<kCoh>(x + j[u]);
 #pragma unroll
       for (int u = 0; u < 4; ++u) s = __dadd_rn(s, __dmul_rn(v[u], xs(xv[u])));
     }
     for (; k < k1; ++k)
-      s = __dadd_rn(s, __dmul_rn(ld_stream(val + k), xs(__ldg(x + ld_stream_i(ci + k)))));
+      s = __dadd_rn(s, __dmul_rn(ld_stream(val + k), xs(ldx<kCoh>(x + ld_stream_i(ci + k)))));
     return s;
   }
 };
@@ -233,6 +235,57 @@ struct CsrRows {
 // block containing flat element p when [0,E) is split as floor(b E / P)
 __device__ __forceinline__ int64_t blk_of(int64_t p, int64_t E, int64_t P) {
   return ((p + 1) * P + E - 1) / E - 1;
+}
+
+// ------------------------------------------------------------ finishers ----
+// Single-kernel pass: the last block to arrive reduces the `nb` block partials
+// (+ split fixes) in fixed order and runs the finisher / finish_block.
+template <class Epi>
+__device__ __forceinline__ void finish_last(Epi& epi, const Work& wk, const double* facc, int nb,
+                                            double* sm, int* sflag) {
+  constexpr int K = Epi::K;
+  if (arrive_last(wk.done, (unsigned)nb, sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, facc, nb, red, sm, epi);
+    if (threadIdx.x == 0) {
+      ktimer_end(epi.timer());
+      epi.finish(red);
+    }
+    __syncthreads();
+    epi.finish_block();
+  }
+}
+
+// Persistent loop: end of a pass phase (all threads of every block of the
+// cooperative grid).  The last block to arrive reduces the first `nb` blocks'
+// partials in the same fixed order, runs the finisher and finish_block, then
+// opens the next generation; the others wait for it.  One atomic per block
+// per phase replaces a kernel boundary.
+template <class Epi>
+__device__ void phase_end(Epi& epi, const Work& wk, const double* facc, int nb) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int slast;
+  unsigned gen0 = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) slast = bar_arrive(wk.gbar, gridDim.x, &gen0) ? 1 : 0;
+  __syncthreads();
+  if (slast) {
+    __threadfence();
+    double red[K];
+    reduce_partials<K>(wk.bacc, facc, nb, red, sm, epi);
+    if (threadIdx.x == 0) {
+      ktimer_end(epi.timer());
+      epi.finish(red);
+    }
+    __syncthreads();
+    epi.finish_block();
+    __syncthreads();
+    if (threadIdx.x == 0) bar_release(wk.gbar, gen0);
+  } else if (threadIdx.x == 0) {
+    bar_wait(wk.gbar, gen0);
+  }
+  __syncthreads();
 }
 
 // ----------------------------------------------------------- k_rows_flat ----
@@ -385,44 +438,41 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_flat(Acc A, const doub
 }
 
 // ---------------------------------------------------------- k_rows_short ----
-template <class Acc, class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const double* __restrict__ x, XS xs,
-                                                    Epi epi, Work wk) {
+template <class Acc, class Epi, bool kP>
+__device__ __forceinline__ void body_rows_short(const Acc& A, const double* __restrict__ x, XS xs,
+                                                Epi& epi, const Work& wk, int64_t b, int64_t P) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
   xs.load();
-  KTimer* kt = epi.timer();
-  ktimer_begin(kt);
+  ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
   __syncthreads();
-  const int64_t P = gridDim.x, b = blockIdx.x, m = A.rows();
+  const int64_t m = A.rows();
   const int64_t R0 = m * b / P, R1 = m * (b + 1) / P;
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  for (int64_t r = R0 + threadIdx.x; r < R1; r += kNT) epi.elem(r, A.row_serial(r, x, xs), acc);
+  for (int64_t r = R0 + threadIdx.x; r < R1; r += kNT)
+    epi.elem(r, A.template row_serial<kP>(r, x, xs), acc);
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
   }
-  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
-    double red[K];
-    reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, epi);
-    if (threadIdx.x == 0) {
-      ktimer_end(kt);
-      epi.finish(red);
-    }
-    __syncthreads();
-    epi.finish_block();
+  if constexpr (!kP) finish_last(epi, wk, nullptr, (int)P, sm, &sflag);
+}
+
+template <class Acc, class Epi>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const double* __restrict__ x, XS xs,
+                                                    Epi epi, Work wk) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
   }
+  body_rows_short<Acc, Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
 }
 
 // ----------------------------------------------------------- k_rows_warp ----
@@ -434,28 +484,22 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const dou
 // reference's, with coalesced HBM traffic instead of per-thread strided rows.
 constexpr int kWCh = 256;  // products staged per warp per chunk
 
-template <class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const double* __restrict__ x,
-                                                             XS xs, Epi epi, Work wk) {
+template <class Epi, bool kP>
+__device__ __forceinline__ void body_rows_warp(const CsrRows& A, const double* __restrict__ x, XS xs,
+                                               Epi& epi, const Work& wk, int64_t b, int64_t P) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ double buf[kWarps][kWCh];
   __shared__ int sflag;
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
   xs.load();
-  KTimer* kt = epi.timer();
-  ktimer_begin(kt);
+  ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t m = A.m;
   const int64_t ngroups = (m + 31) / 32;
-  const int64_t W = (int64_t)gridDim.x * kWarps, w = (int64_t)blockIdx.x * kWarps + wid;
+  const int64_t W = P * kWarps, w = b * kWarps + wid;
   const int64_t g0 = ngroups * w / W, g1 = ngroups * (w + 1) / W;  // contiguous groups per warp
   double acc[K];
 #pragma unroll
@@ -482,7 +526,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
         cc[j] = ok ? ld_stream_i(A.ci + k) : 0;
       }
 #pragma unroll
-      for (int j = 0; j < J; ++j) xv[j] = __ldg(x + cc[j]);  // ... then the gathers
+      for (int j = 0; j < J; ++j) xv[j] = ldx<kP>(x + cc[j]);  // ... then the gathers
 #pragma unroll
       for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xs(xv[j]));
       __syncwarp();
@@ -496,45 +540,40 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+    for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
   }
-  if (arrive_last(wk.done, gridDim.x, &sflag)) {
-    double red[K];
-    reduce_partials<K>(wk.bacc, nullptr, (int)gridDim.x, red, sm, epi);
-    if (threadIdx.x == 0) {
-      ktimer_end(kt);
-      epi.finish(red);
-    }
-    __syncthreads();
-    epi.finish_block();
-  }
+  if constexpr (!kP) finish_last(epi, wk, nullptr, (int)P, sm, &sflag);
 }
 
-// ----------------------------------------------------------- k_cols_tile ----
-// VW columns per thread (2: 128-bit loads, 4: 256-bit loads); tile = VW * kNT
-template <class Epi, int VW>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, const double* __restrict__ x,
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const double* __restrict__ x,
                                                              XS xs, Epi epi, Work wk) {
-  constexpr int K = Epi::K;
-  constexpr int TW = VW * kNT;       // tile width (columns)
-  constexpr int RU = VW == 4 ? 4 : 8;  // rows in flight per thread
-  __shared__ double sm[kWarps * kKMax];
-  __shared__ int sflag;
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
+  body_rows_warp<Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
+}
+
+// ----------------------------------------------------------- k_cols_tile ----
+// VW columns per thread (2: 128-bit loads, 4: 256-bit loads); tile = VW * kNT
+template <class Epi, int VW, bool kP>
+__device__ __forceinline__ void body_cols_tile(const DenseRows& A, const double* __restrict__ x, XS xs,
+                                               Epi& epi, const Work& wk, int64_t b, int64_t P) {
+  constexpr int K = Epi::K;
+  constexpr int TW = VW * kNT;       // tile width (columns)
+  constexpr int RU = VW == 4 ? 4 : 8;  // rows in flight per thread
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
   xs.load();
-  KTimer* kt = epi.timer();
-  ktimer_begin(kt);
+  ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
   __syncthreads();
   const int64_t m = A.m, n = A.n, lda = A.lda;
   const int64_t nct = (n + TW - 1) / TW;
   const int64_t U = nct * m;
-  const int64_t P = gridDim.x, b = blockIdx.x;
   const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
   double acc[K];
 #pragma unroll
@@ -565,20 +604,20 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
           }
         }
 #pragma unroll
-        for (int i = 0; i < RU; ++i) xr[i] = xs(__ldg(x + r + i));
+        for (int i = 0; i < RU; ++i) xr[i] = xs(ldx<kP>(x + r + i));
 #pragma unroll
         for (int i = 0; i < RU; ++i)
 #pragma unroll
           for (int j = 0; j < VW; ++j) ac[i & 1][j] = fma(v[i][j], xr[i], ac[i & 1][j]);
       }
       for (; r < r1; ++r) {
-        const double xr = xs(__ldg(x + r));
+        const double xr = xs(ldx<kP>(x + r));
 #pragma unroll
         for (int j = 0; j < VW; ++j) ac[0][j] = fma(ld_stream(base + r * lda + j), xr, ac[0][j]);
       }
     } else if (nv > 0) {
       for (; r < r1; ++r) {
-        const double xr = xs(__ldg(x + r));
+        const double xr = xs(ldx<kP>(x + r));
         for (int j = 0; j < nv; ++j) ac[0][j] = fma(ld_stream(base + r * lda + j), xr, ac[0][j]);
       }
     }
@@ -644,16 +683,18 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, cons
       if (!end_block) wk.facc[b * kKMax + k] = red_identity(epi.op(k));
     }
   }
-  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
-    double red[K];
-    reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
-    if (threadIdx.x == 0) {
-      ktimer_end(kt);
-      epi.finish(red);
-    }
-    __syncthreads();
-    epi.finish_block();
+  if constexpr (!kP) finish_last(epi, wk, wk.facc, (int)P, sm, &sflag);
+}
+
+template <class Epi, int VW>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, const double* __restrict__ x,
+                                                             XS xs, Epi epi, Work wk) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
   }
+  body_cols_tile<Epi, VW, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------ k_cols_tma ----
@@ -947,12 +988,10 @@ __global__ void __launch_bounds__(kNT, kCtBlocksPerSM) k_csr_ctile(CtileRows A, 
 // coalesced 4 KB row chunks.  A warp keeps its tile's slice of v in registers
 // (loaded once per segment) and reduces one row chunk per step; the per-(tile,
 // row) sums go to `part` and k_tile_combine adds them in tile order.
-template <class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, const double* __restrict__ x,
-                                                             XS xs, Epi epi, double* __restrict__ part) {
+template <class Epi, bool kP>
+__device__ __forceinline__ void body_rows_tile(const DenseRows& A, const double* __restrict__ x, XS xs,
+                                               Epi& epi, double* __restrict__ part, int64_t b, int64_t P) {
   constexpr int TW = 2 * kNT;  // 512 columns: 16 per lane, 8 x 128-bit loads per row chunk
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) return;  // k_tile_combine owns idle()
   xs.load();
   ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
@@ -961,7 +1000,6 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, cons
   const int64_t m = A.m, n = A.n, lda = A.lda;
   const int64_t nct = (n + TW - 1) / TW;
   const int64_t U = nct * m;
-  const int64_t P = gridDim.x, b = blockIdx.x;
   const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int64_t u = U0; u < U1;) {
@@ -973,8 +1011,8 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, cons
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int64_t c = cb + 64 * k + 2 * lane;
-      xv[k].x = (c < n) ? xs(__ldg(x + c)) : 0.0;
-      xv[k].y = (c + 1 < n) ? xs(__ldg(x + c + 1)) : 0.0;
+      xv[k].x = (c < n) ? xs(ldx<kP>(x + c)) : 0.0;
+      xv[k].y = (c + 1 < n) ? xs(ldx<kP>(x + c + 1)) : 0.0;
     }
     for (int64_t r = r0 + wid; r < r1; r += kWarps) {
       const double* row = A.a + r * lda + cb + 2 * lane;
@@ -1003,20 +1041,23 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, cons
   }
 }
 
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, const double* __restrict__ x,
+                                                             XS xs, Epi epi, double* __restrict__ part) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) return;  // k_tile_combine owns idle()
+  body_rows_tile<Epi, false>(A, x, xs, epi, part, blockIdx.x, gridDim.x);
+}
+
 // y_r = sum over tiles of part[r][tile] (row-major partials): one warp per
 // row, lane-strided sums then the fixed xor tree; then the pass epilogue
-template <class Epi>
-__global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, const double* __restrict__ part,
-                                                     Epi epi, Work wk) {
+template <class Epi, bool kP>
+__device__ __forceinline__ void body_tile_combine(int64_t m, int64_t nct, const double* __restrict__ part,
+                                                  Epi& epi, const Work& wk, int64_t b, int64_t P) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ double wacc[kWarps][K];
   __shared__ int sflag;
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
   __syncthreads();
@@ -1024,8 +1065,8 @@ __global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, co
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  const int64_t W = (int64_t)gridDim.x * kWarps;
-  for (int64_t r = (int64_t)blockIdx.x * kWarps + wid; r < m; r += W) {
+  const int64_t W = P * kWarps;
+  for (int64_t r = b * kWarps + wid; r < m; r += W) {
     const double* pr = part + r * nct;
     double y0 = 0.0, y1 = 0.0;
     int64_t t = lane;
@@ -1047,57 +1088,54 @@ __global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, co
     for (int k = 0; k < K; ++k) {
       double v = wacc[0][k];
       for (int j = 1; j < kWarps; ++j) v = red_combine(epi.op(k), v, wacc[j][k]);
-      wk.bacc[blockIdx.x * kKMax + k] = v;
+      wk.bacc[b * kKMax + k] = v;
     }
   }
-  if (arrive_last(wk.done, gridDim.x, &sflag)) {
-    double red[K];
-    reduce_partials<K>(wk.bacc, nullptr, (int)gridDim.x, red, sm, epi);
-    if (threadIdx.x == 0) {
-      ktimer_end(epi.timer());
-      epi.finish(red);
-    }
-    __syncthreads();
-    epi.finish_block();
-  }
+  if constexpr (!kP) finish_last(epi, wk, nullptr, (int)P, sm, &sflag);
 }
 
-// ----------------------------------------------------------------- k_vec ----
 template <class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_vec(int64_t len, Epi epi, Work wk) {
-  constexpr int K = Epi::K;
-  __shared__ double sm[kWarps * kKMax];
-  __shared__ int sflag;
+__global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, const double* __restrict__ part,
+                                                     Epi epi, Work wk) {
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
-  KTimer* kt = epi.timer();
-  ktimer_begin(kt);
+  body_tile_combine<Epi, false>(m, nct, part, epi, wk, blockIdx.x, gridDim.x);
+}
+
+// ----------------------------------------------------------------- k_vec ----
+template <class Epi, bool kP>
+__device__ __forceinline__ void body_vec(int64_t len, Epi& epi, const Work& wk, int64_t b, int64_t P) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
   __syncthreads();
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  const int64_t stride = (int64_t)gridDim.x * kNT;
-  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < len; i += stride) epi.elem(i, acc);
+  const int64_t stride = P * kNT;
+  for (int64_t i = b * kNT + threadIdx.x; i < len; i += stride) epi.elem(i, acc);
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+    for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
   }
-  if (arrive_last(wk.done, gridDim.x, &sflag)) {
-    double red[K];
-    reduce_partials<K>(wk.bacc, nullptr, (int)gridDim.x, red, sm, epi);
-    if (threadIdx.x == 0) {
-      ktimer_end(kt);
-      epi.finish(red);
-    }
-    __syncthreads();
-    epi.finish_block();
+  if constexpr (!kP) finish_last(epi, wk, nullptr, (int)P, sm, &sflag);
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_vec(int64_t len, Epi epi, Work wk) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
   }
+  body_vec<Epi, false>(len, epi, wk, blockIdx.x, gridDim.x);
 }
 
 }  // namespace ts
