@@ -32,6 +32,7 @@
 #ifndef TRISOLVE_B200_H
 #define TRISOLVE_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -122,7 +123,8 @@ typedef struct {
   int64_t kernel_launches;     /* kernels launched by the solve (incl. graph nodes) */
   /* live per-class kernel accounting inside the solve (%globaltimer, earliest
    * block start to last block's finisher): [0] A v passes, [1] A^T v passes,
-   * [2] fused vector passes, [3] small scalar kernels */
+   * [2] fused vector passes, [3] the CTA Hankel solves
+   * (run by the finishing block of the last moments pass) */
   double kernel_ms[4];
   int64_t kernel_count[4];
   double gap_norm;             /* TA family: ||b - b'|| of the final iterate pair */
@@ -191,6 +193,18 @@ TS_API int ts_matrix_destroy(ts_matrix* a);
 /* kind: 0 dense, 1 csr.  frobenius: ||A||_F computed once at creation. */
 TS_API int ts_matrix_info(const ts_matrix* a, int64_t* m, int64_t* n, int64_t* nnz, int32_t* kind,
                    double* frobenius);
+
+/* ---- storage pools --------------------------------------------------------
+ * ts_matrix_destroy retires an unsharded handle (device storage, launch plans,
+ * cached solver instances and their instantiated graphs) into a small
+ * per-process pool; creating a matrix of the same kind and shape on the same
+ * device recycles it, uploading the new entries into the same buffers
+ * (TS_MATRIX_POOL=0 disables).  ts_pool_trim releases retired storage on
+ * `device` (< 0: every device) and the cached pinned host blocks. */
+TS_API int ts_pool_trim(int device);
+/* Page-locked host blocks for solver outputs, cached by size after ts_host_free. */
+TS_API int ts_host_alloc(size_t bytes, void** out);
+TS_API int ts_host_free(void* ptr);
 
 /* ---- operator layer -------------------------------------------------------- */
 TS_API int ts_matvec(const ts_matrix* a, const double* x, double* y, void* stream);   /* y = A x  */

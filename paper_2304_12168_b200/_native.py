@@ -23,6 +23,7 @@ EXPORTS = (
     "ts_moments", "ts_hankel_min_norm", "ts_cta_step", "ts_time_pass",
     "ts_cta_solve", "ts_ta_adaptive", "ts_ta_in_ball", "ts_lp_feasibility",
     "ts_comm_create", "ts_comm_connect", "ts_comm_destroy", "ts_matrix_set_shard",
+    "ts_pool_trim", "ts_host_alloc", "ts_host_free",
 )
 
 # statuses (results.py:11-18)
@@ -100,6 +101,9 @@ def _declare(lib):
         "ts_matrix_create_csr": ([_P, _P, _P, _I64, _I64, _I64, C.c_int, _P, C.POINTER(_P)],
                                  C.c_int),
         "ts_matrix_destroy": ([_P], C.c_int),
+        "ts_pool_trim": ([C.c_int], C.c_int),
+        "ts_host_alloc": ([C.c_size_t, C.POINTER(_P)], C.c_int),
+        "ts_host_free": ([_P], C.c_int),
         "ts_matrix_info": ([_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64),
                             C.POINTER(_I32), C.POINTER(_D)], C.c_int),
         "ts_matvec": ([_P, _P, _P, _P], C.c_int),
@@ -167,6 +171,41 @@ def device_count() -> int:
     if rc != 0:
         return 0
     return int(n.value)
+
+
+class _PinnedBlock:
+    """Owner of one page-locked host block from the library's pool, exposed
+    to numpy through the array interface (the array keeps it alive)."""
+
+    __slots__ = ("_p", "__array_interface__")
+
+    def __init__(self, count: int, dtype):
+        dt = np.dtype(dtype)
+        p = C.c_void_p()
+        check(lib().ts_host_alloc(max(count, 1) * dt.itemsize, C.byref(p)))
+        self._p = p.value
+        self.__array_interface__ = {"shape": (count,), "typestr": dt.str,
+                                    "data": (self._p, False), "version": 3}
+
+    def __del__(self):
+        p = getattr(self, "_p", None)
+        if p and _lib is not None:
+            try:
+                _lib.ts_host_free(p)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._p = None
+
+
+def pinned_empty(count: int, dtype=np.float64) -> np.ndarray:
+    """Uninitialised 1-D numpy array in pinned host memory (result vectors:
+    the device->host copy then runs at full PCIe rate)."""
+    return np.asarray(_PinnedBlock(int(count), dtype))
+
+
+def trim_pools(device: int = -1) -> None:
+    """Release retired matrix storage and cached pinned host blocks."""
+    check(lib().ts_pool_trim(int(device)))
 
 
 def ptr(arr) -> int | None:

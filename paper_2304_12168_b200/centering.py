@@ -201,7 +201,7 @@ def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResul
     o.accel_ratio = float(opts.accel_ratio)
     o.x_start = x_start.ctypes.data if x_start is not None else None
     buf, cap = trace_buffer(opts.max_iters)
-    x = np.empty(n_local)
+    x = N.pinned_empty(n_local)
     res = N.Result()
     N.check(N.lib().ts_cta_solve(dm.handle, N.ptr(b), C.byref(o), x.ctypes.data,
                                  buf.ctypes.data, cap, C.byref(res), None))

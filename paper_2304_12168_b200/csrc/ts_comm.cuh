@@ -122,6 +122,7 @@ struct EpiSymStore {
 template <class Epi>
 struct EpiDefer {
   static constexpr int K = Epi::K;
+  static constexpr bool kPair = kPairOf<Epi>;
   Epi e;
   CommDev c;
   __device__ int op(int k) const { return e.op(k); }
@@ -133,6 +134,9 @@ struct EpiDefer {
   __device__ void prepare(double* smem) { e.prepare(smem); }
   __device__ void elem(int64_t i, double y, double (&acc)[K]) const { e.elem(i, y, acc); }
   __device__ void elem(int64_t i, double (&acc)[K]) const { e.elem(i, acc); }
+  __device__ void elem2(int64_t i, double (&acc)[K]) const {
+    if constexpr (kPair) e.elem2(i, acc);
+  }
   __device__ void finish(double (&red)[K]) const {
     double* s = c.sym + slot_base(c, *c.epoch + 1) + c.vec_cap;
 #pragma unroll

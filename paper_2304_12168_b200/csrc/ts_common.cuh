@@ -93,6 +93,21 @@ __device__ __forceinline__ int ld_stream_i(const int* p) {
   asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+// Epi::kPair when declared, else false (epilogues outside the EpiBase family)
+template <class E>
+constexpr auto pair_of(int) -> decltype(bool(E::kPair)) { return E::kPair; }
+template <class E>
+constexpr bool pair_of(...) { return false; }
+template <class E>
+constexpr bool kPairOf = pair_of<E>(0);
+
+// plain (coherent) 128-bit load / store of an aligned element pair
+__device__ __forceinline__ double2 ld_pair(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ void st_pair(double* p, double2 v) {
+  *reinterpret_cast<double2*>(p) = v;
+}
 // ---- TMA 1-D bulk copies (cp.async.bulk) + mbarrier helpers ---------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

@@ -63,6 +63,116 @@ static int sm_count(int dev) {
   return v;
 }
 
+// ------------------------------------------------------ storage pools ----
+// Retired matrices: ts_matrix_destroy parks an unsharded handle here (device
+// storage, launch plans and its cached solver instances with their
+// instantiated graphs) instead of freeing it; a later create of the same
+// kind and shape on the same device takes it back, uploads the new entries
+// into the same buffers and rebuilds only what depends on them (Frobenius
+// norm; for CSR the transpose and the plan tables).  cudaMalloc / cudaFree
+// of hundreds of MB and graph instantiation then leave the per-call path of
+// a stream of same-shaped solves.  TS_MATRIX_POOL=0 disables it;
+// ts_pool_trim() (and any failing allocation) releases it.
+static std::mutex g_retire_mu;
+static std::vector<Mat*> g_retired;
+constexpr size_t kRetireMax = 2;  // handles kept per process
+
+static bool matrix_pool_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TS_MATRIX_POOL");
+    return !(e && !strcmp(e, "0"));
+  }();
+  return on;
+}
+
+static void free_matrix(Mat* A);
+
+static Mat* retire_take(int dev, int kind, int64_t m, int64_t n, int64_t nnz) {
+  if (!matrix_pool_enabled()) return nullptr;
+  std::lock_guard<std::mutex> g(g_retire_mu);
+  for (size_t i = 0; i < g_retired.size(); ++i) {
+    Mat* A = g_retired[i];
+    if (A->dev == dev && A->kind == kind && A->m == m && A->n == n && A->nnz == nnz) {
+      g_retired.erase(g_retired.begin() + i);
+      return A;
+    }
+  }
+  return nullptr;
+}
+
+static int pool_trim_device(int dev) {  // dev < 0: all devices
+  std::vector<Mat*> drop;
+  {
+    std::lock_guard<std::mutex> g(g_retire_mu);
+    for (size_t i = 0; i < g_retired.size();) {
+      if (dev < 0 || g_retired[i]->dev == dev) {
+        drop.push_back(g_retired[i]);
+        g_retired.erase(g_retired.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+  }
+  for (Mat* A : drop) free_matrix(A);
+  return (int)drop.size();
+}
+
+// cudaMalloc that releases retired storage and retries once on failure
+static cudaError_t dev_malloc(void** p, size_t bytes, int dev) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess && pool_trim_device(dev) > 0) {
+    cudaGetLastError();
+    e = cudaMalloc(p, bytes);
+  }
+  return e;
+}
+template <class T>
+static cudaError_t dev_malloc(T** p, size_t bytes, int dev) {
+  return dev_malloc(reinterpret_cast<void**>(p), bytes, dev);
+}
+
+static void free_plan(RowPlan& p) {
+  if (p.wrow) cudaFree(p.wrow);
+  if (p.chunks) cudaFree(p.chunks);
+  if (p.blk) cudaFree(p.blk);
+  p.wrow = nullptr;
+  p.chunks = nullptr;
+  p.blk = nullptr;
+}
+
+// a new plan replaces `old` in place when the geometry is unchanged (cached
+// graphs bake the grid and the plan-table pointer); false: geometry changed
+static bool adopt_plan(RowPlan& old, RowPlan& nw, cudaStream_t st) {
+  const bool same = old.kind == nw.kind && old.P == nw.P && old.vw == nw.vw &&
+                    old.nchunks == nw.nchunks && (old.wrow != nullptr) == (nw.wrow != nullptr) &&
+                    (old.chunks != nullptr) == (nw.chunks != nullptr);
+  if (same) {
+    if (nw.wrow)
+      cudaMemcpyAsync(old.wrow, nw.wrow, (size_t)nw.P * kWarps * sizeof(int),
+                      cudaMemcpyDeviceToDevice, st);
+    if (nw.chunks) {
+      cudaMemcpyAsync(old.chunks, nw.chunks, (size_t)(nw.nchunks + 1) * sizeof(int2),
+                      cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.blk, nw.blk, (size_t)(nw.P + 1) * sizeof(int), cudaMemcpyDeviceToDevice, st);
+    }
+    cudaStreamSynchronize(st);
+    free_plan(nw);
+  } else {
+    free_plan(old);
+    old = nw;
+  }
+  nw = RowPlan();
+  return same;
+}
+
+// Pinned host blocks for solver outputs (x, b', r): the device->host copy of
+// a result then runs at full PCIe rate instead of through the driver's
+// pageable staging.  Freed blocks are cached by exact size.
+static std::mutex g_host_mu;
+static std::vector<std::pair<size_t, void*>> g_host_free;
+static size_t g_host_cached = 0;
+constexpr size_t kHostCacheMax = (size_t)1 << 31;
+
 // ------------------------------------------------------------ workspace ----
 // Owns stream-ordered allocations for one call.
 struct Arena {
@@ -115,6 +225,49 @@ static void flat_ranges(int64_t E, int64_t P, int64_t b, int wid, int64_t* s, in
   *e = S0 + L * (wid + 1) / kWarps;
 }
 
+// Chunks of <= kStRows rows and <= kStCap entries (greedy, in row order), and
+// an entry-balanced contiguous run of chunks per block (k_rows_stream).
+static int plan_rows_stream(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* out,
+                            cudaStream_t st) {
+  RowPlan p;
+  p.kind = PLAN_STREAM;
+  std::vector<int2> ch;
+  ch.reserve((size_t)(nnz / kStCap + rows / kStRows + 2));
+  int64_t r = 0;
+  while (r < rows) {
+    ch.push_back(make_int2((int)r, rp[r]));
+    int64_t e = r + 1;  // one row always fits (max row length <= kStCap)
+    while (e < rows && e - r < kStRows && rp[e + 1] - rp[r] <= kStCap) ++e;
+    r = e;
+  }
+  ch.push_back(make_int2((int)rows, (int)nnz));
+  p.nchunks = (int)ch.size() - 1;
+  const int64_t pmax = (int64_t)sms * kStBlocks;
+  p.P = (int)std::max<int64_t>(1, std::min<int64_t>(pmax, p.nchunks));
+  std::vector<int> blk((size_t)p.P + 1);
+  for (int b = 0; b <= p.P; ++b) {
+    if (b == p.P) {
+      blk[b] = p.nchunks;
+      continue;
+    }
+    const int64_t target = nnz * b / p.P;
+    int lo = 0, hi = p.nchunks;  // first chunk starting at or after target
+    while (lo < hi) {
+      const int mid = (lo + hi) / 2;
+      if (ch[mid].y < target) lo = mid + 1; else hi = mid;
+    }
+    blk[b] = lo;
+  }
+  for (int b = 1; b <= p.P; ++b) blk[b] = std::max(blk[b], blk[b - 1]);
+  TS_CUDA(cudaMalloc(&p.chunks, ch.size() * sizeof(int2)));
+  TS_CUDA(cudaMalloc(&p.blk, blk.size() * sizeof(int)));
+  TS_CUDA(cudaMemcpyAsync(p.chunks, ch.data(), ch.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaMemcpyAsync(p.blk, blk.data(), blk.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaStreamSynchronize(st));
+  *out = p;
+  return 0;
+}
+
 int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* out,
                   cudaStream_t st) {
   RowPlan p;
@@ -129,10 +282,18 @@ int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* ou
     const char* force = getenv("TS_CSR_SHORT");
     bool thread_rows = nnz < ((int64_t)1 << 21);
     if (force && !strcmp(force, "thread")) thread_rows = true;
-    if (force && !strcmp(force, "warp")) thread_rows = false;
+    if (force && (!strcmp(force, "warp") || !strcmp(force, "stream"))) thread_rows = false;
     p.kind = thread_rows ? PLAN_SHORT : PLAN_WARP;
     int64_t g = thread_rows ? (rows + kNT - 1) / kNT : (rows + kNT * 4 - 1) / (kNT * 4);
     p.P = (int)std::max<int64_t>(1, std::min(g, pmax));
+    // TS_CSR_SHORT=stream: the TMA-streamed chunk kernel (opt-in: bitwise
+    // equal, 16.5 vs 16.6 us bare on C4 in tools/microbench/spmv_short.cu, but
+    // 23.7 vs 21.6 us inside CTA solves, whose epilogues delay its refills)
+    if (!thread_rows && force && !strcmp(force, "stream")) {
+      int64_t maxlen = 0;
+      for (int64_t r = 0; r < rows; ++r) maxlen = std::max<int64_t>(maxlen, rp[r + 1] - rp[r]);
+      if (maxlen <= kStCap) return plan_rows_stream(rp, rows, nnz, sms, out, st);
+    }
     *out = p;
     return 0;
   }
@@ -291,6 +452,21 @@ using namespace ts;
 
 struct ts_matrix : public ts::Mat {};
 
+namespace ts {
+static void free_matrix(Mat* A) {
+  DeviceGuard g(A->dev);
+  cudaDeviceSynchronize();
+  destroy_instances(A);
+  void* ps[] = {A->a,   A->rp,  A->ci,  A->val, A->rpT, A->ciT, A->valT,
+                A->tval, A->tci, A->trp, A->tblk};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  free_plan(A->planN);
+  free_plan(A->planT);
+  delete static_cast<ts_matrix*>(A);
+}
+}  // namespace ts
+
 // ======================================================================= ABI
 extern "C" {
 
@@ -301,16 +477,85 @@ int ts_device_count(int* count) {
   return 0;
 }
 
-int ts_matrix_destroy(ts_matrix* A) {
+
+// A fully built, unsharded, non-column-tiled handle is retired into the
+// storage pool (see retire_take); everything else is freed.
+static int matrix_release(ts_matrix* A, bool complete) {
   if (!A) return 0;
-  DeviceGuard g(A->dev);
-  cudaDeviceSynchronize();
-  destroy_instances(A);
-  void* ps[] = {A->a,    A->rp,   A->ci,  A->val,        A->rpT,       A->ciT, A->valT,
-                A->tval, A->tci,  A->trp, A->tblk, A->planN.wrow, A->planT.wrow};
-  for (void* p : ps)
-    if (p) cudaFree(p);
-  delete A;
+  if (complete && matrix_pool_enabled() && !A->comm && !A->tval) {
+    {
+      DeviceGuard g(A->dev);
+      cudaDeviceSynchronize();  // no solve may still read the storage
+    }
+    Mat* evict = nullptr;
+    {
+      std::lock_guard<std::mutex> g(g_retire_mu);
+      g_retired.push_back(A);
+      if (g_retired.size() > kRetireMax) {
+        evict = g_retired.front();
+        g_retired.erase(g_retired.begin());
+      }
+    }
+    if (evict) free_matrix(evict);
+    return 0;
+  }
+  free_matrix(A);
+  return 0;
+}
+
+int ts_matrix_destroy(ts_matrix* A) { return matrix_release(A, true); }
+
+int ts_pool_trim(int device) {
+  pool_trim_device(device);
+  std::vector<std::pair<size_t, void*>> drop;
+  {
+    std::lock_guard<std::mutex> g(g_host_mu);
+    drop.swap(g_host_free);
+    g_host_cached = 0;
+  }
+  for (auto& kv : drop) cudaFreeHost(static_cast<char*>(kv.second) - 64);
+  return 0;
+}
+
+int ts_host_alloc(size_t bytes, void** out) {
+  if (!out) TS_INVAL("null output pointer");
+  *out = nullptr;
+  bytes = std::max<size_t>(bytes, 64);
+  {
+    std::lock_guard<std::mutex> g(g_host_mu);
+    for (size_t i = g_host_free.size(); i-- > 0;)  // most recently freed first
+      if (g_host_free[i].first == bytes) {
+        *out = g_host_free[i].second;
+        g_host_cached -= bytes;
+        g_host_free.erase(g_host_free.begin() + i);
+        return 0;
+      }
+  }
+  // pinned blocks carry their size in a 64-byte header
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, bytes + 64, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    set_error("cudaHostAlloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    return TS_ENOMEM;
+  }
+  *reinterpret_cast<size_t*>(p) = bytes;
+  *out = static_cast<char*>(p) + 64;
+  return 0;
+}
+
+int ts_host_free(void* ptr) {
+  if (!ptr) return 0;
+  void* base = static_cast<char*>(ptr) - 64;
+  const size_t bytes = *reinterpret_cast<size_t*>(base);
+  {
+    std::lock_guard<std::mutex> g(g_host_mu);
+    if (g_host_cached + bytes <= kHostCacheMax) {
+      g_host_free.emplace_back(bytes, ptr);
+      g_host_cached += bytes;
+      return 0;
+    }
+  }
+  cudaFreeHost(base);
   return 0;
 }
 
@@ -354,6 +599,26 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
   DeviceGuard g(device);
   setup_pool(device);
   cudaStream_t st = (cudaStream_t)stream;
+  if (ts_matrix* R = static_cast<ts_matrix*>(retire_take(device, 0, m, n, m * n))) {
+    // same shape: plans, instances and graphs stay valid; new entries only
+    int rc = 0;
+    {
+      Arena ar(st);
+      cudaError_t e = cudaMemcpy2DAsync(R->a, R->lda * sizeof(double), a, lda * sizeof(double),
+                                        n * sizeof(double), m, cudaMemcpyDefault, st);
+      if (e != cudaSuccess) {
+        set_error("dense upload failed: %s", cudaGetErrorString(e));
+        rc = TS_ECUDA;
+      }
+      if (!rc) rc = finish_create(R, st, ar);
+    }
+    if (rc) {
+      matrix_release(R, false);
+      return rc;
+    }
+    *out = R;
+    return 0;
+  }
   ts_matrix* A = new ts_matrix();
   A->dev = device;
   A->sms = sm_count(device);
@@ -365,7 +630,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
   int rc = 0;
   {
     Arena ar(st);
-    cudaError_t e = cudaMalloc(&A->a, (size_t)A->lda * m * sizeof(double));
+    cudaError_t e = dev_malloc(&A->a, (size_t)A->lda * m * sizeof(double), device);
     if (e != cudaSuccess) {
       set_error("cudaMalloc(dense %lld x %lld) failed: %s", (long long)m, (long long)A->lda,
                 cudaGetErrorString(e));
@@ -408,7 +673,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
     if (!rc) rc = finish_create(A, st, ar);
   }
   if (rc) {
-    ts_matrix_destroy(A);
+    matrix_release(A, false);
     return rc;
   }
   *out = A;
@@ -435,7 +700,9 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
   for (int64_t r = 0; r < m; ++r)
     if (rp_h[r + 1] < rp_h[r]) TS_INVAL("CSR indptr is not nondecreasing at row %lld", (long long)r);
 
-  ts_matrix* A = new ts_matrix();
+  ts_matrix* A = static_cast<ts_matrix*>(retire_take(device, 1, m, n, nnz));
+  const bool reuse = A != nullptr;  // same shape: storage, plans and instances recycled
+  if (!A) A = new ts_matrix();
   A->dev = device;
   A->sms = sm_count(device);
   A->kind = 1;
@@ -444,18 +711,19 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
   A->nnz = nnz;
   int rc = 0;
   auto fail = [&](int code) {
-    ts_matrix_destroy(A);
+    matrix_release(A, false);
     return code;
   };
   {
     Arena ar(st);
     const size_t nz = (size_t)std::max<int64_t>(nnz, 1);
-    if (cudaMalloc(&A->rp, (m + 1) * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&A->ci, nz * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&A->val, nz * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&A->rpT, (n + 1) * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&A->ciT, nz * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&A->valT, nz * sizeof(double)) != cudaSuccess) {
+    // +16 B tails: k_rows_stream's bulk copies round their ranges to 16 bytes
+    if (!reuse && (dev_malloc(&A->rp, (m + 1 + 4) * sizeof(int), device) != cudaSuccess ||
+                   dev_malloc(&A->ci, (nz + 4) * sizeof(int), device) != cudaSuccess ||
+                   dev_malloc(&A->val, (nz + 2) * sizeof(double), device) != cudaSuccess ||
+                   dev_malloc(&A->rpT, (n + 1 + 4) * sizeof(int), device) != cudaSuccess ||
+                   dev_malloc(&A->ciT, (nz + 4) * sizeof(int), device) != cudaSuccess ||
+                   dev_malloc(&A->valT, (nz + 2) * sizeof(double), device) != cudaSuccess)) {
       set_error("cudaMalloc for CSR storage failed (nnz=%lld)", (long long)nnz);
       return fail(TS_ENOMEM);
     }
@@ -551,8 +819,18 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       set_error("CSR transpose failed: %s", cudaGetErrorString(cudaGetLastError()));
       return fail(TS_ECUDA);
     }
-    if ((rc = plan_rows_csr(rp_h.data(), m, nnz, A->sms, &A->planN, st))) return fail(rc);
-    if ((rc = plan_rows_csr(rpT_h.data(), n, nnz, A->sms, &A->planT, st))) return fail(rc);
+    {
+      RowPlan pN, pT;
+      if ((rc = plan_rows_csr(rp_h.data(), m, nnz, A->sms, &pN, st))) return fail(rc);
+      if ((rc = plan_rows_csr(rpT_h.data(), n, nnz, A->sms, &pT, st))) {
+        free_plan(pN);
+        return fail(rc);
+      }
+      const bool keepN = adopt_plan(A->planN, pN, st);
+      const bool keepT = adopt_plan(A->planT, pT, st);
+      // a recycled handle's instances bake the old launch geometry
+      if (reuse && !(keepN && keepT)) destroy_instances(A);
+    }
     if (A->ct_nct > 0) {
       // nnz-balanced (tile, row) unit ranges, one per block
       const int64_t U = (int64_t)A->ct_nct * m;

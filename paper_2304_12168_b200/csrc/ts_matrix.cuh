@@ -23,7 +23,7 @@
 namespace ts {
 
 enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4,
-                      PLAN_CTILE = 5 };
+                      PLAN_CTILE = 5, PLAN_STREAM = 6 };
 
 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans)
@@ -34,6 +34,10 @@ struct RowPlan {
   int P = 1;            // blocks
   int* wrow = nullptr;  // device [P * kWarps] (PLAN_FLAT)
   int vw = 2;           // dense: columns per 128/256-bit load
+  // PLAN_STREAM: chunk table (first row, first entry) and per-block chunk runs
+  int nchunks = 0;
+  int2* chunks = nullptr;  // device [nchunks + 1]
+  int* blk = nullptr;      // device [P + 1]
 };
 
 struct Instance;  // cached solver instance (ts_drivers.cuh)
@@ -185,6 +189,15 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
       k_rows_flat<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk, pl.wrow);
     else if (pl.kind == PLAN_WARP)
       k_rows_warp<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
+    else if (pl.kind == PLAN_STREAM) {
+      static bool attr_set = false;
+      if (!attr_set) {
+        cudaFuncSetAttribute(k_rows_stream<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStSmem);
+        attr_set = true;
+      }
+      k_rows_stream<Epi><<<pl.P, kNT, kStSmem, st>>>(StreamRows{acc.rp, acc.ci, acc.val, pl.chunks, pl.blk},
+                                                     x, xs, epi, wk);
+    }
     else
       k_rows_short<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
   }

@@ -556,6 +556,125 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
   body_rows_warp<Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
 }
 
+// --------------------------------------------------------- k_rows_stream ----
+// Short CSR rows streamed through shared memory by the Tensor Memory
+// Accelerator.  The rows are cut (once, at plan time) into chunks of at most
+// kStRows rows and kStCap entries; a block owns a contiguous, entry-balanced
+// run of chunks.  One thread keeps kStStages chunks in flight with
+// cp.async.bulk copies of the chunk's values, column indices and row
+// pointers (three contiguous byte ranges) completing on a per-stage mbarrier,
+// so HBM sees deep sequential streams that do not wait on the gathers.  The
+// block then forms the exact products v * x in place (all threads, batched
+// gathers) and each thread adds ITS row's products left to right without FMA
+// — scipy's csr_matvec operation sequence, so the result is bitwise the
+// reference's.  Used for HBM-sized short-row matrices (C4; C5's A^T v).
+constexpr int kStCap = 1024;   // entries per chunk
+constexpr int kStRows = 256;   // rows per chunk
+constexpr int kStStages = 4;   // chunks in flight per block
+constexpr int kStBlocks = 4;   // resident blocks per SM (4 x 53.5 KB of stages)
+struct __align__(16) StStage {
+  double val[kStCap + 2];  // +2: the copy starts at the 16-B boundary below e0
+  int idx[kStCap + 4];
+  int rp[kStRows + 8];
+};
+constexpr int kStSmem = kStStages * (int)sizeof(StStage);
+static_assert(sizeof(StStage) % 16 == 0, "stage must keep 16-B alignment");
+
+struct StreamRows {
+  const int* rp;
+  const int* ci;
+  const double* val;
+  const int2* chunks;  // [nchunks + 1] (first row, first entry) of each chunk
+  const int* blk;      // [P + 1] first chunk of each block
+};
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kStBlocks) k_rows_stream(StreamRows A, const double* __restrict__ x,
+                                                               XS xs, Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  extern __shared__ __align__(128) unsigned char st_raw[];
+  StStage* stg = reinterpret_cast<StStage*>(st_raw);
+  __shared__ __align__(8) unsigned long long full[kStStages];
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  const int tid = threadIdx.x;
+  const int c0 = __ldg(A.blk + blockIdx.x), c1 = __ldg(A.blk + blockIdx.x + 1);
+  auto issue = [&](int c, int s) {  // thread 0: bring chunk c into stage s
+    const int2 a = __ldg(A.chunks + c), z = __ldg(A.chunks + c + 1);
+    const int e0v = a.y & ~1, e0i = a.y & ~3, r0 = a.x & ~3;
+    const unsigned bv = (unsigned)(((z.y - e0v) * 8 + 15) & ~15);
+    const unsigned bi = (unsigned)(((z.y - e0i) * 4 + 15) & ~15);
+    const unsigned br = (unsigned)(((z.x + 1 - r0) * 4 + 15) & ~15);
+    mbar_expect_tx(&full[s], bv + bi + br);
+    bulk_g2s(stg[s].val, A.val + e0v, bv, &full[s]);
+    bulk_g2s(stg[s].idx, A.ci + e0i, bi, &full[s]);
+    bulk_g2s(stg[s].rp, A.rp + r0, br, &full[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kStStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kStStages && c0 + s < c1; ++s) issue(c0 + s, s);
+  }
+  xs.load();
+  ktimer_begin(epi.timer());
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  int2 a = c0 < c1 ? __ldg(A.chunks + c0) : make_int2(0, 0);
+  for (int c = c0, g = 0; c < c1; ++c, ++g) {
+    const int s = g % kStStages;
+    const int2 z = __ldg(A.chunks + c + 1);
+    const int ne = z.y - a.y, nr = z.x - a.x;
+    mbar_wait(&full[s], (unsigned)((g / kStStages) & 1));
+    double* sv = stg[s].val + (a.y & 1);
+    const int* si = stg[s].idx + (a.y & 3);
+    const int* sr = stg[s].rp + (a.x & 3);
+    // exact products in place; four independent gathers in flight per thread
+    for (int k0 = tid; k0 < ne; k0 += 4 * kNT) {
+      double xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * kNT;
+        xv[u] = k < ne ? __ldg(x + si[k]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * kNT;
+        if (k < ne) sv[k] = __dmul_rn(sv[k], xs(xv[u]));
+      }
+    }
+    __syncthreads();
+    for (int r = tid; r < nr; r += kNT) {
+      const int kb = sr[r] - a.y, ke = sr[r + 1] - a.y;
+      double sum = 0.0;
+      for (int k = kb; k < ke; ++k) sum = __dadd_rn(sum, sv[k]);
+      epi.elem((int64_t)a.x + r, sum, acc);
+    }
+    __syncthreads();  // stage consumed by every thread
+    if (tid == 0 && c + kStStages < c1) {
+      // the generic-proxy product stores must be ordered before the async
+      // proxy overwrites the stage
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(c + kStStages, s);
+    }
+    a = z;
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+  }
+  finish_last(epi, wk, nullptr, (int)gridDim.x, sm, &sflag);
+}
+
 // ----------------------------------------------------------- k_cols_tile ----
 // VW columns per thread (2: 128-bit loads, 4: 256-bit loads); tile = VW * kNT
 template <class Epi, int VW, bool kP>
@@ -1119,7 +1238,14 @@ __device__ __forceinline__ void body_vec(int64_t len, Epi& epi, const Work& wk, 
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
   const int64_t stride = P * kNT;
-  for (int64_t i = b * kNT + threadIdx.x; i < len; i += stride) epi.elem(i, acc);
+  if constexpr (kPairOf<Epi>) {
+    // pair epilogues: elements (2i, 2i+1) per call with 128-bit loads (twice
+    // the bytes in flight per thread on the multi-vector CTA passes)
+    const int64_t np = (len + 1) >> 1;
+    for (int64_t ip = b * kNT + threadIdx.x; ip < np; ip += stride) epi.elem2(2 * ip, acc);
+  } else {
+    for (int64_t i = b * kNT + threadIdx.x; i < len; i += stride) epi.elem(i, acc);
+  }
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {
 #pragma unroll

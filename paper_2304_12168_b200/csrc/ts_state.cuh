@@ -204,6 +204,9 @@ struct EpiBase {
   int tclass = -1;  // live accounting class (set by the launch helper)
   // vector passes: reduction slots that sum over n-space (column-sharded)
   static constexpr unsigned kShardMask = 0;
+  // vector passes: true -> the epilogue provides elem2(i, acc) for elements
+  // i, i+1 (i even) and k_vec walks pairs
+  static constexpr bool kPair = false;
   __device__ __forceinline__ void count_launch() const {
     if (st) atomicAdd(reinterpret_cast<unsigned long long*>(&st->launches), 1ull);
   }

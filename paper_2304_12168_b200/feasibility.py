@@ -61,7 +61,7 @@ def nonnegative_feasibility(a, b, eps, rho_max=None, max_iters=100_000) -> Solve
     o.max_iters = int(max_iters)
     o.gram = int(gram)
     buf, cap = trace_buffer(max_iters)
-    x = np.empty(nn)
+    x = N.pinned_empty(nn)
     res = N.Result()
     N.check(N.lib().ts_lp_feasibility(dm.handle, N.ptr(b), C.byref(o), x.ctypes.data,
                                       buf.ctypes.data, cap, C.byref(res), None))

@@ -99,8 +99,8 @@ def solve_in_ball(a, b, rho, eps, eps_prime=None, max_iters=100_000, x0=None) ->
     o.x0 = N.ptr(x0v) if x0v is not None else None
     o.gram = int(gram)
     buf, cap = trace_buffer(max_iters)
-    x = np.empty(nn)
-    bp = np.empty(mo)
+    x = N.pinned_empty(nn)
+    bp = N.pinned_empty(mo)
     res = N.Result()
     N.check(N.lib().ts_ta_in_ball(dm.handle, N.ptr(b), C.byref(o), x.ctypes.data, bp.ctypes.data,
                                   buf.ctypes.data, cap, C.byref(res), None))
@@ -127,7 +127,7 @@ def solve_adaptive(a, b, eps, eps_prime=None, rho_cap=None, max_iters=100_000,
     x0v = host_vec(local_slice(a, x0, nn), nn, "x0 has wrong shape") if x0 is not None else None
     o.x0 = N.ptr(x0v) if x0v is not None else None
     buf, cap = trace_buffer(max_iters)
-    x = np.empty(nn)
+    x = N.pinned_empty(nn)
     res = N.Result()
     N.check(N.lib().ts_ta_adaptive(dm.handle, N.ptr(b), C.byref(o), x.ctypes.data,
                                    buf.ctypes.data, cap, C.byref(res), None))

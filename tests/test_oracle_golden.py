@@ -89,3 +89,25 @@ def test_schedule_wave():
     assert [next(gen) for _ in range(12)] == [1, 2, 3, 4, 5, 4, 3, 2, 1, 2, 3, 4]
     gen = port.schedule(1)
     assert [next(gen) for _ in range(3)] == [1, 1, 1]
+
+
+def test_chaotic_bands_cover_the_recorded_and_oracle_runs():
+    """tests/golden/chaotic_bands.json (the reference's own spread under 1e-15
+    input perturbations, recorded by make_bands.py) contains the recorded
+    reference run, and the oracle lands inside the band the device tests use."""
+    import json
+
+    from conftest import Golden
+
+    with open(os.path.join(GOLDEN, "chaotic_bands.json")) as fh:
+        bands = json.load(fh)
+    assert set(bands) == {"cta_c1_cap", "ta_c1_500", "ta_c1_revalidate", "cta_c3_clement",
+                          "ta_sparse_c3", "cta_c4_convdiff"}
+    for name, bd in bands.items():
+        g = Golden(name)
+        assert bd["residual_lo"] <= g.residual_norm <= bd["residual_hi"]
+        assert bd["iterations_lo"] <= g.iterations <= bd["iterations_hi"]
+        if name in ("cta_c1_cap", "ta_c1_500", "ta_c1_revalidate"):
+            continue  # dense: the oracle's BLAS order is the recorded one (checked above)
+        out = run_oracle(g)
+        assert 0.5 * bd["residual_lo"] <= out["residual_norm"] <= 2.0 * bd["residual_hi"]

@@ -11,7 +11,7 @@ for name, iters in [(n, int(i)) for n, i in (a.split(":") for a in sys.argv[1:])
     for _ in range(2):
         r = ts.centering_solve(dm, w.b, ts.CenteringOptions(epsilon=1e-300, max_iters=iters))
     it = r.iterations
-    names = ["A v", "A^T v", "vector", "scalar"]
+    names = ["A v", "A^T v", "vector", "hankel"]
     print(f"{name}: {it} it, device {r.device_ms:.2f} ms = {r.device_ms/it*1e3:.1f} us/it, "
           f"kernels {r.kernel_launches} ({r.kernel_launches/it:.1f}/it)")
     tot = 0.0
