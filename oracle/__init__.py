@@ -14,8 +14,11 @@ Contents
             same numpy/BLAS/LAPACK primitives so its arithmetic matches the
             reference call for call.
 ``mirror``  ctypes binding of ``mirror.c``: a plain-C restatement of the *device*
-            kernels' exact reduction order, used for bitwise checks of the CUDA
-            kernels (``oracle/Makefile`` builds ``oracle/_ref/libmirror.so``).
+            arithmetic of the dense TA path (launch geometry, FMA chains, warp /
+            block reduction trees, split-tile merges), used for the bitwise
+            checks of the CUDA kernels in ``tests/test_gpu_mirror.py`` (C1 TA at
+            500 iterations, BASELINE configs[0]); ``oracle/Makefile`` builds
+            ``oracle/_build/libmirror.so``.
 
 Parity pinning: ``tests/golden/make_golden.py`` imports the real reference
 (present only in the build container) and records its outputs as fixtures;
