@@ -28,6 +28,8 @@
  *   ts_ta_adaptive                   triangle.solve_adaptive  triangle.py:170-251
  *   ts_ta_in_ball                    triangle.solve_in_ball   triangle.py:92-113 (+ _membership_loop 136-167)
  *   ts_lp_feasibility                feasibility.nonnegative_feasibility feasibility.py:59-140
+ *   ts_mm_parse / _coo / _dense      mmio.read_matrix_market_with_info mmio.py:100-156
+ *   ts_mm_to_device                  mmio coordinate read + csr_array(coo), assembled on the device
  */
 #ifndef TRISOLVE_B200_H
 #define TRISOLVE_B200_H
@@ -205,6 +207,33 @@ TS_API int ts_pool_trim(int device);
 /* Page-locked host blocks for solver outputs, cached by size after ts_host_free. */
 TS_API int ts_host_alloc(size_t bytes, void** out);
 TS_API int ts_host_free(void* ptr);
+
+/* ---- Matrix Market ingest (reference mmio.py:41-156) ------------------------
+ * ts_mm_parse reads a file (is_path = 1: `data` is a NUL-terminated path) or an
+ * in-memory image (`data`, `len`) with the reference's acceptance rules; a
+ * malformed input returns TS_EINVAL with ts_last_error() = "line N: ..."
+ * (the reference's MatrixMarketError text).  ts_mm_coo returns the
+ * coordinate entries expanded as the reference stores them (each entry, then
+ * its mirror for symmetric / skew-symmetric files; `stored` of them);
+ * ts_mm_dense the m x n row-major array of an array file.  ts_mm_to_device
+ * builds a CSR handle from a coordinate file with the assembly (mirroring,
+ * sort, duplicate summation in file order, compression) on the device. */
+typedef struct ts_mm ts_mm;
+typedef struct {
+  int32_t format;   /* 0 coordinate, 1 array */
+  int32_t field;    /* 0 real, 1 integer, 2 pattern */
+  int32_t symmetry; /* 0 general, 1 symmetric, 2 skew-symmetric */
+  int32_t reserved;
+  int64_t rows, cols;
+  int64_t entries; /* as stated in the size line (array: rows * cols) */
+  int64_t stored;  /* coordinate: expanded entries; array: values in the file */
+} ts_mm_info;
+TS_API int ts_mm_parse(const char* data, int64_t len, int32_t is_path, ts_mm** out, ts_mm_info* info);
+TS_API int ts_mm_coo(const ts_mm* mm, int32_t* rows, int32_t* cols, double* vals);
+TS_API int ts_mm_dense(const ts_mm* mm, double* rowmajor);
+TS_API int ts_mm_to_device(const ts_mm* mm, int device, void* stream, ts_matrix** out,
+                           int64_t* duplicates);
+TS_API int ts_mm_free(ts_mm* mm);
 
 /* ---- operator layer -------------------------------------------------------- */
 TS_API int ts_matvec(const ts_matrix* a, const double* x, double* y, void* stream);   /* y = A x  */

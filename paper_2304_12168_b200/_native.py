@@ -24,6 +24,7 @@ EXPORTS = (
     "ts_cta_solve", "ts_ta_adaptive", "ts_ta_in_ball", "ts_lp_feasibility",
     "ts_comm_create", "ts_comm_connect", "ts_comm_destroy", "ts_matrix_set_shard",
     "ts_pool_trim", "ts_host_alloc", "ts_host_free",
+    "ts_mm_parse", "ts_mm_coo", "ts_mm_dense", "ts_mm_to_device", "ts_mm_free",
 )
 
 # statuses (results.py:11-18)

@@ -16,6 +16,7 @@
 #include "ts_cta.cuh"
 #include "ts_comm.cuh"
 #include "ts_persist.cuh"
+#include "ts_mmio.cuh"
 
 namespace ts {
 
@@ -861,6 +862,165 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       A->fro = 0.0;
     }
   }
+  *out = A;
+  return 0;
+}
+
+// ---------------------------------------------------------- Matrix Market
+struct ts_mm : public ts::MmParsed {};
+
+int ts_mm_parse(const char* data, int64_t len, int32_t is_path, ts_mm** out, ts_mm_info* info) {
+  if (!out || !data) TS_INVAL("null argument");
+  *out = nullptr;
+  std::vector<char> buf;
+  const char* p = data;
+  size_t n = (size_t)std::max<int64_t>(len, 0);
+  if (is_path) {
+    FILE* fh = fopen(data, "rb");
+    if (!fh) TS_INVAL("cannot open %s", data);
+    fseek(fh, 0, SEEK_END);
+    const long sz = ftell(fh);
+    fseek(fh, 0, SEEK_SET);
+    buf.resize((size_t)std::max(sz, 0L));
+    const size_t got = sz > 0 ? fread(buf.data(), 1, (size_t)sz, fh) : 0;
+    fclose(fh);
+    p = buf.data();
+    n = got;
+  }
+  ts_mm* P = new ts_mm();
+  const int rc = ts::mm_parse(p, n, P);
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  if (info) {
+    info->format = P->fmt;
+    info->field = P->field;
+    info->symmetry = P->sym;
+    info->rows = P->m;
+    info->cols = P->n;
+    info->entries = P->entries;
+    info->stored = P->fmt == 0 ? ts::mm_expanded_count(*P) : (int64_t)P->vals.size();
+  }
+  *out = P;
+  return 0;
+}
+
+int ts_mm_coo(const ts_mm* P, int32_t* rows, int32_t* cols, double* vals) {
+  if (!P || P->fmt != 0) TS_INVAL("not a coordinate Matrix Market object");
+  int64_t c = 0;
+  for (size_t k = 0; k < P->ri.size(); ++k) {
+    rows[c] = P->ri[k];
+    cols[c] = P->ci[k];
+    vals[c] = P->v[k];
+    ++c;
+    if (P->sym != 0 && P->ri[k] != P->ci[k]) {
+      rows[c] = P->ci[k];
+      cols[c] = P->ri[k];
+      vals[c] = P->sym == 2 ? -P->v[k] : P->v[k];
+      ++c;
+    }
+  }
+  return 0;
+}
+
+int ts_mm_dense(const ts_mm* P, double* a) {
+  if (!P || P->fmt != 1) TS_INVAL("not an array Matrix Market object");
+  const int64_t m = P->m, n = P->n;
+  std::fill(a, a + m * n, 0.0);
+  int64_t k = 0;
+  for (int64_t j = 0; j < n; ++j) {  // column-major per the exchange format (mmio.py:142-155)
+    const int64_t i0 = P->sym == 0 ? 0 : (P->sym == 1 ? j : j + 1);
+    for (int64_t i = i0; i < m; ++i) {
+      const double v = P->vals[k++];
+      a[i * n + j] = v;
+      if (P->sym == 1 && i != j) a[j * n + i] = v;
+      else if (P->sym == 2) a[j * n + i] = -v;
+    }
+  }
+  return 0;
+}
+
+int ts_mm_free(ts_mm* P) {
+  delete P;
+  return 0;
+}
+
+// Coordinate file -> device CSR handle: triplets uploaded once, mirrored,
+// sorted, de-duplicated and compressed on the device.
+int ts_mm_to_device(const ts_mm* P, int device, void* stream, ts_matrix** out, int64_t* duplicates) {
+  if (!P || !out) TS_INVAL("null argument");
+  *out = nullptr;
+  if (P->fmt != 0) TS_INVAL("array files are dense: build them with ts_matrix_create_dense");
+  DeviceGuard g(device);
+  setup_pool(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ne = (int64_t)P->ri.size(), m = P->m, n = P->n;
+  std::vector<int64_t> off((size_t)ne + 1);
+  off[0] = 0;
+  for (int64_t k = 0; k < ne; ++k) off[k + 1] = off[k] + ((P->sym != 0 && P->ri[k] != P->ci[k]) ? 2 : 1);
+  const int64_t cnt = off[ne];
+  if (cnt >= (int64_t)INT32_MAX) TS_INVAL("nnz %lld outside the int32 index range", (long long)cnt);
+  int rc = 0;
+  ts_matrix* A = nullptr;
+  int64_t uniq = 0;
+  {
+    Arena ar(st);
+    const size_t c1 = (size_t)std::max<int64_t>(cnt, 1), e1 = (size_t)std::max<int64_t>(ne, 1);
+    int32_t *dri, *dci;
+    double *dv, *val, *vout;
+    int64_t *doff, *pos, *perm;
+    unsigned long long *key, *key_s;
+    int *head, *uidx, *rowcnt, *rp, *ciout;
+    if ((rc = ar.get(&dri, e1)) || (rc = ar.get(&dci, e1)) || (rc = ar.get(&dv, e1)) ||
+        (rc = ar.get(&doff, e1 + 1)) || (rc = ar.get(&key, c1)) || (rc = ar.get(&key_s, c1)) ||
+        (rc = ar.get(&pos, c1)) || (rc = ar.get(&perm, c1)) || (rc = ar.get(&val, c1)) ||
+        (rc = ar.get(&head, c1)) || (rc = ar.get(&uidx, c1)) || (rc = ar.get(&vout, c1)) ||
+        (rc = ar.get(&ciout, c1)) || (rc = ar.get(&rowcnt, (size_t)m + 1)) || (rc = ar.get(&rp, (size_t)m + 1)))
+      return rc;
+    if (ne) {
+      TS_CUDA(cudaMemcpyAsync(dri, P->ri.data(), ne * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      TS_CUDA(cudaMemcpyAsync(dci, P->ci.data(), ne * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      TS_CUDA(cudaMemcpyAsync(dv, P->v.data(), ne * sizeof(double), cudaMemcpyHostToDevice, st));
+      TS_CUDA(cudaMemcpyAsync(doff, off.data(), ne * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      k_mm_expand<<<grid_for(ne), 256, 0, st>>>(dri, dci, dv, doff, ne, P->sym, n, key, pos, val);
+      int end_bit = 1;
+      while (end_bit < 63 && (1ull << end_bit) < (unsigned long long)(m * n)) ++end_bit;
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key_s, pos, perm, (int)cnt, 0, end_bit, st);
+      char* tmp;
+      if ((rc = ar.get(&tmp, tb))) return rc;
+      if (cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_s, pos, perm, (int)cnt, 0, end_bit, st) !=
+          cudaSuccess) {
+        set_error("radix sort of the Matrix Market coordinates failed");
+        return TS_ECUDA;
+      }
+      k_mm_heads<<<grid_for(cnt), 256, 0, st>>>(key_s, cnt, head);
+      size_t sb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, sb, head, uidx, (int)cnt, st);
+      char* tmp2;
+      if ((rc = ar.get(&tmp2, std::max(sb, (size_t)16)))) return rc;
+      cub::DeviceScan::ExclusiveSum(tmp2, sb, head, uidx, (int)cnt, st);
+      TS_CUDA(cudaMemsetAsync(rowcnt, 0, (m + 1) * sizeof(int), st));
+      k_mm_unique<<<grid_for(cnt), 256, 0, st>>>(key_s, perm, val, head, uidx, cnt, n, ciout, vout, rowcnt);
+      int last[2];
+      TS_CUDA(cudaMemcpyAsync(&last[0], uidx + cnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+      TS_CUDA(cudaMemcpyAsync(&last[1], head + cnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+      size_t sb2 = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, sb2, rowcnt, rp, (int)(m + 1), st);
+      char* tmp3;
+      if ((rc = ar.get(&tmp3, std::max(sb2, (size_t)16)))) return rc;
+      cub::DeviceScan::ExclusiveSum(tmp3, sb2, rowcnt, rp, (int)(m + 1), st);
+      TS_CUDA(cudaStreamSynchronize(st));
+      uniq = (int64_t)last[0] + last[1];
+    } else {
+      TS_CUDA(cudaMemsetAsync(rp, 0, (m + 1) * sizeof(int), st));
+      TS_CUDA(cudaStreamSynchronize(st));
+    }
+    rc = ts_matrix_create_csr(rp, ciout, vout, m, n, uniq, device, stream, &A);
+  }
+  if (rc) return rc;
+  if (duplicates) *duplicates = cnt - uniq;
   *out = A;
   return 0;
 }

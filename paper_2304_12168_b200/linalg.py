@@ -80,6 +80,20 @@ class DeviceMatrix:
             m, n = arr.shape
             N.check(lib.ts_matrix_create_dense(arr.ctypes.data, m, n, n, self.device, stream,
                                                C.byref(self._handle)))
+        self._read_info()
+
+    @classmethod
+    def from_handle(cls, handle, device: int = 0) -> "DeviceMatrix":
+        """Adopt a ``ts_matrix`` handle built by the native library (device-side
+        ingest); the new object owns and destroys it."""
+        obj = cls.__new__(cls)
+        obj.device = int(device)
+        obj._handle = handle if isinstance(handle, C.c_void_p) else C.c_void_p(handle)
+        obj._read_info()
+        return obj
+
+    def _read_info(self):
+        lib = N.lib()
         mm, nn, nz, kind, fro = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32(), C.c_double()
         N.check(lib.ts_matrix_info(self._handle, C.byref(mm), C.byref(nn), C.byref(nz),
                                    C.byref(kind), C.byref(fro)))
