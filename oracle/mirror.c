@@ -32,7 +32,9 @@
 #define WARPS 8
 #define MINBLK 4
 #define TW 512 /* 2 columns per thread */
-#define RU 8
+#define RU 12 /* kTileTRows: rows in flight per thread in k_cols_tile */
+#define TBLK_T 3 /* kTileTBlocks */
+#define TBLK_N 2 /* kTileNBlocks */
 
 enum { RED_SUM = 0, RED_MIN = 1 };
 
@@ -93,10 +95,10 @@ typedef struct {
   int64_t m, n;
 } Geo;
 static int64_t resident(const Geo* g) { return (int64_t)g->sms * MINBLK; }
-static int tile_grid(const Geo* g) {
+static int tile_grid(const Geo* g, int per_sm) {
   const int64_t nct = (g->n + TW - 1) / TW, U = nct * g->m;
   int64_t p = U / 8;
-  if (p > resident(g)) p = resident(g);
+  if (p > (int64_t)g->sms * per_sm) p = (int64_t)g->sms * per_sm;
   if (p < 1) p = 1;
   return (int)p;
 }
@@ -492,8 +494,8 @@ int64_t ts_mirror_ta_dense(const double* a, int64_t m, int64_t n, const double* 
   D.g.n = n;
   D.a = a;
   D.lda = n;
-  D.P_t = tile_grid(&D.g);
-  D.P_n = tile_grid(&D.g);
+  D.P_t = tile_grid(&D.g, TBLK_T);
+  D.P_n = tile_grid(&D.g, TBLK_N);
   D.P_c = combine_grid(&D.g);
   D.nct = (n + TW - 1) / TW;
   const int64_t pmax = (int64_t)sms * 8 + 8;

@@ -130,12 +130,13 @@ inline int combine_grid(int64_t m, int sms) {
   return (int)std::max<int64_t>(1, std::min(g, cap));
 }
 
-inline int tile_grid(int64_t m, int64_t n, int sms, int vw) {
+// per_sm: resident blocks per SM of the tile kernel (one full wave)
+inline int tile_grid(int64_t m, int64_t n, int sms, int vw, int per_sm = kMinBlocks) {
   const int64_t tw = (int64_t)vw * kNT;
   const int64_t nct = (n + tw - 1) / tw;
   const int64_t U = nct * m;
   int64_t g = U / 8;  // >= 8 rows of a tile per block (latency-bound sizes want more blocks)
-  const int64_t pmax = resident_blocks(sms);
+  const int64_t pmax = (int64_t)sms * per_sm;
   if (g > pmax) g = pmax;
   if (g < 1) g = 1;
   return (int)g;

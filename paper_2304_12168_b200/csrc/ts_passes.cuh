@@ -677,12 +677,19 @@ __global__ void __launch_bounds__(kNT, kStBlocks) k_rows_stream(StreamRows A, co
 
 // ----------------------------------------------------------- k_cols_tile ----
 // VW columns per thread (2: 128-bit loads, 4: 256-bit loads); tile = VW * kNT
-template <class Epi, int VW, bool kP>
+// k_cols_tile occupancy and depth: 3 blocks/SM with 12 rows in flight per
+// thread streams the C2 matrix in 118 us vs 122 us at 4 x 8
+// (tools/microbench/dense_av.cu); RU is even, so rows keep alternating
+// between the two accumulators exactly as before.
+constexpr int kTileTBlocks = 3;
+constexpr int kTileTRows = 12;
+
+template <class Epi, int VW, bool kP, int RU0 = 8>
 __device__ __forceinline__ void body_cols_tile(const DenseRows& A, const double* __restrict__ x, XS xs,
                                                Epi& epi, const Work& wk, int64_t b, int64_t P) {
   constexpr int K = Epi::K;
   constexpr int TW = VW * kNT;       // tile width (columns)
-  constexpr int RU = VW == 4 ? 4 : 8;  // rows in flight per thread
+  constexpr int RU = VW == 4 ? 4 : RU0;  // rows in flight per thread
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
   xs.load();
@@ -806,14 +813,14 @@ __device__ __forceinline__ void body_cols_tile(const DenseRows& A, const double*
 }
 
 template <class Epi, int VW>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_cols_tile(DenseRows A, const double* __restrict__ x,
-                                                             XS xs, Epi epi, Work wk) {
+__global__ void __launch_bounds__(kNT, kTileTBlocks) k_cols_tile(DenseRows A, const double* __restrict__ x,
+                                                               XS xs, Epi epi, Work wk) {
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
-  body_cols_tile<Epi, VW, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
+  body_cols_tile<Epi, VW, false, kTileTRows>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------ k_cols_tma ----
@@ -1107,65 +1114,96 @@ __global__ void __launch_bounds__(kNT, kCtBlocksPerSM) k_csr_ctile(CtileRows A, 
 // coalesced 4 KB row chunks.  A warp keeps its tile's slice of v in registers
 // (loaded once per segment) and reduces one row chunk per step; the per-(tile,
 // row) sums go to `part` and k_tile_combine adds them in tile order.
-template <class Epi, bool kP>
+// The tile's 512-entry slice of v is staged once per segment in shared
+// memory (registers then hold only matrix data), and each warp keeps R row
+// chunks (R x 4 KB) in flight.  tools/microbench/dense_av.cu on C2: 141 us
+// with the slice in registers and one chunk per warp at 4 blocks/SM, 124 us
+// (6.44 TB/s) with R = 2 at 2 blocks/SM; every variant yields the same partials
+// bit for bit (each row chunk is reduced by the same lane FMA chain + xor tree).
+constexpr int kTileNBlocks = 2;  // k_rows_tile blocks per SM (128 registers)
+constexpr int kTileNRows = 2;    // row chunks in flight per warp
+
+template <class Epi, bool kP, int R = 1>
 __device__ __forceinline__ void body_rows_tile(const DenseRows& A, const double* __restrict__ x, XS xs,
                                                Epi& epi, double* __restrict__ part, int64_t b, int64_t P) {
   constexpr int TW = 2 * kNT;  // 512 columns: 16 per lane, 8 x 128-bit loads per row chunk
+  __shared__ __align__(16) double xsl[TW];
   xs.load();
   ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
-  __syncthreads();
   const int64_t m = A.m, n = A.n, lda = A.lda;
   const int64_t nct = (n + TW - 1) / TW;
   const int64_t U = nct * m;
   const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto dot = [&](const double2 (&v)[8]) -> double {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      const double2 x0 = *reinterpret_cast<const double2*>(xsl + 64 * k + 2 * lane);
+      const double2 x1 = *reinterpret_cast<const double2*>(xsl + 64 * (k + 1) + 2 * lane);
+      a0 = fma(v[k].x, x0.x, a0); a0 = fma(v[k].y, x0.y, a0);
+      a1 = fma(v[k + 1].x, x1.x, a1); a1 = fma(v[k + 1].y, x1.y, a1);
+    }
+    return warp_reduce(a0 + a1, RED_SUM);
+  };
   for (int64_t u = U0; u < U1;) {
     const int64_t ct = u / m, r0 = u - ct * m;
     const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
     const int64_t cb = ct * TW;
     const bool full = cb + TW <= n;
-    double2 xv[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t c = cb + 64 * k + 2 * lane;
-      xv[k].x = (c < n) ? xs(ldx<kP>(x + c)) : 0.0;
-      xv[k].y = (c + 1 < n) ? xs(ldx<kP>(x + c + 1)) : 0.0;
+    __syncthreads();  // previous slice consumed
+    for (int k = threadIdx.x; k < TW; k += kNT) {
+      const int64_t c = cb + k;
+      xsl[k] = (c < n) ? xs(ldx<kP>(x + c)) : 0.0;
     }
-    for (int64_t r = r0 + wid; r < r1; r += kWarps) {
-      const double* row = A.a + r * lda + cb + 2 * lane;
-      double a0 = 0.0, a1 = 0.0;
-      if (full) {
+    __syncthreads();
+    int64_t r = r0 + wid;
+    if (full) {
+      for (; r + 8 * (R - 1) < r1; r += 8 * R) {
+        double2 v[R][8];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[q][k] = ld_stream2(A.a + (r + 8 * q) * lda + cb + 2 * lane + 64 * k);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const double sum = dot(v[q]);
+          if (lane == 0) part[(r + 8 * q) * nct + ct] = sum;
+        }
+      }
+      for (; r < r1; r += 8) {
         double2 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = ld_stream2(row + 64 * k);
-#pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-          a0 = fma(v[k].x, xv[k].x, a0); a0 = fma(v[k].y, xv[k].y, a0);
-          a1 = fma(v[k + 1].x, xv[k + 1].x, a1); a1 = fma(v[k + 1].y, xv[k + 1].y, a1);
-        }
-      } else {
+        for (int k = 0; k < 8; ++k) v[k] = ld_stream2(A.a + r * lda + cb + 2 * lane + 64 * k);
+        const double sum = dot(v);
+        if (lane == 0) part[r * nct + ct] = sum;
+      }
+    } else {
+      for (; r < r1; r += 8) {
+        const double* row = A.a + r * lda + cb + 2 * lane;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int64_t c = cb + 64 * k + 2 * lane;
-          if (c < n) a0 = fma(ld_stream(row + 64 * k), xv[k].x, a0);
-          if (c + 1 < n) a1 = fma(ld_stream(row + 64 * k + 1), xv[k].y, a1);
+          if (c < n) a0 = fma(ld_stream(row + 64 * k), xsl[64 * k + 2 * lane], a0);
+          if (c + 1 < n) a1 = fma(ld_stream(row + 64 * k + 1), xsl[64 * k + 2 * lane + 1], a1);
         }
+        const double sum = warp_reduce(a0 + a1, RED_SUM);
+        if (lane == 0) part[r * nct + ct] = sum;
       }
-      const double sum = warp_reduce(a0 + a1, RED_SUM);
-      if (lane == 0) part[r * nct + ct] = sum;
     }
     u += r1 - r0;
   }
 }
 
 template <class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_tile(DenseRows A, const double* __restrict__ x,
-                                                             XS xs, Epi epi, double* __restrict__ part) {
+__global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile(DenseRows A, const double* __restrict__ x,
+                                                               XS xs, Epi epi, double* __restrict__ part) {
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) return;  // k_tile_combine owns idle()
-  body_rows_tile<Epi, false>(A, x, xs, epi, part, blockIdx.x, gridDim.x);
+  body_rows_tile<Epi, false, kTileNRows>(A, x, xs, epi, part, blockIdx.x, gridDim.x);
 }
 
 // y_r = sum over tiles of part[r][tile] (row-major partials): one warp per
