@@ -123,6 +123,7 @@ template <class Epi>
 struct EpiDefer {
   static constexpr int K = Epi::K;
   static constexpr bool kPair = kPairOf<Epi>;
+  static constexpr int kVecBlocks = kVecBlocksOf<Epi>;
   Epi e;
   CommDev c;
   __device__ int op(int k) const { return e.op(k); }

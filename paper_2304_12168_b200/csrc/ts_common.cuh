@@ -101,6 +101,15 @@ constexpr bool pair_of(...) { return false; }
 template <class E>
 constexpr bool kPairOf = pair_of<E>(0);
 
+// Epi::kVecBlocks when declared (resident blocks per SM of its k_vec, i.e. the
+// register budget of a heavy vector epilogue), else kMinBlocks
+template <class E>
+constexpr auto vec_blocks_of(int) -> decltype(int(E::kVecBlocks)) { return E::kVecBlocks; }
+template <class E>
+constexpr int vec_blocks_of(...) { return kMinBlocks; }
+template <class E>
+constexpr int kVecBlocksOf = vec_blocks_of<E>(0);
+
 // plain (coherent) 128-bit load / store of an aligned element pair
 __device__ __forceinline__ double2 ld_pair(const double* p) {
   return *reinterpret_cast<const double2*>(p);

@@ -399,6 +399,7 @@ struct EpiCtaCand : EpiBase {
   // pair version: the same per-element arithmetic for j, j+1 (128-bit loads),
   // order-t specialised so the t direction loads are independent registers
   static constexpr bool kPair = true;
+  static constexpr int kVecBlocks = 2;  // 128 registers: the order-8 pair paths spilled at 64
   template <int T>
   __device__ __forceinline__ void cand2(int64_t j, double (&acc)[K]) const {
     double2 r, pv[T];
@@ -425,6 +426,8 @@ struct EpiCtaCand : EpiBase {
       if (two) acc[o - 1] = fma(cy, cy, acc[o - 1]);
     }
   }
+  // orders above the default t_max = 5 take the scalar path twice (the same
+  // arithmetic and accumulation order; the order-8 pair code spilled)
   __device__ void elem2(int64_t j, double (&acc)[K]) const {
     switch (t_c) {
       case 1: cand2<1>(j, acc); break;
@@ -432,9 +435,10 @@ struct EpiCtaCand : EpiBase {
       case 3: cand2<3>(j, acc); break;
       case 4: cand2<4>(j, acc); break;
       case 5: cand2<5>(j, acc); break;
-      case 6: cand2<6>(j, acc); break;
-      case 7: cand2<7>(j, acc); break;
-      default: cand2<8>(j, acc); break;
+      default:
+        elem(j, acc);
+        if (j + 1 < m) elem(j + 1, acc);
+        break;
     }
   }
   __device__ void finish(double (&red)[K]) const {
@@ -527,6 +531,7 @@ struct EpiCtaUpd : EpiBase {
   // pair version (elements j, j+1; 128-bit loads), specialised on the chosen
   // order so every direction load is issued before the arithmetic
   static constexpr bool kPair = true;
+  static constexpr int kVecBlocks = 2;  // 128 registers: the order-8 pair paths spilled at 64
   template <int O>
   __device__ __forceinline__ void upd2(int64_t j, double (&acc)[K]) const {
     const double* al = al_s;
@@ -584,9 +589,10 @@ struct EpiCtaUpd : EpiBase {
       case 3: upd2<3>(j, acc); break;
       case 4: upd2<4>(j, acc); break;
       case 5: upd2<5>(j, acc); break;
-      case 6: upd2<6>(j, acc); break;
-      case 7: upd2<7>(j, acc); break;
-      default: upd2<8>(j, acc); break;
+      default:  // orders above t_max = 5: the scalar path (same arithmetic)
+        elem(j, acc);
+        if (j + 1 < (m > n ? m : n)) elem(j + 1, acc);
+        break;
     }
   }
   __device__ void finish(double (&red)[K]) const {

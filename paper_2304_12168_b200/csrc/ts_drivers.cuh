@@ -156,6 +156,7 @@ struct Instance {
     TS_CHECK(alloc(&wk.bpart, (size_t)pmax * 2));
     TS_CHECK(alloc(&wk.tpart, (size_t)pmax * 2 * kCW));
     TS_CHECK(alloc(&wk.npart, (size_t)std::max<int64_t>(M.npart, 1)));
+    TS_CUDA(cudaMemset(wk.npart, 0, sizeof(double) * std::max<int64_t>(M.npart, 1)));
     TS_CHECK(alloc(&wk.cnt, (size_t)pmax));
     TS_CHECK(alloc(&wk.done, 4));
     wk.pmax = pmax;

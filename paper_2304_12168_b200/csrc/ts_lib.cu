@@ -207,6 +207,7 @@ static int make_work(Arena& ar, int pmax, Work* w, int64_t npart = 0) {
   TS_CHECK(ar.get(&w->tpart, (size_t)pmax * 2 * kCW));
   TS_CHECK(ar.get(&w->cnt, (size_t)pmax));
   TS_CHECK(ar.get(&w->done, 4));
+  TS_CUDA(cudaMemsetAsync(w->npart, 0, sizeof(double) * std::max<int64_t>(npart, 1), ar.st));
   TS_CUDA(cudaMemsetAsync(w->cnt, 0, sizeof(unsigned) * pmax, ar.st));
   TS_CUDA(cudaMemsetAsync(w->done, 0, sizeof(unsigned) * 4, ar.st));
   return 0;
@@ -298,8 +299,22 @@ int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* ou
     *out = p;
     return 0;
   }
+  // long rows of near-uniform length (no row above twice the mean): one warp per
+  // row with prefetched chunks (k_rows_wrow); else the load-balanced flat split.
+  // TS_CSR_LONG=flat forces the flat split.
+  {
+    const char* lf = getenv("TS_CSR_LONG");
+    int64_t maxlen = 0;
+    for (int64_t r = 0; r < rows; ++r) maxlen = std::max<int64_t>(maxlen, rp[r + 1] - rp[r]);
+    if (!(lf && !strcmp(lf, "flat")) && maxlen * rows <= 2 * nnz) {
+      p.kind = PLAN_WROW;
+      p.P = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * kWrowBlocks, (rows + kWarps - 1) / kWarps));
+      *out = p;
+      return 0;
+    }
+  }
   p.kind = PLAN_FLAT;
-  p.P = (int)std::max<int64_t>(1, std::min(pmax, nnz / ((int64_t)kWarps * 256)));
+  p.P = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * kFlatBlocks, nnz / ((int64_t)kWarps * 256)));
   std::vector<int> wr((size_t)p.P * kWarps);
   for (int64_t b = 0; b < p.P; ++b)
     for (int w = 0; w < kWarps; ++w) {
@@ -325,7 +340,7 @@ int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t st
     return 0;
   }
   p.kind = PLAN_FLAT;
-  p.P = (int)std::max<int64_t>(1, std::min(pmax, E / ((int64_t)kWarps * 256)));
+  p.P = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * kFlatBlocks, E / ((int64_t)kWarps * 256)));
   std::vector<int> wr((size_t)p.P * kWarps);
   for (int64_t b = 0; b < p.P; ++b)
     for (int w = 0; w < kWarps; ++w) {
@@ -669,6 +684,13 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
       if (A->planN.kind == PLAN_FLAT && !(fe && !strcmp(fe, "flat"))) {
         A->planN.kind = PLAN_TILE;
         A->planN.P = tile_grid(m, n, A->sms, 2, kTileNBlocks);
+        // TS_DENSE_N=fused: one-kernel A v (k_rows_tile_fused; opt-in: C2 A v
+        // 199 us vs 136 us split, because tile-major units complete every row
+        // group in the last few blocks, which then combine them serially)
+        const int64_t nct = (n + 2 * kNT - 1) / (2 * kNT);
+        const int64_t rows_pb = nct * m / A->planN.P + 1;
+        const int64_t max_groups = rows_pb / kGroupRows + 2 * std::min<int64_t>(nct, rows_pb) + 2;
+        A->planN.fused = (fe && !strcmp(fe, "fused")) && max_groups <= kMaxGroupsPerBlock;
       }
     }
     if (!rc) rc = finish_create(A, st, ar);

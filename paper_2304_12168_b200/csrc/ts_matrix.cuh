@@ -23,17 +23,22 @@
 namespace ts {
 
 enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4,
-                      PLAN_CTILE = 5, PLAN_STREAM = 6 };
+                      PLAN_CTILE = 5, PLAN_STREAM = 6, PLAN_WROW = 7 };
 
 
-// elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans)
-inline int64_t npart_elems(int64_t m, int64_t n) { return ((n + 2 * kNT - 1) / (2 * kNT)) * m; }
+// elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans):
+// tile partials, then the fused A v's group slots and counters (k_rows_tile_fused)
+inline int64_t npart_elems(int64_t m, int64_t n) {
+  const int64_t g = (m + 31) / 32;
+  return ((n + 2 * kNT - 1) / (2 * kNT)) * m + g * kKMax + (g + 1) / 2;
+}
 
 struct RowPlan {
   int kind = PLAN_SHORT;
   int P = 1;            // blocks
   int* wrow = nullptr;  // device [P * kWarps] (PLAN_FLAT)
   int vw = 2;           // dense: columns per 128/256-bit load
+  int fused = 0;        // dense PLAN_TILE A v: one kernel (k_rows_tile_fused)
   // PLAN_STREAM: chunk table (first row, first entry) and per-block chunk runs
   int nchunks = 0;
   int2* chunks = nullptr;  // device [nchunks + 1]
@@ -115,9 +120,9 @@ int plan_rows_csr(const int* rp_host, int64_t rows, int64_t nnz, int sms, RowPla
 int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t st);
 void destroy_instances(Mat* M);
 
-inline int vec_grid(int64_t len, int sms) {
+inline int vec_grid(int64_t len, int sms, int per_sm = 0) {
   int64_t g = (len + kNT * 4 - 1) / (kNT * 4);
-  int64_t pmax = resident_blocks(sms);
+  int64_t pmax = per_sm > 0 ? (int64_t)sms * per_sm : resident_blocks(sms);
   if (g > pmax) g = pmax;
   if (g < 1) g = 1;
   return (int)g;
@@ -149,7 +154,9 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
                 cudaStream_t st) {
   if (M.kind == 0) {
     if (!trans) {
-      if (M.planN.kind == PLAN_TILE) {
+      if (M.planN.kind == PLAN_TILE && M.planN.fused) {
+        k_rows_tile_fused<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+      } else if (M.planN.kind == PLAN_TILE) {
         const int64_t nct = (M.n + 2 * kNT - 1) / (2 * kNT);
         k_rows_tile<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk.npart);
         k_tile_combine<Epi><<<combine_grid(M.m, M.sms), kNT, 0, st>>>(M.m, nct, wk.npart, epi, wk);
@@ -190,6 +197,8 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
       k_rows_flat<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk, pl.wrow);
     else if (pl.kind == PLAN_WARP)
       k_rows_warp<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
+    else if (pl.kind == PLAN_WROW)
+      k_rows_wrow<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
     else if (pl.kind == PLAN_STREAM) {
       static bool attr_set = false;
       if (!attr_set) {
@@ -208,7 +217,7 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
 
 template <class Epi>
 int launch_vec(int64_t len, int sms, const Epi& epi, const Work& wk, cudaStream_t st) {
-  k_vec<Epi><<<vec_grid(len, sms), kNT, 0, st>>>(len, epi, wk);
+  k_vec<Epi><<<vec_grid(len, sms, kVecBlocksOf<Epi>), kNT, 0, st>>>(len, epi, wk);
   TS_CUDA(cudaGetLastError());
   return 0;
 }

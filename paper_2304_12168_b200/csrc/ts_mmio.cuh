@@ -345,12 +345,12 @@ inline int64_t mm_expanded_count(const MmParsed& P) {
   return c;
 }
 
-// ---- device assembly -------------------------------------------------------
+// ---- device assembly (grid-stride: launched with grid_for's capped grids) ----
 __global__ void k_mm_expand(const int32_t* ri, const int32_t* ci, const double* v, const int64_t* off,
                             int64_t cnt, int sym, int64_t n, unsigned long long* key, int64_t* pos,
                             double* val) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cnt) return;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+       k += (int64_t)gridDim.x * blockDim.x) {
   const int64_t o = off[k];
   const int32_t i = ri[k], j = ci[k];
   key[o] = (unsigned long long)i * (unsigned long long)n + (unsigned long long)j;
@@ -361,25 +361,28 @@ __global__ void k_mm_expand(const int32_t* ri, const int32_t* ci, const double* 
     pos[o + 1] = o + 1;
     val[o + 1] = sym == 2 ? -v[k] : v[k];
   }
+  }
 }
 __global__ void k_mm_heads(const unsigned long long* key, int64_t cnt, int* head) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cnt) return;
-  head[k] = (k == 0 || key[k] != key[k - 1]) ? 1 : 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+       k += (int64_t)gridDim.x * blockDim.x)
+    head[k] = (k == 0 || key[k] != key[k - 1]) ? 1 : 0;
 }
 // one thread per unique (row, col): sum its duplicates in file order
 __global__ void k_mm_unique(const unsigned long long* key, const int64_t* perm, const double* val,
                             const int* head, const int* uidx, int64_t cnt, int64_t n, int* ci_out,
                             double* v_out, int* rowcnt) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cnt || !head[k]) return;
-  const int u = uidx[k];
-  double s = val[perm[k]];
-  for (int64_t q = k + 1; q < cnt && !head[q]; ++q) s += val[perm[q]];
-  const unsigned long long kk = key[k];
-  ci_out[u] = (int)(kk % (unsigned long long)n);
-  v_out[u] = s;
-  atomicAdd(rowcnt + (kk / (unsigned long long)n), 1);  // integer counts: order-free
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (!head[k]) continue;
+    const int u = uidx[k];
+    double s = val[perm[k]];
+    for (int64_t q = k + 1; q < cnt && !head[q]; ++q) s += val[perm[q]];
+    const unsigned long long kk = key[k];
+    ci_out[u] = (int)(kk % (unsigned long long)n);
+    v_out[u] = s;
+    atomicAdd(rowcnt + (kk / (unsigned long long)n), 1);  // integer counts: order-free
+  }
 }
 
 }  // namespace ts

@@ -289,8 +289,10 @@ __device__ void phase_end(Epi& epi, const Work& wk, const double* facc, int nb) 
 }
 
 // ----------------------------------------------------------- k_rows_flat ----
+// 3 blocks/SM (85 registers): at 64 the 8-deep gather loop spilled
+constexpr int kFlatBlocks = 3;
 template <class Acc, class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_flat(Acc A, const double* __restrict__ x, XS xs,
+__global__ void __launch_bounds__(kNT, kFlatBlocks) k_rows_flat(Acc A, const double* __restrict__ x, XS xs,
                                                    Epi epi, Work wk,
                                                    const int* __restrict__ wrow) {
   constexpr int K = Epi::K;
@@ -554,6 +556,85 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
     return;
   }
   body_rows_warp<Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
+}
+
+// ----------------------------------------------------------- k_rows_wrow ----
+// Long, near-uniform CSR rows (C5's A v: 10^4 rows of ~1000 entries gathering
+// x at random from 8 MB): one warp per row, lanes striding the row 32 entries
+// at a time, with the next kWrowU chunks' values and column indices loaded
+// before the current chunk's x gathers are issued, so every warp always has
+// matrix loads AND gathers in flight.  tools/microbench/spmv_long.cu on C5:
+// 49 us vs 64 us for the flat split kernel (whose warps wait on one chunk's
+// gathers before loading the next).  Four partial accumulators per lane
+// (entry k of a lane goes to accumulator (k / 32) % 4), then the xor tree.
+constexpr int kWrowU = 6;
+constexpr int kWrowBlocks = 3;  // 85 registers: no spills with the epilogues
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kWrowBlocks) k_rows_wrow(CsrRows A, const double* __restrict__ x, XS xs,
+                                                             Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  constexpr int U = kWrowU;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  xs.load();
+  ktimer_begin(epi.timer());
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t W = ((int64_t)gridDim.x * kNT) >> 5;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  for (int64_t r = w; r < A.m; r += W) {
+    const int k0 = __ldg(A.rp + r), k1 = __ldg(A.rp + r + 1);
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    double pv[U];
+    int pj[U];
+    int k = k0 + lane;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = k + 32 * u;
+      pv[u] = kk < k1 ? ld_stream(A.val + kk) : 0.0;
+      pj[u] = kk < k1 ? ld_stream_i(A.ci + kk) : 0;
+    }
+    for (; k < k1; k += 32 * U) {
+      double v[U];
+      int j[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = pv[u];
+        j[u] = pj[u];
+      }
+      const int kn = k + 32 * U;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = kn + 32 * u;
+        pv[u] = kk < k1 ? ld_stream(A.val + kk) : 0.0;
+        pj[u] = kk < k1 ? ld_stream_i(A.ci + kk) : 0;
+      }
+      double xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = xs(__ldg(x + j[u]));  // j = 0 past the end: v = 0
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u & 3] = fma(v[u], xv[u], a[u & 3]);
+    }
+    const double sum = warp_reduce((a[0] + a[1]) + (a[2] + a[3]), RED_SUM);
+    if (lane == 0) epi.elem(r, sum, acc);
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+  }
+  finish_last(epi, wk, nullptr, (int)gridDim.x, sm, &sflag);
 }
 
 // --------------------------------------------------------- k_rows_stream ----
@@ -1206,6 +1287,132 @@ __global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile(DenseRows A, co
   body_rows_tile<Epi, false, kTileNRows>(A, x, xs, epi, part, blockIdx.x, gridDim.x);
 }
 
+// ------------------------------------------------------ k_rows_tile_fused ----
+// Dense A v in ONE kernel: the tile pass above, then the per-row combine of
+// the tile partials done by whichever block completes a 32-row group.  Every
+// block counts the rows it finished per group (one atomic per group touched,
+// after a fence); the block whose count completes a group (all tiles of its
+// rows present) sums those rows' partials exactly as k_tile_combine does (warp
+// per row, lane-strided over tiles, xor tree) and runs the epilogue, leaving
+// the group's reduction slots in gacc[group]; the last block to arrive reduces
+// gacc in group order.  Work::npart holds [tiles x m partials | gacc | group
+// counters], zeroed once and self-resetting.  Opt-in (TS_DENSE_N=fused): the
+// (tile, row) units are tile-major, so every group completes in the blocks of
+// the last tile, which combine them one after another (C2: 199 us vs 136 us
+// for the tile + combine kernels); kept for the record and for study.
+constexpr int kGroupRows = 32;
+constexpr int kMaxGroupsPerBlock = 256;
+
+__host__ __device__ inline int64_t tile_groups(int64_t m) { return (m + kGroupRows - 1) / kGroupRows; }
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile_fused(DenseRows A, const double* __restrict__ x,
+                                                                     XS xs, Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ double wacc[kWarps][kKMax];
+  __shared__ int glist[kMaxGroupsPerBlock];
+  __shared__ unsigned gadd[kMaxGroupsPerBlock];
+  __shared__ int gcount, gdone;
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int64_t m = A.m, nct = (A.n + 2 * kNT - 1) / (2 * kNT);
+  const int64_t U = nct * m, U0 = U * b / P, U1 = U * (b + 1) / P;
+  double* part = wk.npart;
+  double* gacc = part + nct * m;
+  unsigned* gcnt = reinterpret_cast<unsigned*>(gacc + tile_groups(m) * kKMax);
+  body_rows_tile<Epi, false, kTileNRows>(A, x, xs, epi, part, b, P);
+  __threadfence();  // this thread's partial stores before the group arrivals
+  __syncthreads();
+  if (threadIdx.x == 0) {  // (group, rows finished) pairs of this block; no atomics yet
+    int c = 0;
+    for (int64_t u = U0; u < U1;) {
+      const int64_t ct = u / m, r0 = u - ct * m;
+      const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
+      for (int64_t g = r0 / kGroupRows; g * kGroupRows < r1; ++g) {
+        const int64_t gb = g * kGroupRows, ge = (gb + kGroupRows < m) ? gb + kGroupRows : m;
+        glist[c] = (int)g;
+        gadd[c] = (unsigned)(((r1 < ge) ? r1 : ge) - ((r0 > gb) ? r0 : gb));
+        ++c;
+      }
+      u += r1 - r0;
+    }
+    gcount = c;
+    gdone = 0;
+  }
+  __syncthreads();
+  {  // arrivals in parallel, one thread per (group, count); keep the completed groups
+    const int c = gcount;
+    bool complete = false;
+    int g = -1;
+    if ((int)threadIdx.x < c) {
+      __threadfence();
+      g = glist[threadIdx.x];
+      const int64_t gb = (int64_t)g * kGroupRows, ge = (gb + kGroupRows < m) ? gb + kGroupRows : m;
+      const unsigned total = (unsigned)(nct * (ge - gb));
+      const unsigned add = gadd[threadIdx.x];
+      complete = atomicAdd(gcnt + g, add) + add == total;
+    }
+    __syncthreads();
+    if (complete) glist[atomicAdd(&gdone, 1)] = g;  // order irrelevant: slots are per group
+    __syncthreads();
+    if (threadIdx.x == 0) gcount = gdone;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ng = gcount;
+  if (ng > 0) __threadfence();  // acquire the other blocks' partials
+  for (int q = 0; q < ng; ++q) {
+    const int64_t g = glist[q];
+    const int64_t gb = g * kGroupRows, ge = (gb + kGroupRows < m) ? gb + kGroupRows : m;
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+    for (int64_t r = gb + wid; r < ge; r += kWarps) {
+      const double* pr = part + r * nct;
+      double y0 = 0.0, y1 = 0.0;
+      int64_t t = lane;
+      for (; t + 32 < nct; t += 64) {
+        y0 += __ldcg(pr + t);
+        y1 += __ldcg(pr + t + 32);
+      }
+      if (t < nct) y0 += __ldcg(pr + t);
+      const double y = warp_reduce(y0 + y1, RED_SUM);
+      if (lane == 0) epi.elem(r, y, acc);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) wacc[wid][k] = acc[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double v = wacc[0][k];
+        for (int j = 1; j < kWarps; ++j) v = red_combine(epi.op(k), v, wacc[j][k]);
+        gacc[g * kKMax + k] = v;
+      }
+      gcnt[g] = 0u;  // self-reset for the next launch
+    }
+    __syncthreads();
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    double red[K];
+    reduce_partials<K>(gacc, nullptr, (int)tile_groups(m), red, sm, epi);
+    if (threadIdx.x == 0) {
+      ktimer_end(epi.timer());
+      epi.finish(red);
+    }
+    __syncthreads();
+    epi.finish_block();
+  }
+}
+
 // y_r = sum over tiles of part[r][tile] (row-major partials): one warp per
 // row, lane-strided sums then the fixed xor tree; then the pass epilogue
 template <class Epi, bool kP>
@@ -1293,7 +1500,7 @@ __device__ __forceinline__ void body_vec(int64_t len, Epi& epi, const Work& wk, 
 }
 
 template <class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_vec(int64_t len, Epi epi, Work wk) {
+__global__ void __launch_bounds__(kNT, kVecBlocksOf<Epi>) k_vec(int64_t len, Epi epi, Work wk) {
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();

@@ -44,12 +44,13 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
 
     from paper_2304_12168_b200 import _native as N
+    from paper_2304_12168_b200 import mmio
 
     if shutil.which("gcc") is None:
         pytest.skip("gcc not available")
     structs = {"ts_trace_row": N.TraceRow, "ts_result": N.Result, "ts_cta_options": N.CtaOptions,
                "ts_ta_options": N.TaOptions, "ts_ball_options": N.BallOptions,
-               "ts_lp_options": N.LpOptions}
+               "ts_lp_options": N.LpOptions, "ts_mm_info": mmio._Info}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')

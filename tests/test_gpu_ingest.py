@@ -48,7 +48,7 @@ def test_device_ingest_full_size_general_and_symmetric(tmp_path):
     from paper_2304_12168_b200 import mmio
     from paper_2304_12168_b200 import workloads as W
 
-    a = W.convdiff_upwind(400).a  # 160000 x 160000 five-point operator
+    a = W.convdiff_upwind(1000).a  # C4: 10^6 x 10^6, 4,996,000 entries (> one capped grid)
     p = tmp_path / "a.mtx"
     mmio.write_matrix_market(a, str(p))
     dm, info = mmio.read_matrix_market_device(str(p))
