@@ -95,9 +95,9 @@ typedef struct {
   int64_t m, n;
 } Geo;
 static int64_t resident(const Geo* g) { return (int64_t)g->sms * MINBLK; }
-static int tile_grid(const Geo* g, int per_sm) {
+static int tile_grid(const Geo* g, int per_sm, int min_rows) {
   const int64_t nct = (g->n + TW - 1) / TW, U = nct * g->m;
-  int64_t p = U / 8;
+  int64_t p = U / min_rows; /* kTileMinRowsN = 8 (A v), kTileMinRowsT = 32 (A^T v) */
   if (p > (int64_t)g->sms * per_sm) p = (int64_t)g->sms * per_sm;
   if (p < 1) p = 1;
   return (int)p;
@@ -494,8 +494,8 @@ int64_t ts_mirror_ta_dense(const double* a, int64_t m, int64_t n, const double* 
   D.g.n = n;
   D.a = a;
   D.lda = n;
-  D.P_t = tile_grid(&D.g, TBLK_T);
-  D.P_n = tile_grid(&D.g, TBLK_N);
+  D.P_t = tile_grid(&D.g, TBLK_T, 32);
+  D.P_n = tile_grid(&D.g, TBLK_N, 8);
   D.P_c = combine_grid(&D.g);
   D.nct = (n + TW - 1) / TW;
   const int64_t pmax = (int64_t)sms * 8 + 8;

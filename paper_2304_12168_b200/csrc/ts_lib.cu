@@ -669,7 +669,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
       A->planN.vw = vw;
       A->planT.kind = PLAN_TILE;
       A->planT.vw = vw;
-      A->planT.P = tile_grid(m, n, A->sms, vw, vw == 2 ? kTileTBlocks : kMinBlocks);
+      A->planT.P = tile_grid(m, n, A->sms, vw, vw == 2 ? kTileTBlocks : kMinBlocks, kTileMinRowsT);
       // TMA-streamed A^T v: TS_DENSE_T=tma (measured ~4 % slower than the
       // register-staged tile kernel on C2, kept for experiments)
       const char* te = getenv("TS_DENSE_T");

@@ -135,12 +135,19 @@ inline int combine_grid(int64_t m, int sms) {
   return (int)std::max<int64_t>(1, std::min(g, cap));
 }
 
-// per_sm: resident blocks per SM of the tile kernel (one full wave)
-inline int tile_grid(int64_t m, int64_t n, int sms, int vw, int per_sm = kMinBlocks) {
+// per_sm: resident blocks per SM of the tile kernel (one full wave);
+// min_rows: rows of a tile per block at least.  Only small (L2-resident)
+// matrices feel it: for A^T v the column pieces of a tile are merged in block
+// order by one block, and C1 runs 9.5 us per A^T v with 32 rows per block vs
+// 15.7 us with 8 (16 and 64 were worse); A v is best at 8 (7.2 vs 9.1 us).
+constexpr int kTileMinRowsN = 8;
+constexpr int kTileMinRowsT = 32;
+inline int tile_grid(int64_t m, int64_t n, int sms, int vw, int per_sm = kMinBlocks,
+                     int min_rows = kTileMinRowsN) {
   const int64_t tw = (int64_t)vw * kNT;
   const int64_t nct = (n + tw - 1) / tw;
   const int64_t U = nct * m;
-  int64_t g = U / 8;  // >= 8 rows of a tile per block (latency-bound sizes want more blocks)
+  int64_t g = U / min_rows;
   const int64_t pmax = (int64_t)sms * per_sm;
   if (g > pmax) g = pmax;
   if (g < 1) g = 1;
