@@ -25,9 +25,11 @@ the per-step solve time.
 * --impl reference: the reference's CPU algorithm (oracle port) timed for
   K steps on the host; rank 0 only.
 
-N > 1 (torchrun): ONE column-sharded solve over all ranks (strong scaling):
-rank p holds A[:, p n/N : (p+1) n/N]; every A v is a fused fixed-rank-order
-all-reduce over NVLink peer memory; value = the solve's iterations / max time.
+N > 1 (torchrun): ONE sharded solve over all ranks (strong scaling): column
+blocks (rank p holds A[:, p n/N : (p+1) n/N]; every A v is a fused
+fixed-rank-order all-reduce over NVLink peer memory), or for C4 row blocks
+(a halo exchange with each neighbour before every pass, scalar all-reduces);
+value = the solve's iterations / max time.
 """
 
 from __future__ import annotations
@@ -251,7 +253,13 @@ def ours_arm(args, cfg):
 
     w = make_workload(cfg)
     bn = float(np.linalg.norm(w.b))
-    if world > 1:
+    if world > 1 and cfg["gen"] == "c4":
+        # row-block sharded solve (square banded C4): each rank owns rows and
+        # columns [r0, r1); a halo exchange with each neighbour before every pass
+        from paper_2304_12168_b200.shard import RowShardedMatrix
+
+        dm = RowShardedMatrix(w.a, device=dev)
+    elif world > 1:
         # column-sharded solve: each rank holds A[:, c0:c1]; A v is one fused
         # fixed-rank-order all-reduce over NVLink peer memory per pass
         from paper_2304_12168_b200.shard import ShardedMatrix
@@ -344,7 +352,9 @@ def ours_arm(args, cfg):
                    "l2": "no flush: matrix larger than L2" if cfg["gen"] in ("c2", "c4", "c5")
                          else "L2-resident matrix (latency-bound config)",
                    "parallelism": "single GPU" if world == 1 else
-                   f"column-sharded x{world} (fused fixed-order all-reduce over NVLink)"},
+                   (f"row-block sharded x{world} (halo exchange + scalar all-reduce over NVLink)"
+                    if cfg["gen"] == "c4" else
+                    f"column-sharded x{world} (fused fixed-order all-reduce over NVLink)")},
         "roofline": roofline,
         "kernel_breakdown": breakdown,
         "gpu_launches": int(launches),
@@ -403,7 +413,11 @@ def e2e_measure(ts, cfg, w, bn, args, dev, world):
         h2d = h2d  # job total: the shards together upload A once per step
 
     def step():
-        if world > 1:
+        if world > 1 and cfg["gen"] == "c4":
+            from paper_2304_12168_b200.shard import RowShardedMatrix
+
+            dm = RowShardedMatrix(w.a, device=dev)
+        elif world > 1:
             dm = ShardedMatrix(a_host, device=dev, local=True, n_global=w.a.shape[1])
         else:
             dm = ts.DeviceMatrix(a_host, device=dev)

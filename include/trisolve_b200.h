@@ -280,6 +280,20 @@ TS_API int ts_comm_connect(ts_comm* comm, const void* all_handles /* world x 128
 TS_API int ts_comm_destroy(ts_comm* comm);
 TS_API int ts_matrix_set_shard(ts_matrix* a, ts_comm* comm, int64_t n_global, int64_t col_offset,
                                double frobenius_global);
+/* Row-block sharding of a square matrix (C4-like banded operators): rank p
+ * owns rows AND columns [off, off + m).  The handle holds the rank's rows of A
+ * and its columns of A (as rows of A^T), indices local to the block (j - off),
+ * reaching at most `halo` entries past either end.  Every vector of a solve on
+ * it is the rank's block (b, x, r, ...); before each pass a halo exchange
+ * copies the neighbours' boundary entries over NVLink, and every reduction is
+ * summed over ranks in rank order.  Bitwise identical operator results to the
+ * unsharded path (each row / column is still added in the reference's order). */
+TS_API int ts_matrix_create_csr_pair(const int32_t* indptr, const int32_t* indices, const double* data,
+                                     int64_t nnz, const int32_t* indptr_t, const int32_t* indices_t,
+                                     const double* data_t, int64_t nnz_t, int64_t m, int64_t halo,
+                                     int device, void* stream, ts_matrix** out);
+TS_API int ts_matrix_set_row_shard(ts_matrix* a, ts_comm* comm, int64_t n_global, int64_t row_offset,
+                                   double frobenius_global);
 
 /* ---- solvers --------------------------------------------------------------- */
 TS_API int ts_cta_solve(const ts_matrix* a, const double* b, const ts_cta_options* opts, double* x_out,

@@ -23,6 +23,7 @@ from .linalg import (
     H_MODE_SYMMETRIC,
     HOperator,
     as_device_matrix,
+    local_rows,
     local_slice,
     norm2,
     shape_of,
@@ -172,6 +173,7 @@ def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResul
     m, n = shape_of(a)
     opts = opts.validated(m)
     b = host_vec(b, m, f"b has shape {np.shape(b)}, expected ({m},)")
+    b = local_rows(a, b)  # row-block shards keep their block of b
     if opts.h_mode == H_MODE_SYMMETRIC and m != n:
         # the reference returns the b = 0 early exit before building H
         if norm2(b) == 0.0:

@@ -182,6 +182,36 @@ __global__ void __launch_bounds__(kNT) k_ar_scalars(Epi epi, CommDev c, unsigned
   epi.finish_block();
 }
 
+// Row-block sharding (square A, SURVEY 8(e) for C4): every vector is split
+// like the rows, and a pass over this rank's rows reads its input vector up to
+// `hw` entries past either end of the local block.  k_halo publishes the
+// block's first and last hw entries in this rank's symmetric slot, meets every
+// rank at the epoch barrier, and copies the left neighbour's tail / right
+// neighbour's head into the vector's halo padding (x[-hw, 0) and
+// x[n, n + hw)).  One block; a pass whose epilogue is inactive skips it on
+// every rank alike (the state is replicated), so epochs stay in step.
+template <class Epi>
+__global__ void __launch_bounds__(kNT) k_halo(Epi epi, double* x, int64_t n, int64_t hw, CommDev c) {
+  __shared__ int live;
+  if (threadIdx.x == 0) live = epi.active();
+  __syncthreads();
+  if (!live) return;
+  const unsigned long long e = *c.epoch + 1;
+  const size_t base = slot_base(c, e);
+  for (int64_t i = threadIdx.x; i < hw; i += kNT) {
+    c.sym[base + i] = x[i];                // head: the left neighbour's right halo
+    c.sym[base + hw + i] = x[n - hw + i];  // tail: the right neighbour's left halo
+  }
+  __syncthreads();
+  comm_barrier(c, e);
+  for (int64_t i = threadIdx.x; i < hw; i += kNT) {
+    x[-hw + i] = c.rank > 0 ? ld_peer(c.psym[c.rank - 1] + base + hw + i) : 0.0;
+    x[n + i] = c.rank + 1 < c.world ? ld_peer(c.psym[c.rank + 1] + base + i) : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *c.epoch = e;
+}
+
 // sum the ranks' partial m-vectors in rank order and run the pass epilogue
 template <class Epi>
 __global__ void __launch_bounds__(kNT) k_ar_vec(int64_t len, Epi epi, Work wk, CommDev c) {

@@ -76,6 +76,15 @@ static int pass(const Mat& M, int trans, const double* x, XS xs, const Epi& e, c
   if (!M.comm) return launch_pass(M, trans, x, xs, e2, w, s);
   const CommDev cd = M.comm->dev_view();
   ++g_launches;
+  if (M.row_shard) {  // halo in, local pass, every reduction slot summed over ranks
+    g_launches += 1;
+    k_halo<Epi><<<1, kNT, 0, s>>>(e2, const_cast<double*>(x), M.m, M.halo, cd);
+    EpiDefer<Epi> d{e2, cd};
+    TS_CHECK(launch_pass(M, trans, x, xs, d, w, s));
+    k_ar_scalars<Epi><<<1, kNT, 0, s>>>(e2, cd, all_slots<Epi::K>());
+    TS_CUDA(cudaGetLastError());
+    return 0;
+  }
   if (!trans) {
     if (M.m > (int64_t)cd.vec_cap) TS_INVAL("communicator vector capacity too small");
     EpiSymStore<Epi> ps{e2, cd};
@@ -98,6 +107,7 @@ static int vecpass(const Mat& M, int64_t len, const Epi& e, const Work& w, cudaS
     e2.tclass = 2;
     mask = Epi::kShardMask;
   }
+  if (M.comm && M.row_shard) mask = all_slots<Epi::K>();  // both vector spaces are split
   if (!M.comm || !mask) return launch_vec(len, M.sms, e2, w, s);
   const CommDev cd = M.comm->dev_view();
   ++g_launches;
@@ -137,16 +147,18 @@ struct Instance {
   cudaStream_t cap = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+  int64_t pad = 0;  // row-block shards: halo entries before and after every vector
   template <class T>
   int alloc(T** out, size_t count) {
     void* p = nullptr;
-    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    const size_t bytes = std::max<size_t>((count + 2 * pad) * sizeof(T), 16);
     if (cudaMalloc(&p, bytes) != cudaSuccess) {
       set_error("cudaMalloc(%zu) for a solver instance failed", bytes);
       return TS_ENOMEM;
     }
+    if (pad) cudaMemset(p, 0, bytes);
     allocs.push_back(p);
-    *out = static_cast<T*>(p);
+    *out = static_cast<T*>(p) + pad;
     return 0;
   }
   int init_common(const Mat& M) {
@@ -218,6 +230,7 @@ static int acquire(const Mat& Mc, const int key[4], const std::function<int(Inst
   }
   Instance* I = new Instance();
   memcpy(I->key, key, sizeof(I->key));
+  I->pad = M.row_shard ? M.halo : 0;
   int rc = I->init_common(M);
   if (!rc) rc = setup(I);
   if (rc) {
@@ -470,7 +483,7 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
   s0.max_iters = a.max_iters;
   s0.halvings_left = std::max(0, a.halvings);
   s0.a_fro = a.gram ? M.fro * M.fro : M.fro;
-  s0.m_rows = mo;
+  s0.m_rows = M.row_shard ? M.m_global : mo;
   s0.n_cols = M.comm ? M.n_global : no;
   TS_CHECK(c.init(s0, trace, trace_cap));
   SolveState* ds = I->ds;
@@ -768,7 +781,7 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   s0.accel_ratio = a.accel_ratio;
   s0.rcond = a.rcond;
   s0.a_fro = M.fro;
-  s0.m_rows = M.m;
+  s0.m_rows = M.row_shard ? M.m_global : M.m;
   s0.n_cols = M.comm ? M.n_global : M.n;
   s0.warm = 1;
   s0.enhanced = a.enhanced;
@@ -1219,7 +1232,32 @@ int ts_matrix_set_shard(ts_matrix* A, ts_comm* h, int64_t n_global, int64_t col_
   A->comm = c;
   A->n_global = c ? n_global : A->n;
   A->col_off = c ? col_offset : 0;
+  A->row_shard = 0;
   if (c) A->fro = fro_global;
+  return 0;
+}
+
+int ts_matrix_set_row_shard(ts_matrix* A, ts_comm* h, int64_t n_global, int64_t row_offset,
+                            double fro_global) {
+  TS_CHECK_HANDLE(A);
+  Comm* c = reinterpret_cast<Comm*>(h);
+  if (!c) TS_INVAL("row sharding needs a communicator");
+  if (c->dev != A->dev) TS_INVAL("communicator and matrix live on different devices");
+  if (A->kind != 1 || A->m != A->n) TS_INVAL("row sharding takes a square local CSR block");
+  if (row_offset < 0 || row_offset + A->m > n_global)
+    TS_INVAL("shard rows [%lld, %lld) outside 0..%lld", (long long)row_offset,
+             (long long)(row_offset + A->m), (long long)n_global);
+  if (A->halo > A->m) TS_INVAL("halo (%lld) wider than the local block (%lld)", (long long)A->halo,
+                               (long long)A->m);
+  if (2 * A->halo > (int64_t)c->vec_cap) TS_INVAL("communicator vector capacity below 2 * halo");
+  destroy_instances(A);
+  A->comm = c;
+  A->row_shard = 1;
+  A->n_global = n_global;
+  A->m_global = n_global;
+  A->row_off = row_offset;
+  A->col_off = row_offset;
+  A->fro = fro_global;
   return 0;
 }
 

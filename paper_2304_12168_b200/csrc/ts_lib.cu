@@ -498,7 +498,7 @@ int ts_device_count(int* count) {
 // storage pool (see retire_take); everything else is freed.
 static int matrix_release(ts_matrix* A, bool complete) {
   if (!A) return 0;
-  if (complete && matrix_pool_enabled() && !A->comm && !A->tval) {
+  if (complete && matrix_pool_enabled() && !A->comm && !A->tval && A->halo == 0) {
     {
       DeviceGuard g(A->dev);
       cudaDeviceSynchronize();  // no solve may still read the storage
@@ -878,6 +878,107 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       A->planN.P = P;
       A->npart = U;
     }
+    if (nnz > 0) {
+      if ((rc = finish_create(A, st, ar))) return fail(rc);
+    } else {
+      A->fro = 0.0;
+    }
+  }
+  *out = A;
+  return 0;
+}
+
+// A row block of a square matrix with both orientations given by the caller
+// (the rank's rows of A and the rank's columns of A as rows of A^T), column /
+// row indices local to the block and reaching `halo` entries past either end.
+int ts_matrix_create_csr_pair(const int32_t* indptr, const int32_t* indices, const double* data,
+                              int64_t nnz, const int32_t* indptr_t, const int32_t* indices_t,
+                              const double* data_t, int64_t nnz_t, int64_t m, int64_t halo,
+                              int device, void* stream, ts_matrix** out) {
+  if (!out) TS_INVAL("null output handle");
+  *out = nullptr;
+  if (m < 1) TS_INVAL("row block must have at least one row");
+  if (halo < 0 || halo > m) TS_INVAL("halo %lld outside 0..%lld", (long long)halo, (long long)m);
+  if (nnz < 0 || nnz >= (int64_t)INT32_MAX || nnz_t < 0 || nnz_t >= (int64_t)INT32_MAX)
+    TS_INVAL("nnz outside the int32 index range");
+  if (!indptr || !indptr_t || (nnz && (!indices || !data)) || (nnz_t && (!indices_t || !data_t)))
+    TS_INVAL("null CSR array");
+  DeviceGuard g(device);
+  setup_pool(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int> rp_h((size_t)m + 1), rpT_h((size_t)m + 1);
+  TS_CUDA(cudaMemcpyAsync(rp_h.data(), indptr, (m + 1) * sizeof(int), cudaMemcpyDefault, st));
+  TS_CUDA(cudaMemcpyAsync(rpT_h.data(), indptr_t, (m + 1) * sizeof(int), cudaMemcpyDefault, st));
+  TS_CUDA(cudaStreamSynchronize(st));
+  if (rp_h[0] != 0 || rp_h[m] != nnz || rpT_h[0] != 0 || rpT_h[m] != nnz_t)
+    TS_INVAL("CSR indptr must start at 0 and end at nnz");
+  for (int64_t r = 0; r < m; ++r)
+    if (rp_h[r + 1] < rp_h[r] || rpT_h[r + 1] < rpT_h[r])
+      TS_INVAL("CSR indptr is not nondecreasing at row %lld", (long long)r);
+  ts_matrix* A = new ts_matrix();
+  A->dev = device;
+  A->sms = sm_count(device);
+  A->kind = 1;
+  A->m = m;
+  A->n = m;
+  A->nnz = nnz;
+  A->halo = halo;
+  int rc = 0;
+  auto fail = [&](int code) {
+    matrix_release(A, false);
+    return code;
+  };
+  {
+    Arena ar(st);
+    const size_t nz = (size_t)std::max<int64_t>(nnz, 1), nzt = (size_t)std::max<int64_t>(nnz_t, 1);
+    if (dev_malloc(&A->rp, (m + 1 + 4) * sizeof(int), device) != cudaSuccess ||
+        dev_malloc(&A->ci, (nz + 4) * sizeof(int), device) != cudaSuccess ||
+        dev_malloc(&A->val, (nz + 2) * sizeof(double), device) != cudaSuccess ||
+        dev_malloc(&A->rpT, (m + 1 + 4) * sizeof(int), device) != cudaSuccess ||
+        dev_malloc(&A->ciT, (nzt + 4) * sizeof(int), device) != cudaSuccess ||
+        dev_malloc(&A->valT, (nzt + 2) * sizeof(double), device) != cudaSuccess) {
+      set_error("cudaMalloc for the row-block CSR failed");
+      return fail(TS_ENOMEM);
+    }
+    if (cudaMemcpyAsync(A->rp, rp_h.data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(A->rpT, rpT_h.data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice, st) ||
+        (nnz && cudaMemcpyAsync(A->ci, indices, nnz * sizeof(int), cudaMemcpyDefault, st)) ||
+        (nnz && cudaMemcpyAsync(A->val, data, nnz * sizeof(double), cudaMemcpyDefault, st)) ||
+        (nnz_t && cudaMemcpyAsync(A->ciT, indices_t, nnz_t * sizeof(int), cudaMemcpyDefault, st)) ||
+        (nnz_t && cudaMemcpyAsync(A->valT, data_t, nnz_t * sizeof(double), cudaMemcpyDefault, st))) {
+      set_error("row-block CSR upload failed");
+      return fail(TS_ECUDA);
+    }
+    // local indices must stay inside [-halo, m + halo)
+    Work wk;
+    double* rng;
+    if ((rc = make_work(ar, work_blocks(A->sms), &wk)) || (rc = ar.get(&rng, 2))) return fail(rc);
+    double hr[4] = {0, 0, 0, 0};
+    if (nnz) {
+      EpiIdxRange er{A->ci, rng};
+      if ((rc = launch_vec(nnz, A->sms, er, wk, st))) return fail(rc);
+      cudaMemcpyAsync(hr, rng, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+    }
+    if (nnz_t) {
+      EpiIdxRange er{A->ciT, rng};
+      if ((rc = launch_vec(nnz_t, A->sms, er, wk, st))) return fail(rc);
+      cudaMemcpyAsync(hr + 2, rng, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+    }
+    if ((nnz && (hr[0] < -(double)halo || hr[1] >= (double)(m + halo))) ||
+        (nnz_t && (hr[2] < -(double)halo || hr[3] >= (double)(m + halo)))) {
+      set_error("row-block index outside [-%lld, %lld)", (long long)halo, (long long)(m + halo));
+      return fail(TS_EINVAL);
+    }
+    RowPlan pN, pT;
+    if ((rc = plan_rows_csr(rp_h.data(), m, nnz, A->sms, &pN, st))) return fail(rc);
+    if ((rc = plan_rows_csr(rpT_h.data(), m, nnz_t, A->sms, &pT, st))) {
+      free_plan(pN);
+      return fail(rc);
+    }
+    adopt_plan(A->planN, pN, st);
+    adopt_plan(A->planT, pT, st);
     if (nnz > 0) {
       if ((rc = finish_create(A, st, ar))) return fail(rc);
     } else {

@@ -74,6 +74,11 @@ struct Mat {
   // column shard of a matrix split over ranks (nullptr: unsharded)
   Comm* comm = nullptr;
   int64_t n_global = 0, col_off = 0;
+  // row-block shard (square A): rows / columns [row_off, row_off + m) are this
+  // rank's; column indices are local (j - row_off) and reach `halo` entries
+  // past either end, served from neighbours before every pass (k_halo)
+  int row_shard = 0;
+  int64_t halo = 0, m_global = 0, row_off = 0;
   // solver instances (buffers + instantiated graphs) cached per solver shape
   std::mutex cache_mu;
   std::vector<Instance*> cache;

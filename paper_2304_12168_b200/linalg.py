@@ -161,7 +161,7 @@ def as_device_matrix(a):
         return a, False
     if isinstance(a, GramProduct):
         return a.device_matrix, True
-    if type(a).__name__ == "ShardedMatrix":
+    if type(a).__name__ in ("ShardedMatrix", "RowShardedMatrix"):
         return a.device_matrix, False
     if isinstance(a, np.ndarray) or sparse.issparse(a) or _is_torch(a):
         return DeviceMatrix(a), False
@@ -173,12 +173,20 @@ def as_device_matrix(a):
 
 
 def local_slice(a, v, n_local: int):
-    """For a column-sharded matrix, this rank's slice of an n-vector given
-    either globally or already locally; identity otherwise."""
-    if v is None or type(a).__name__ != "ShardedMatrix":
+    """For a sharded matrix, this rank's slice of an n-vector given either
+    globally or already locally; identity otherwise."""
+    if v is None or type(a).__name__ not in ("ShardedMatrix", "RowShardedMatrix"):
         return v
     arr = np.asarray(v, dtype=np.float64)
     return a.local(arr) if arr.shape == (a.n_global,) else arr
+
+
+def local_rows(a, b):
+    """For a row-block sharded matrix, this rank's block of an m-vector (b);
+    identity otherwise (column shards keep m-vectors replicated)."""
+    if b is None or type(a).__name__ != "RowShardedMatrix":
+        return b
+    return a.local(b)
 
 
 def matvec(a, v) -> np.ndarray:

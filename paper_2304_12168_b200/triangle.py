@@ -20,8 +20,8 @@ import numpy as np
 
 from . import _native as N
 from ._solve import build_result, host_vec, rows_to_trace, trace_buffer
-from .linalg import (as_device_matrix, dot, local_slice, matvec, matvec_transpose, norm2, residual,
-                     shape_of)
+from .linalg import (as_device_matrix, dot, local_rows, local_slice, matvec, matvec_transpose, norm2,
+                     residual, shape_of)
 from .results import (
     APPROX_SOLUTION,
     ITERATION_CAP,
@@ -116,6 +116,7 @@ def solve_adaptive(a, b, eps, eps_prime=None, rho_cap=None, max_iters=100_000,
     """Growing-radius solver (triangle.py:170-251), loop on the device."""
     m, n = shape_of(a)
     b = host_vec(b, m, f"b has shape {np.shape(b)}, expected ({m},)")
+    b = local_rows(a, b)  # row-block shards keep their block of b
     dm, gram, mo, nn = _dims(a)
     o = N.TaOptions()
     o.eps = float(eps)

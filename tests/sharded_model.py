@@ -142,3 +142,85 @@ def cta_sharded(a_loc, b, epsilon, max_iters, t_max=5):
     fr = b - _mv(a_loc, x)
     return dict(status=status, iterations=it, x=x, residual_norm=float(np.linalg.norm(fr)),
                 normal_residual_norm=_nrm2_sharded(_rmv(a_loc, fr)))
+
+
+# ----------------------------------------------------------- row blocks ----
+# Row-block sharding of a square matrix (RowShardedMatrix, k_halo): every
+# vector is split like the rows; a pass reads its input through a halo of the
+# band's half-width obtained from the neighbours; every dot / norm is a local
+# sum all-reduced over ranks.
+
+def _halo(v_loc, hw):
+    """[left neighbour's tail | own block | right neighbour's head] (k_halo)."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    parts = [None] * world
+    dist.all_gather_object(parts, (v_loc[:hw].copy(), v_loc[len(v_loc) - hw:].copy()))
+    left = parts[rank - 1][1] if rank > 0 else np.zeros(hw)
+    right = parts[rank + 1][0] if rank + 1 < world else np.zeros(hw)
+    return np.concatenate([left, v_loc, right])
+
+
+def shifted_blocks(rows, cols, r0, hw):
+    """Local CSR blocks whose indices address the halo-extended vector
+    (global index j -> j - r0 + hw): the device's (j - r0) plus the offset of
+    its halo padding."""
+    import scipy.sparse as sp
+
+    n_p = rows.shape[0]
+    ext = n_p + 2 * hw
+    shift = lambda blk: sp.csr_array((blk.data, blk.indices - r0 + hw, blk.indptr),  # noqa: E731
+                                     shape=(n_p, ext))
+    return shift(rows), shift(cols)
+
+
+def _dot_rows(u, v):
+    return float(_ar(float(np.dot(u, v)))[0])
+
+
+def cta_row_sharded(rows_ext, cols_ext, hw, b_loc, epsilon, max_iters, t_max=5):
+    """centering_solve (centering.py:263-358, Gram mode) on row blocks."""
+    x = np.zeros(rows_ext.shape[0])
+    r = b_loc.copy()
+    bn = math.sqrt(_dot_rows(b_loc, b_loc))
+    eps_abs = epsilon * bn
+    m_glob = int(_ar(float(len(b_loc)))[0])
+    sched = port.schedule(min(t_max, m_glob))
+    status, it = "iteration_cap", 0
+    while it < max_iters:
+        rn = math.sqrt(_dot_rows(r, r))
+        if rn <= eps_abs:
+            status = "approx_solution"
+            break
+        t = next(sched)
+        p, q = [r], []
+        for _ in range(t):
+            q.append(cols_ext @ _halo(p[-1], hw))   # A^T p: own columns, rows ascending
+            p.append(rows_ext @ _halo(q[-1], hw))   # A q: own rows
+        phi = np.array([_dot_rows(p[k // 2], p[k - k // 2]) for k in range(1, 2 * t + 1)])
+        if phi[1] == 0.0:
+            status = "normal_eq_solution"
+            break
+        atr = math.sqrt(_dot_rows(q[0], q[0]))
+        pick = None
+        for order in range(t, 0, -1):
+            al = port.hankel_coeffs(phi, order)
+            cand = r.copy()
+            for i in range(order):
+                cand -= al[i] * p[i + 1]
+            cn = math.sqrt(_dot_rows(cand, cand))
+            if pick is None or cn < pick[0]:
+                pick = (cn, order, al, cand)
+            if cn <= rn * (1.0 + 1e-13):
+                pick = (cn, order, al, cand)
+                break
+        if atr * atr <= eps_abs * eps_abs:
+            status = "normal_eq_solution"
+            break
+        _, order, al, r = pick
+        for i in range(order):
+            x = x + al[i] * q[i]
+        it += 1
+    fr = b_loc - rows_ext @ _halo(x, hw)
+    atf = cols_ext @ _halo(fr, hw)
+    return dict(status=status, iterations=it, x=x, residual_norm=math.sqrt(_dot_rows(fr, fr)),
+                normal_residual_norm=math.sqrt(_dot_rows(atf, atf)))

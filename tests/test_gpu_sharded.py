@@ -80,3 +80,30 @@ def test_sharded_ta_and_lp_sparse(group):
     assert (r1.status, r1.iterations) == (r0.status, r0.iterations)
     assert rel_l2(r1.x, r0.x) <= 1e-9
     assert r1.residual_norm == pytest.approx(r0.residual_norm, rel=1e-6)
+
+
+def test_row_sharded_cta_and_ta_convdiff(group):
+    """Row-block sharding (RowShardedMatrix: halo exchange kernel, both
+    orientations given per rank, every reduction deferred to the scalar
+    all-reduce) at world size 1 against the unsharded path: the passes add
+    every row / column in the same order, so x must be bitwise equal."""
+    import paper_2304_12168_b200 as ts
+    from paper_2304_12168_b200 import workloads as W
+    from paper_2304_12168_b200.shard import RowShardedMatrix
+
+    w = W.convdiff_upwind(40, seed=2)  # 1600 x 1600 five-point operator
+    dm = ts.DeviceMatrix(w.a)
+    rs = RowShardedMatrix(w.a)
+    assert rs.halo == 0 and rs.local_shape == w.a.shape
+    opts = ts.CenteringOptions(epsilon=1e-8, max_iters=50)
+    r0 = ts.centering_solve(dm, w.b, opts)
+    r1 = ts.centering_solve(rs, w.b, opts)
+    assert (r1.status, r1.iterations) == (r0.status, r0.iterations)
+    assert np.array_equal(r1.x, r0.x)
+    assert r1.residual_norm == r0.residual_norm
+    assert r1.kernel_launches > r0.kernel_launches  # halo + scalar all-reduce kernels ran
+    bn = float(np.linalg.norm(w.b))
+    t0 = ts.solve_adaptive(dm, w.b, eps=1e-6 * bn, max_iters=60)
+    t1 = ts.solve_adaptive(rs, w.b, eps=1e-6 * bn, max_iters=60)
+    assert (t1.status, t1.iterations) == (t0.status, t0.iterations)
+    assert np.array_equal(t1.x, t0.x)

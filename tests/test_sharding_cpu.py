@@ -45,6 +45,18 @@ def _worker(rank, world, port, case, outdir):
         c0, c1 = column_range(w.a.shape[1], world, rank)
         out = SM.ta_adaptive_sharded(local_block(w.a, c0, c1), w.b,
                                      1e-8 * np.linalg.norm(w.b), 30)
+    elif case == "cta_rows_convdiff":  # C4 family, row blocks + halo exchange
+        from paper_2304_12168_b200.shard import row_blocks
+
+        w = W.convdiff_upwind(24, seed=2)
+        c0, c1 = column_range(w.a.shape[0], world, rank)
+        rows, cols, hw = row_blocks(w.a, c0, c1)
+        import torch
+        t = torch.tensor([hw], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        hw = int(t.item())
+        rows_ext, cols_ext = SM.shifted_blocks(rows, cols, c0, hw)
+        out = SM.cta_row_sharded(rows_ext, cols_ext, hw, w.b[c0:c1], 1e-8, 40)
     else:  # lp_sparse: the C5 family (cone stall)
         w = W.lp_columns(60, 3000, 10, seed=5)
         c0, c1 = column_range(w.a.shape[1], world, rank)
@@ -56,7 +68,7 @@ def _worker(rank, world, port, case, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["cta_dense", "ta_dense", "lp_sparse"])
+@pytest.mark.parametrize("case", ["cta_dense", "ta_dense", "lp_sparse", "cta_rows_convdiff"])
 def test_sharded_decomposition_matches_oracle(case, tmp_path):
     import torch.multiprocessing as mp
 
@@ -74,6 +86,9 @@ def test_sharded_decomposition_matches_oracle(case, tmp_path):
     elif case == "ta_dense":
         w = W.dense_gaussian(40, 90, seed=4)
         ref = port.ta_adaptive(w.a, w.b, eps=1e-8 * np.linalg.norm(w.b), max_iters=30)
+    elif case == "cta_rows_convdiff":
+        w = W.convdiff_upwind(24, seed=2)
+        ref = port.cta_solve(w.a, w.b, epsilon=1e-8, max_iters=40)
     else:
         w = W.lp_columns(60, 3000, 10, seed=5)
         ref = port.lp_feasibility(w.a, w.b, eps=1e-6 * np.linalg.norm(w.b), max_iters=1000)
@@ -81,7 +96,7 @@ def test_sharded_decomposition_matches_oracle(case, tmp_path):
         assert str(p["status"]) == ref["status"]
         assert int(p["iterations"]) == ref["iterations"]
         assert float(p["residual_norm"]) == pytest.approx(ref["residual_norm"], rel=1e-9)
-    if "trace" in ref and case != "cta_dense":
+    if "trace" in ref and not case.startswith("cta"):
         assert list(parts[0]["events"]) == [row[4] for row in ref["trace"]]
     assert np.linalg.norm(x - ref["x"]) <= 1e-9 * max(np.linalg.norm(ref["x"]), 1e-300)
 
@@ -110,3 +125,22 @@ def test_local_block_dense_and_sparse():
         blk = local_block(csr, c0, c1)
         assert blk.format == "csr"
         assert np.array_equal(blk.toarray(), dense[:, c0:c1])
+
+
+def test_row_blocks_halo_width():
+    from paper_2304_12168_b200 import workloads as W
+    from paper_2304_12168_b200.shard import column_range, row_blocks
+
+    w = W.convdiff_upwind(10, seed=1)  # 5-point stencil: half-bandwidth = grid = 10
+    n = w.a.shape[0]
+    for world in (1, 2, 3):
+        for rank in range(world):
+            r0, r1 = column_range(n, world, rank)
+            rows, cols, hw = row_blocks(w.a, r0, r1)
+            assert hw == (0 if world == 1 else 10)
+            assert rows.shape == (r1 - r0, n) and cols.shape == (r1 - r0, n)
+            assert rows.indices.min() >= r0 - hw and rows.indices.max() < r1 + hw
+            # columns of A as rows of A^T, row indices ascending (the reference's order)
+            assert all(np.all(np.diff(cols.indices[cols.indptr[i]:cols.indptr[i + 1]]) > 0)
+                       for i in range(r1 - r0))
+            assert np.array_equal(cols.toarray(), w.a.toarray()[:, r0:r1].T)
