@@ -235,6 +235,16 @@ TS_API int ts_mm_to_device(const ts_mm* mm, int device, void* stream, ts_matrix*
                            int64_t* duplicates);
 TS_API int ts_mm_free(ts_mm* mm);
 
+/* ---- device gallery (reference gallery.py:64-71, 118-191) -------------------
+ * The 5-point stencil families (poisson Dirichlet / Neumann, convdiff) and
+ * Clement generated straight into a device CSR handle.  Stencil coefficients
+ * are passed in (computed by the caller with the reference's expressions);
+ * center_mode = 1 puts the neighbour count on the diagonal (Neumann). */
+TS_API int ts_matrix_gen_stencil5(int64_t grid, double center, double west, double east, double south,
+                                  double north, int32_t center_mode, int device, void* stream,
+                                  ts_matrix** out);
+TS_API int ts_matrix_gen_clement(int64_t n, int device, void* stream, ts_matrix** out);
+
 /* ---- operator layer -------------------------------------------------------- */
 TS_API int ts_matvec(const ts_matrix* a, const double* x, double* y, void* stream);   /* y = A x  */
 TS_API int ts_rmatvec(const ts_matrix* a, const double* x, double* y, void* stream);  /* y = A^T x */

@@ -26,6 +26,7 @@ EXPORTS = (
     "ts_pool_trim", "ts_host_alloc", "ts_host_free",
     "ts_mm_parse", "ts_mm_coo", "ts_mm_dense", "ts_mm_to_device", "ts_mm_free",
     "ts_matrix_create_csr_pair", "ts_matrix_set_row_shard",
+    "ts_matrix_gen_stencil5", "ts_matrix_gen_clement",
 )
 
 # statuses (results.py:11-18)
@@ -124,6 +125,9 @@ def _declare(lib):
         "ts_comm_destroy": ([_P], C.c_int),
         "ts_matrix_set_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
         "ts_matrix_set_row_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
+        "ts_matrix_gen_stencil5": ([_I64, _D, _D, _D, _D, _D, _I32, C.c_int, _P, C.POINTER(_P)],
+                                   C.c_int),
+        "ts_matrix_gen_clement": ([_I64, C.c_int, _P, C.POINTER(_P)], C.c_int),
         "ts_matrix_create_csr_pair": ([_P, _P, _P, _I64, _P, _P, _P, _I64, _I64, _I64, C.c_int, _P,
                                        C.POINTER(_P)], C.c_int),
         "ts_cta_solve": ([_P, _P, C.POINTER(CtaOptions), _P, _P, _I64, C.POINTER(Result), _P],

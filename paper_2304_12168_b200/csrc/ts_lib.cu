@@ -989,6 +989,109 @@ int ts_matrix_create_csr_pair(const int32_t* indptr, const int32_t* indices, con
   return 0;
 }
 
+// ------------------------------------------------------ device gallery ----
+// Deterministic sparse families generated straight into device CSR
+// (reference gallery.py:64-71, 118-191); the coefficients arrive computed on
+// the host with the reference's own expressions, so values are bit-identical.
+namespace ts {
+__global__ void k_stencil5_count(int64_t g, int* cnt) {
+  const int64_t n = g * g;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ix = k % g, iy = k / g;
+    cnt[k] = 1 + (ix > 0) + (ix < g - 1) + (iy > 0) + (iy < g - 1);
+  }
+}
+// entries in ascending column order: south, west, centre, east, north
+__global__ void k_stencil5_fill(int64_t g, double c, double w, double e, double s, double nn, int mode,
+                                const int* rp, int* ci, double* val) {
+  const int64_t n = g * g;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ix = k % g, iy = k / g;
+    int q = rp[k];
+    const int nb = (ix > 0) + (ix < g - 1) + (iy > 0) + (iy < g - 1);
+    if (iy > 0) { ci[q] = (int)(k - g); val[q++] = s; }
+    if (ix > 0) { ci[q] = (int)(k - 1); val[q++] = w; }
+    ci[q] = (int)k;
+    val[q++] = mode ? (double)nb : c;
+    if (ix < g - 1) { ci[q] = (int)(k + 1); val[q++] = e; }
+    if (iy < g - 1) { ci[q] = (int)(k + g); val[q++] = nn; }
+  }
+}
+// Clement: A[i, i-1] = sqrt(i (n - i)), A[i, i+1] = sqrt((i + 1) (n - i - 1))
+__global__ void k_clement_fill(int64_t n, int* rp, int* ci, double* val) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+    rp[i] = (int)(i == 0 ? 0 : (i == n ? 2 * n - 2 : 2 * i - 1));
+    if (i == n) continue;
+    int q = i == 0 ? 0 : (int)(2 * i - 1);
+    if (i > 0) {
+      const double k = (double)i;
+      ci[q] = (int)(i - 1);
+      val[q++] = sqrt(__dmul_rn(k, __dsub_rn((double)n, k)));
+    }
+    if (i < n - 1) {
+      const double k = (double)(i + 1);
+      ci[q] = (int)(i + 1);
+      val[q] = sqrt(__dmul_rn(k, __dsub_rn((double)n, k)));
+    }
+  }
+}
+}  // namespace ts
+
+int ts_matrix_gen_stencil5(int64_t grid, double center, double west, double east, double south,
+                           double north, int32_t center_mode, int device, void* stream, ts_matrix** out) {
+  if (!out) TS_INVAL("null output handle");
+  *out = nullptr;
+  if (grid < 2) TS_INVAL("grid must be at least 2");
+  const int64_t n = grid * grid, nnz = 5 * n - 4 * grid;
+  if (nnz >= (int64_t)INT32_MAX) TS_INVAL("nnz outside the int32 index range");
+  DeviceGuard g(device);
+  setup_pool(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = 0;
+  {
+    Arena ar(st);
+    int *cnt, *rp, *ci;
+    double* val;
+    if ((rc = ar.get(&cnt, n + 1)) || (rc = ar.get(&rp, n + 1)) || (rc = ar.get(&ci, nnz)) ||
+        (rc = ar.get(&val, nnz)))
+      return rc;
+    TS_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(int), st));
+    k_stencil5_count<<<grid_for(n), 256, 0, st>>>(grid, cnt);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, rp, (int)(n + 1), st);
+    char* tmp;
+    if ((rc = ar.get(&tmp, std::max<size_t>(tb, 16)))) return rc;
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, rp, (int)(n + 1), st);
+    k_stencil5_fill<<<grid_for(n), 256, 0, st>>>(grid, center, west, east, south, north, center_mode,
+                                                  rp, ci, val);
+    TS_CUDA(cudaGetLastError());
+    rc = ts_matrix_create_csr(rp, ci, val, n, n, nnz, device, stream, out);
+  }
+  return rc;
+}
+
+int ts_matrix_gen_clement(int64_t n, int device, void* stream, ts_matrix** out) {
+  if (!out) TS_INVAL("null output handle");
+  *out = nullptr;
+  if (n < 2) TS_INVAL("n must be at least 2");
+  const int64_t nnz = 2 * n - 2;
+  if (nnz >= (int64_t)INT32_MAX) TS_INVAL("nnz outside the int32 index range");
+  DeviceGuard g(device);
+  setup_pool(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = 0;
+  {
+    Arena ar(st);
+    int *rp, *ci;
+    double* val;
+    if ((rc = ar.get(&rp, n + 1)) || (rc = ar.get(&ci, nnz)) || (rc = ar.get(&val, nnz))) return rc;
+    k_clement_fill<<<grid_for(n + 1), 256, 0, st>>>(n, rp, ci, val);
+    TS_CUDA(cudaGetLastError());
+    rc = ts_matrix_create_csr(rp, ci, val, n, n, nnz, device, stream, out);
+  }
+  return rc;
+}
+
 // ---------------------------------------------------------- Matrix Market
 struct ts_mm : public ts::MmParsed {};
 
