@@ -116,9 +116,23 @@ __global__ void __launch_bounds__(256, NB) k_v1(const double* __restrict__ a, in
 
 // A^T v core loop (k_cols_tile<Epi,2> without the merges): RU rows in flight
 // per thread, NB blocks per SM; column sums of each segment to `out`
-template <int RU, int NB>
+struct XSr {  // the library's runtime input transform (identity when sp == nullptr)
+  const double* sp = nullptr;
+  int relu = 0;
+  double s = 1.0;
+  __device__ __forceinline__ double operator()(double v) const {
+    if (!sp) return v;
+    if (relu) v = (v >= 0.0 || v != v) ? v : 0.0;
+    return __dmul_rn(s, v);
+  }
+};
+struct XSi {
+  __device__ __forceinline__ double operator()(double v) const { return v; }
+};
+template <int RU, int NB, class XT = XSi>
 __global__ void __launch_bounds__(256, NB) k_t(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
-                                              const double* __restrict__ x, double* __restrict__ out) {
+                                              const double* __restrict__ x, double* __restrict__ out,
+                                              XT xs = XT{}) {
   const int64_t nct = (n + TW - 1) / TW, U = nct * m, P = gridDim.x, b = blockIdx.x;
   const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
   for (int64_t u = U0; u < U1;) {
@@ -133,7 +147,7 @@ __global__ void __launch_bounds__(256, NB) k_t(const double* __restrict__ a, int
 #pragma unroll
       for (int i = 0; i < RU; ++i) v[i] = ld_stream2(base + (r + i) * lda);
 #pragma unroll
-      for (int i = 0; i < RU; ++i) xr[i] = __ldg(x + r + i);
+      for (int i = 0; i < RU; ++i) xr[i] = xs(__ldg(x + r + i));
 #pragma unroll
       for (int i = 0; i < RU; ++i) {
         ac[i & 1][0] = fma(v[i].x, xr[i], ac[i & 1][0]);
@@ -211,6 +225,10 @@ int main() {
     float t = timeit([&] { k_t<RU, NB><<<sms * NB, 256>>>(a, lda, m, n, xmd, tout); }, 30);    \
     printf("%-24s %8.2f us %7.1f GB/s\n", "A^T RU" #RU " " #NB "blk", t * 1e3, bytes / (t * 1e-3) / 1e9); \
   }
-  VT(8, 4) VT(16, 4) VT(8, 2) VT(16, 2) VT(24, 2) VT(32, 1) VT(12, 3)
+  VT(8, 4) VT(12, 3)
+  {
+    float t = timeit([&] { k_t<12, 3, XSr><<<sms * 3, 256>>>(a, lda, m, n, xmd, tout, XSr{}); }, 30);
+    printf("%-24s %8.2f us %7.1f GB/s\n", "A^T RU12 3blk runtime XS", t * 1e3, bytes / (t * 1e-3) / 1e9);
+  }
   return 0;
 }
