@@ -46,6 +46,23 @@ static int capture_into(cudaStream_t cap, cudaGraph_t g, const std::function<int
   return 0;
 }
 
+// ---- solve inputs without the copy engines -------------------------------
+// A solve's host->device traffic (its state, b, x0) goes through kernels that
+// read pinned / mapped host memory over PCIe instead of cudaMemcpy: the H2D
+// copy engine may be busy for tens of milliseconds with another stream's
+// matrix upload (the double-buffered pipeline of same-shaped problems), and a
+// small cudaMemcpy queued behind it would stall the whole solve.
+__global__ void k_put_state(SolveState* ds, const SolveState s) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ds = s;
+}
+__global__ void k_put_ll(long long* p, long long v) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p = v;
+}
+__global__ void k_copy_in(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 static SolveState* pinned_state() {
   static thread_local SolveState* hs = nullptr;
   if (!hs) {
@@ -148,6 +165,39 @@ struct Instance {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   int64_t pad = 0;  // row-block shards: halo entries before and after every vector
+  double* hstage = nullptr;  // pinned staging of pageable host inputs (lazily sized)
+  size_t hstage_n = 0;
+  // dst (device, n) <- src (device, pinned host, or pageable host), copy-engine free
+  int stage_in(double* dst, const double* src, int64_t n, cudaStream_t st) {
+    if (n <= 0) return 0;
+    cudaPointerAttributes at;
+    const double* from = src;
+    if (cudaPointerGetAttributes(&at, src) != cudaSuccess) {
+      cudaGetLastError();
+      at.type = cudaMemoryTypeUnregistered;
+    }
+    if (at.type == cudaMemoryTypeHost && at.devicePointer) {
+      from = static_cast<const double*>(at.devicePointer);
+    } else if (at.type == cudaMemoryTypeUnregistered) {  // pageable: through pinned staging
+      if (hstage_n < (size_t)n) {
+        TS_CUDA(cudaStreamSynchronize(st));
+        if (hstage) cudaFreeHost(hstage);
+        hstage = nullptr;
+        hstage_n = 0;
+        TS_CUDA(cudaHostAlloc(&hstage, (size_t)n * sizeof(double), cudaHostAllocMapped));
+        hstage_n = (size_t)n;
+      }
+      TS_CUDA(cudaStreamSynchronize(st));  // the previous staged input was consumed
+      memcpy(hstage, src, (size_t)n * sizeof(double));
+      double* dp = nullptr;
+      TS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), hstage, 0));
+      from = dp;
+    }
+    const int64_t g = std::min<int64_t>((n + 255) / 256, 1024);
+    k_copy_in<<<(int)g, 256, 0, st>>>(dst, from, n);
+    TS_CUDA(cudaGetLastError());
+    return 0;
+  }
   template <class T>
   int alloc(T** out, size_t count) {
     void* p = nullptr;
@@ -181,6 +231,7 @@ struct Instance {
     return 0;
   }
   ~Instance() {
+    if (hstage) cudaFreeHost(hstage);
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (cap) cudaStreamDestroy(cap);
@@ -291,7 +342,8 @@ struct SolveCtx {
     for (int i = 0; i < 4; ++i) init_state.kt[i] = KTimer{~0ull, 0ull, 0, 0};
     *hs = init_state;
     TS_CUDA(cudaEventRecord(I->ev0, st));
-    TS_CUDA(cudaMemcpyAsync(I->ds, hs, sizeof(SolveState), cudaMemcpyHostToDevice, st));
+    k_put_state<<<1, 32, 0, st>>>(I->ds, init_state);
+    TS_CUDA(cudaGetLastError());
     return 0;
   }
 
@@ -320,9 +372,9 @@ struct SolveCtx {
       flushed += chunk;
     }
     *hflushed = flushed;
-    TS_CUDA(cudaMemcpyAsync(&I->ds->trace_flushed, hflushed, sizeof(long long),
-                            cudaMemcpyHostToDevice, st));
-    TS_CUDA(cudaStreamSynchronize(st));  // hflushed / ring reuse
+    k_put_ll<<<1, 32, 0, st>>>(&I->ds->trace_flushed, flushed);
+    TS_CUDA(cudaGetLastError());
+    TS_CUDA(cudaStreamSynchronize(st));  // ring reuse
     return 0;
   }
 
@@ -489,11 +541,11 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
   SolveState* ds = I->ds;
   const Work& wk = I->wk;
   TaKernels K{M, I, a.gram, relu, mo, no, mx};
-  TS_CUDA(cudaMemcpyAsync(I->b, b_in, mo * sizeof(double), cudaMemcpyDefault, st));
+  TS_CHECK(I->stage_in(I->b, b_in, mo, st));
 
   // ---- init (triangle.py:197-204, feasibility.py:77-79)
   if (a.x0) {
-    TS_CUDA(cudaMemcpyAsync(I->x0, a.x0, no * sizeof(double), cudaMemcpyDefault, st));
+    TS_CHECK(I->stage_in(I->x0, a.x0, no, st));
     EpiNormTo en;
     en.st = ds; en.v = I->x0; en.len = no; en.what = 0;
     TS_CHECK(vecpass(M, no, en, wk, st));
@@ -789,9 +841,9 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   TS_CHECK(c.init(s0, trace, trace_cap));
   SolveState* ds = I->ds;
   const Work& wk = I->wk;
-  TS_CUDA(cudaMemcpyAsync(I->b, b_in, M.m * sizeof(double), cudaMemcpyDefault, st));
+  TS_CHECK(I->stage_in(I->b, b_in, M.m, st));
   if (a.x_start) {
-    TS_CUDA(cudaMemcpyAsync(I->xs, a.x_start, M.n * sizeof(double), cudaMemcpyDefault, st));
+    TS_CHECK(I->stage_in(I->xs, a.x_start, M.n, st));
     EpiCopyWarm ec;
     ec.st = ds; ec.src = I->xs; ec.dst = I->x;
     TS_CHECK(vecpass(M, M.n, ec, wk, st));

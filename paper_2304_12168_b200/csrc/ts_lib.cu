@@ -141,6 +141,26 @@ static void free_plan(RowPlan& p) {
   p.blk = nullptr;
 }
 
+// Dense upload: one linear copy when both sides are contiguous, else row slabs
+// of ~16 MB (one copy-engine command per slab, so
+// the small host<->device copies of a solve running concurrently on another
+// stream (state, b, x) are not queued behind a whole 800 MB transfer
+// (double-buffered pipelines of same-shaped problems).
+static cudaError_t upload_rows(double* dst, int64_t dld, const double* src, int64_t sld, int64_t m,
+                               int64_t n, cudaStream_t st) {
+  if (dld == n && sld == n)  // contiguous both sides: one linear copy
+    return cudaMemcpyAsync(dst, src, (size_t)m * n * sizeof(double), cudaMemcpyDefault, st);
+  const int64_t slab = std::max<int64_t>(1, ((int64_t)16 << 20) / std::max<int64_t>(1, n * 8));
+  for (int64_t r = 0; r < m; r += slab) {
+    const int64_t rows = std::min(slab, m - r);
+    cudaError_t e = cudaMemcpy2DAsync(dst + r * dld, dld * sizeof(double), src + r * sld,
+                                      sld * sizeof(double), n * sizeof(double), rows,
+                                      cudaMemcpyDefault, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 // a new plan replaces `old` in place when the geometry is unchanged (cached
 // graphs bake the grid and the plan-table pointer); false: geometry changed
 static bool adopt_plan(RowPlan& old, RowPlan& nw, cudaStream_t st) {
@@ -164,6 +184,32 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, cudaStream_t st) {
   }
   nw = RowPlan();
   return same;
+}
+
+// Device -> host reads of the creation path land in pinned scratch first: a
+// copy into pageable memory is synchronous inside the driver and stalls the
+// kernels of solves running concurrently on other streams.
+static cudaError_t d2h_pinned(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  static thread_local void* buf = nullptr;
+  static thread_local size_t cap = 0;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, src) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+  }
+  if (cap < bytes) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    cudaError_t e = cudaHostAlloc(&buf, bytes, cudaHostAllocDefault);
+    if (e != cudaSuccess) return e;
+    cap = bytes;
+  }
+  cudaError_t e = cudaMemcpyAsync(buf, src, bytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) memcpy(dst, buf, bytes);
+  return e;
 }
 
 // Pinned host blocks for solver outputs (x, b', r): the device->host copy of
@@ -286,6 +332,9 @@ int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* ou
     if (force && !strcmp(force, "thread")) thread_rows = true;
     if (force && (!strcmp(force, "warp") || !strcmp(force, "stream"))) thread_rows = false;
     p.kind = thread_rows ? PLAN_SHORT : PLAN_WARP;
+    // TS_CSR_SHORT=pf: the prefetching warp kernel (opt-in: 39.0 vs 37.9 us on
+    // C5's A^T v inside the library, despite 33.6 vs 41 us in the microbench)
+    if (!thread_rows && force && !strcmp(force, "pf")) p.kind = PLAN_WARP_PF;
     int64_t g = thread_rows ? (rows + kNT - 1) / kNT : (rows + kNT * 4 - 1) / (kNT * 4);
     p.P = (int)std::max<int64_t>(1, std::min(g, pmax));
     // TS_CSR_SHORT=stream: the TMA-streamed chunk kernel (opt-in: bitwise
@@ -599,8 +648,13 @@ static int finish_create(ts_matrix* A, cudaStream_t st, Arena& ar) {
     EpiFroVals e{A->val, dfro};
     TS_CHECK(launch_vec(A->nnz, A->sms, e, wk, st));
   }
-  TS_CUDA(cudaMemcpyAsync(&A->fro, dfro, sizeof(double), cudaMemcpyDeviceToHost, st));
+  // read back through pinned memory: a device->pageable copy is synchronous in
+  // the driver and stalled concurrent solves on other streams
+  static thread_local double* hfro = nullptr;
+  if (!hfro) TS_CUDA(cudaHostAlloc(&hfro, sizeof(double), cudaHostAllocDefault));
+  TS_CUDA(cudaMemcpyAsync(hfro, dfro, sizeof(double), cudaMemcpyDeviceToHost, st));
   TS_CUDA(cudaStreamSynchronize(st));
+  A->fro = *hfro;
   return 0;
 }
 
@@ -620,8 +674,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
     int rc = 0;
     {
       Arena ar(st);
-      cudaError_t e = cudaMemcpy2DAsync(R->a, R->lda * sizeof(double), a, lda * sizeof(double),
-                                        n * sizeof(double), m, cudaMemcpyDefault, st);
+      cudaError_t e = upload_rows(R->a, R->lda, a, lda, m, n, st);
       if (e != cudaSuccess) {
         set_error("dense upload failed: %s", cudaGetErrorString(e));
         rc = TS_ECUDA;
@@ -653,9 +706,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
       rc = TS_ENOMEM;
     }
     if (!rc && A->lda != n) e = cudaMemsetAsync(A->a, 0, (size_t)A->lda * m * sizeof(double), st);
-    if (!rc && e == cudaSuccess)
-      e = cudaMemcpy2DAsync(A->a, A->lda * sizeof(double), a, lda * sizeof(double),
-                            n * sizeof(double), m, cudaMemcpyDefault, st);
+    if (!rc && e == cudaSuccess) e = upload_rows(A->a, A->lda, a, lda, m, n, st);
     if (!rc && e != cudaSuccess) {
       set_error("dense upload failed: %s", cudaGetErrorString(e));
       rc = TS_ECUDA;
@@ -717,8 +768,7 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
   cudaStream_t st = (cudaStream_t)stream;
   // host copy of the row pointer for validation and planning
   std::vector<int> rp_h((size_t)m + 1);
-  TS_CUDA(cudaMemcpyAsync(rp_h.data(), indptr, (m + 1) * sizeof(int), cudaMemcpyDefault, st));
-  TS_CUDA(cudaStreamSynchronize(st));
+  TS_CUDA(d2h_pinned(rp_h.data(), indptr, (m + 1) * sizeof(int), st));
   if (rp_h[0] != 0 || rp_h[m] != nnz) TS_INVAL("CSR indptr must start at 0 and end at nnz");
   for (int64_t r = 0; r < m; ++r)
     if (rp_h[r + 1] < rp_h[r]) TS_INVAL("CSR indptr is not nondecreasing at row %lld", (long long)r);
@@ -765,8 +815,7 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       EpiIdxRange er{A->ci, rng};
       if ((rc = launch_vec(nnz, A->sms, er, wk, st))) return fail(rc);
       double hr[2];
-      cudaMemcpyAsync(hr, rng, sizeof(hr), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
+      d2h_pinned(hr, rng, sizeof(hr), st);
       if (hr[0] < 0 || hr[1] >= (double)n) {
         set_error("CSR column index out of range [0, %lld)", (long long)n);
         return fail(TS_EINVAL);
@@ -837,8 +886,7 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       return fail(TS_ECUDA);
     }
     std::vector<int> rpT_h((size_t)n + 1);
-    cudaMemcpyAsync(rpT_h.data(), A->rpT, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) {
+    if (d2h_pinned(rpT_h.data(), A->rpT, (n + 1) * sizeof(int), st) != cudaSuccess) {
       set_error("CSR transpose failed: %s", cudaGetErrorString(cudaGetLastError()));
       return fail(TS_ECUDA);
     }

@@ -23,7 +23,7 @@
 namespace ts {
 
 enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4,
-                      PLAN_CTILE = 5, PLAN_STREAM = 6, PLAN_WROW = 7 };
+                      PLAN_CTILE = 5, PLAN_STREAM = 6, PLAN_WROW = 7, PLAN_WARP_PF = 8 };
 
 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans):
@@ -211,6 +211,8 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
       k_rows_warp<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
     else if (pl.kind == PLAN_WROW)
       k_rows_wrow<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
+    else if (pl.kind == PLAN_WARP_PF)
+      k_rows_warp_pf<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
     else if (pl.kind == PLAN_STREAM) {
       static bool attr_set = false;
       if (!attr_set) {

@@ -558,6 +558,105 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const 
   body_rows_warp<Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
 }
 
+// ------------------------------------------------------- k_rows_warp_pf ----
+// k_rows_warp with software prefetch, for short rows of >= 8 entries whose x
+// gathers are scattered (C5's A^T v: 10 entries per column at random rows):
+// chunks are kWpfJ x 32 entries, and the NEXT chunk's values and indices (of
+// this group, else of the next group) are loaded before the current chunk's
+// gathers, so a warp always has matrix loads in flight.  Same products, same
+// per-row left-to-right sums without FMA as k_rows_warp: bitwise scipy.
+// tools/microbench/spmv_short.cu, C5^T-like: 33.6 us vs 41 us, but inside the
+// library on C5's A^T v 39.0 vs 37.9 us for k_rows_warp: opt-in
+// (TS_CSR_SHORT=pf).
+constexpr int kWpfJ = 6;
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp_pf(CsrRows A, const double* __restrict__ x,
+                                                                XS xs, Epi epi, Work wk) {
+  constexpr int K = Epi::K;
+  constexpr int J = kWpfJ, CH = 32 * J;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ double buf[kWarps][CH];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  xs.load();
+  ktimer_begin(epi.timer());
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t m = A.m, ngroups = (m + 31) / 32;
+  const int64_t W = (int64_t)gridDim.x * kWarps, w = (int64_t)blockIdx.x * kWarps + wid;
+  const int64_t g0 = ngroups * w / W, g1 = ngroups * (w + 1) / W;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  double* sb = buf[wid];
+  double pv[J];
+  int pc[J];
+  auto load = [&](int cs, int ge) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = cs + j * 32 + lane;
+      const bool ok = k < ge;
+      pv[j] = ok ? ld_stream(A.val + k) : 0.0;
+      pc[j] = ok ? ld_stream_i(A.ci + k) : 0;
+    }
+  };
+  auto bounds = [&](int64_t g, int* gb, int* ge) {
+    const int64_t rf = g * 32, rl = (rf + 32 < m) ? rf + 32 : m;
+    *gb = __ldg(A.rp + rf);
+    *ge = __ldg(A.rp + rl);
+  };
+  int gb = 0, ge = 0;
+  if (g0 < g1) {
+    bounds(g0, &gb, &ge);
+    load(gb, ge);
+  }
+  for (int64_t g = g0; g < g1; ++g) {
+    const int64_t r = g * 32 + lane;
+    const bool live = r < m;
+    const int kb = live ? __ldg(A.rp + r) : 0, ke = live ? __ldg(A.rp + r + 1) : 0;
+    int ngb = 0, nge = 0;
+    const bool more = g + 1 < g1;
+    if (more) bounds(g + 1, &ngb, &nge);
+    double sum = 0.0;
+    for (int cs = gb; cs < ge; cs += CH) {
+      double vv[J];
+      int cc[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        vv[j] = pv[j];
+        cc[j] = pc[j];
+      }
+      if (cs + CH < ge) load(cs + CH, ge);
+      else if (more) load(ngb, nge);
+      double xv[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) xv[j] = __ldg(x + cc[j]);
+#pragma unroll
+      for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xs(xv[j]));
+      __syncwarp();
+      const int lo = kb > cs ? kb : cs, hi = ke < cs + CH ? ke : cs + CH;
+      for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, sb[k - cs]);
+      __syncwarp();
+    }
+    if (live) epi.elem(r, sum, acc);
+    gb = ngb;
+    ge = nge;
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+  }
+  finish_last(epi, wk, nullptr, (int)gridDim.x, sm, &sflag);
+}
+
 // ----------------------------------------------------------- k_rows_wrow ----
 // Long, near-uniform CSR rows (C5's A v: 10^4 rows of ~1000 entries gathering
 // x at random from 8 MB): one warp per row, lanes striding the row 32 entries

@@ -47,11 +47,17 @@ class DeviceMatrix:
     Safe to share across threads and concurrent solves (linalg.py:10-13).
     """
 
-    def __init__(self, a, device: int = 0):
+    def __init__(self, a, device: int = 0, stream=None):
+        """``stream``: a torch CUDA stream or a raw ``cudaStream_t`` for the
+        upload and the device-side preparation (transpose, plans, Frobenius
+        norm); the handle is ready when the constructor returns.  A
+        non-blocking stream lets a new matrix upload while solves on other
+        streams run (double-buffered pipelines of same-shaped problems)."""
         lib = N.lib()
         self.device = int(device)
         self._handle = C.c_void_p()
-        stream = None
+        if stream is not None and not isinstance(stream, int):
+            stream = int(stream.cuda_stream)
         if isinstance(a, DeviceMatrix):
             raise TypeError("already a DeviceMatrix")
         if sparse.issparse(a):

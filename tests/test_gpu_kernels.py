@@ -171,3 +171,27 @@ def test_pinned_results_are_recycled():
     b = a @ rng.standard_normal(80)
     r = ts.solve_adaptive(a, b, eps=1e-6 * np.linalg.norm(b), max_iters=200)
     assert np.linalg.norm(a @ r.x - b) == pytest.approx(r.residual_norm, rel=1e-9, abs=1e-12)
+
+
+def test_prefetching_warp_kernel_bitwise_scipy():
+    """The prefetching short-row kernel (k_rows_warp_pf, opt-in
+    TS_CSR_SHORT=pf) on HBM-sized rows of >= 8 entries (C5's A^T v shape):
+    bitwise scipy in both orientations, incl. empty rows and rows spanning
+    several prefetch chunks."""
+    import paper_2304_12168_b200 as ts
+
+    a = _ragged(300_000, 20_000, seed=21, max_row=24, empty_frac=0.05,
+                long_rows=((5, 700), (299_999, 400), (150_000, 193)))
+    assert a.nnz >= (1 << 21) and a.nnz >= 8 * a.shape[0]
+    os.environ["TS_CSR_SHORT"] = "pf"
+    try:
+        dm = ts.DeviceMatrix(a)
+        lp = sparse.random_array((2000, 400_000), density=0.005, random_state=22, format="csr")
+        dm2 = ts.DeviceMatrix(lp)
+    finally:
+        del os.environ["TS_CSR_SHORT"]
+    rng = np.random.default_rng(8)
+    v = rng.standard_normal(a.shape[1])
+    assert np.array_equal(dm.matvec(v), a @ v)
+    w = rng.standard_normal(lp.shape[0])
+    assert np.array_equal(dm2.rmatvec(w), w @ lp)
