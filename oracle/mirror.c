@@ -14,7 +14,7 @@
  *
  * Device code it restates (paper_2304_12168_b200/csrc/):
  *   k_cols_tile<Epi,2>          ts_passes.cuh  dense A^T v (512-column tiles)
- *   k_rows_tile, k_tile_combine ts_passes.cuh  dense A v
+ *   k_rows_tile_fused           ts_passes.cuh  dense A v
  *   k_vec                       ts_passes.cuh  fused vector passes
  *   block_reduce, warp_reduce,  ts_common.cuh  fixed-order reductions
  *   reduce_partials
@@ -295,85 +295,70 @@ static void pass_T(Dev* D, const double* x, double xs, int use_xs, const Ops* op
   reduce_partials(D->bacc, D->facc, P, ops, red);
 }
 
-/* k_rows_tile + k_tile_combine: y = A x (x on the n side, optional scale) */
+/* k_rows_tile_fused: y = A x (x on the n side, optional scale).  The
+ * (row, tile) partials do not depend on which block computes them; the
+ * combine runs per 256-row group: one thread per row sums its tile partials
+ * in tile order, the group's block_reduce lands in slot g, and the slots are
+ * reduced in group order. */
 static void pass_N(Dev* D, const double* x, double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx,
                    double* red) {
   const int64_t m = D->g.m, n = D->g.n, lda = D->lda;
-  const int64_t nct = (n + TW - 1) / TW, U = nct * m;
-  const int P = D->P_n;
-  for (int b = 0; b < P; ++b) {
-    const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
-    for (int64_t u = U0; u < U1;) {
-      const int64_t ct = u / m, r0 = u - ct * m;
-      const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
-      const int64_t cb = ct * TW;
-      const int full = cb + TW <= n;
-      double xv[32][8][2];
-      for (int l = 0; l < 32; ++l)
-        for (int k = 0; k < 8; ++k) {
-          const int64_t c = cb + 64 * k + 2 * l;
-          xv[l][k][0] = (c < n) ? (use_xs ? xs * x[c] : x[c]) : 0.0;
-          xv[l][k][1] = (c + 1 < n) ? (use_xs ? xs * x[c + 1] : x[c + 1]) : 0.0;
-        }
-      for (int64_t r = r0; r < r1; ++r) { /* warps take rows r0+wid, +8, ...: any order */
-        const double* row = D->a + r * lda + cb;
-        double lane[32];
-        for (int l = 0; l < 32; ++l) {
-          double a0 = 0.0, a1 = 0.0;
-          if (full) {
-            for (int k = 0; k < 8; k += 2) {
-              a0 = fma(row[64 * k + 2 * l], xv[l][k][0], a0);
-              a0 = fma(row[64 * k + 2 * l + 1], xv[l][k][1], a0);
-              a1 = fma(row[64 * (k + 1) + 2 * l], xv[l][k + 1][0], a1);
-              a1 = fma(row[64 * (k + 1) + 2 * l + 1], xv[l][k + 1][1], a1);
-            }
-          } else {
-            for (int k = 0; k < 8; ++k) {
-              const int64_t c = cb + 64 * k + 2 * l;
-              if (c < n) a0 = fma(row[64 * k + 2 * l], xv[l][k][0], a0);
-              if (c + 1 < n) a1 = fma(row[64 * k + 2 * l + 1], xv[l][k][1], a1);
-            }
-          }
-          lane[l] = a0 + a1;
-        }
-        D->part[r * nct + ct] = warp_reduce(lane, RED_SUM);
+  const int64_t nct = (n + TW - 1) / TW;
+  for (int64_t ct = 0; ct < nct; ++ct) {
+    const int64_t cb = ct * TW;
+    const int full = cb + TW <= n;
+    double xv[32][8][2];
+    for (int l = 0; l < 32; ++l)
+      for (int k = 0; k < 8; ++k) {
+        const int64_t c = cb + 64 * k + 2 * l;
+        xv[l][k][0] = (c < n) ? (use_xs ? xs * x[c] : x[c]) : 0.0;
+        xv[l][k][1] = (c + 1 < n) ? (use_xs ? xs * x[c + 1] : x[c + 1]) : 0.0;
       }
-      u += r1 - r0;
+    for (int64_t r = 0; r < m; ++r) {
+      const double* row = D->a + r * lda + cb;
+      double lane[32];
+      for (int l = 0; l < 32; ++l) {
+        double a0 = 0.0, a1 = 0.0;
+        if (full) {
+          for (int k = 0; k < 8; k += 2) {
+            a0 = fma(row[64 * k + 2 * l], xv[l][k][0], a0);
+            a0 = fma(row[64 * k + 2 * l + 1], xv[l][k][1], a0);
+            a1 = fma(row[64 * (k + 1) + 2 * l], xv[l][k + 1][0], a1);
+            a1 = fma(row[64 * (k + 1) + 2 * l + 1], xv[l][k + 1][1], a1);
+          }
+        } else {
+          for (int k = 0; k < 8; ++k) {
+            const int64_t c = cb + 64 * k + 2 * l;
+            if (c < n) a0 = fma(row[64 * k + 2 * l], xv[l][k][0], a0);
+            if (c + 1 < n) a1 = fma(row[64 * k + 2 * l + 1], xv[l][k][1], a1);
+          }
+        }
+        lane[l] = a0 + a1;
+      }
+      D->part[r * nct + ct] = warp_reduce(lane, RED_SUM);
     }
   }
-  /* k_tile_combine: warp per row, lane 0 carries the epilogue sums */
-  const int Pc = D->P_c;
-  const int64_t W = (int64_t)Pc * WARPS;
   const int K = ops->K;
-  for (int b = 0; b < Pc; ++b) {
-    double wacc[WARPS][KMAX];
-    for (int w = 0; w < WARPS; ++w) {
+  const int64_t ng = (m + NT - 1) / NT;
+  double* gacc = (double*)malloc(sizeof(double) * (size_t)ng * KMAX);
+  for (int64_t g = 0; g < ng; ++g) {
+    double tv[KMAX][NT];
+    for (int t = 0; t < NT; ++t) {
       double acc[KMAX];
       for (int k = 0; k < K; ++k) acc[k] = red_identity(ops->op[k]);
-      for (int64_t r = (int64_t)b * WARPS + w; r < m; r += W) {
+      const int64_t r = g * NT + t;
+      if (r < m) {
         const double* pr = D->part + r * nct;
-        double lane[32];
-        for (int l = 0; l < 32; ++l) {
-          double y0 = 0.0, y1 = 0.0;
-          int64_t t = l;
-          for (; t + 32 < nct; t += 64) {
-            y0 += pr[t];
-            y1 += pr[t + 32];
-          }
-          if (t < nct) y0 += pr[t];
-          lane[l] = y0 + y1;
-        }
-        elem(ctx, r, warp_reduce(lane, RED_SUM), acc);
+        double y = pr[0];
+        for (int64_t c = 1; c < nct; ++c) y += pr[c];
+        elem(ctx, r, y, acc);
       }
-      for (int k = 0; k < K; ++k) wacc[w][k] = acc[k];
+      for (int k = 0; k < K; ++k) tv[k][t] = acc[k];
     }
-    for (int k = 0; k < K; ++k) {
-      double v = wacc[0][k];
-      for (int j = 1; j < WARPS; ++j) v = red_combine(ops->op[k], v, wacc[j][k]);
-      D->bacc[(size_t)b * KMAX + k] = v;
-    }
+    for (int k = 0; k < K; ++k) gacc[g * KMAX + k] = block_reduce1(tv[k], ops->op[k]);
   }
-  reduce_partials(D->bacc, NULL, Pc, ops, red);
+  reduce_partials(gacc, NULL, (int)ng, ops, red);
+  free(gacc);
 }
 
 /* k_vec: elem(ctx, i, 0, acc) over [0, len) */

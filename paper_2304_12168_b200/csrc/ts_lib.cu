@@ -735,13 +735,9 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
       if (A->planN.kind == PLAN_FLAT && !(fe && !strcmp(fe, "flat"))) {
         A->planN.kind = PLAN_TILE;
         A->planN.P = tile_grid(m, n, A->sms, 2, kTileNBlocks);
-        // TS_DENSE_N=fused: one-kernel A v (k_rows_tile_fused; opt-in: C2 A v
-        // 199 us vs 136 us split, because tile-major units complete every row
-        // group in the last few blocks, which then combine them serially)
-        const int64_t nct = (n + 2 * kNT - 1) / (2 * kNT);
-        const int64_t rows_pb = nct * m / A->planN.P + 1;
-        const int64_t max_groups = rows_pb / kGroupRows + 2 * std::min<int64_t>(nct, rows_pb) + 2;
-        A->planN.fused = (fe && !strcmp(fe, "fused")) && max_groups <= kMaxGroupsPerBlock;
+        // one-kernel A v (k_rows_tile_fused); TS_DENSE_N=split keeps the tile +
+        // combine kernels
+        A->planN.fused = !(fe && !strcmp(fe, "split"));
       }
     }
     if (!rc) rc = finish_create(A, st, ar);

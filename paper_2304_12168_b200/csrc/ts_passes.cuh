@@ -1387,19 +1387,19 @@ __global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile(DenseRows A, co
 }
 
 // ------------------------------------------------------ k_rows_tile_fused ----
-// Dense A v in ONE kernel: the tile pass above, then the per-row combine of
-// the tile partials done by whichever block completes a 32-row group.  Every
-// block counts the rows it finished per group (one atomic per group touched,
-// after a fence); the block whose count completes a group (all tiles of its
-// rows present) sums those rows' partials exactly as k_tile_combine does (warp
-// per row, lane-strided over tiles, xor tree) and runs the epilogue, leaving
-// the group's reduction slots in gacc[group]; the last block to arrive reduces
-// gacc in group order.  Work::npart holds [tiles x m partials | gacc | group
-// counters], zeroed once and self-resetting.  Opt-in (TS_DENSE_N=fused): the
-// (tile, row) units are tile-major, so every group completes in the blocks of
-// the last tile, which combine them one after another (C2: 199 us vs 136 us
-// for the tile + combine kernels); kept for the record and for study.
-constexpr int kGroupRows = 32;
+// Dense A v in ONE kernel.  The (tile, row) units are ordered group-major:
+// 256-row groups one after another, inside a group tile by tile, so a group's
+// 512-column tiles are produced by consecutive blocks and groups complete
+// progressively while the rest of the matrix streams.  Each block, after a
+// segment (one tile of rows of one group), adds the rows it finished to the
+// group's counter; the block that completes a group combines it at once: one
+// thread per row sums the row's tile partials in tile order, runs the
+// epilogue, and the block's reduction lands in the group's slot gacc[g]; the
+// last block to arrive reduces the slots in group order.  Only the last
+// group's combine is left on the tail, instead of a second kernel (C2:
+// k_rows_tile + k_tile_combine 137 us).  Work::npart = [m x tiles partials |
+// gacc | group counters] (zeroed once, self-resetting).
+constexpr int kGroupRows = kNT;  // rows per combine group: one per thread
 constexpr int kMaxGroupsPerBlock = 256;
 
 __host__ __device__ inline int64_t tile_groups(int64_t m) { return (m + kGroupRows - 1) / kGroupRows; }
@@ -1408,101 +1408,117 @@ template <class Epi>
 __global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile_fused(DenseRows A, const double* __restrict__ x,
                                                                      XS xs, Epi epi, Work wk) {
   constexpr int K = Epi::K;
+  constexpr int TW = 2 * kNT;
+  constexpr int R = kTileNRows;
   __shared__ double sm[kWarps * kKMax];
-  __shared__ double wacc[kWarps][kKMax];
-  __shared__ int glist[kMaxGroupsPerBlock];
-  __shared__ unsigned gadd[kMaxGroupsPerBlock];
-  __shared__ int gcount, gdone;
-  __shared__ int sflag;
+  __shared__ __align__(16) double xsl[TW];
+  __shared__ int sdone, sflag;
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
+  xs.load();
+  ktimer_begin(epi.timer());
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
   const int64_t P = gridDim.x, b = blockIdx.x;
-  const int64_t m = A.m, nct = (A.n + 2 * kNT - 1) / (2 * kNT);
+  const int64_t m = A.m, n = A.n, lda = A.lda, nct = (n + TW - 1) / TW;
+  const int64_t ng = tile_groups(m), GU = nct * kGroupRows;
   const int64_t U = nct * m, U0 = U * b / P, U1 = U * (b + 1) / P;
   double* part = wk.npart;
   double* gacc = part + nct * m;
-  unsigned* gcnt = reinterpret_cast<unsigned*>(gacc + tile_groups(m) * kKMax);
-  body_rows_tile<Epi, false, kTileNRows>(A, x, xs, epi, part, b, P);
-  __threadfence();  // this thread's partial stores before the group arrivals
-  __syncthreads();
-  if (threadIdx.x == 0) {  // (group, rows finished) pairs of this block; no atomics yet
-    int c = 0;
-    for (int64_t u = U0; u < U1;) {
-      const int64_t ct = u / m, r0 = u - ct * m;
-      const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
-      for (int64_t g = r0 / kGroupRows; g * kGroupRows < r1; ++g) {
-        const int64_t gb = g * kGroupRows, ge = (gb + kGroupRows < m) ? gb + kGroupRows : m;
-        glist[c] = (int)g;
-        gadd[c] = (unsigned)(((r1 < ge) ? r1 : ge) - ((r0 > gb) ? r0 : gb));
-        ++c;
-      }
-      u += r1 - r0;
-    }
-    gcount = c;
-    gdone = 0;
-  }
-  __syncthreads();
-  {  // arrivals in parallel, one thread per (group, count); keep the completed groups
-    const int c = gcount;
-    bool complete = false;
-    int g = -1;
-    if ((int)threadIdx.x < c) {
-      __threadfence();
-      g = glist[threadIdx.x];
-      const int64_t gb = (int64_t)g * kGroupRows, ge = (gb + kGroupRows < m) ? gb + kGroupRows : m;
-      const unsigned total = (unsigned)(nct * (ge - gb));
-      const unsigned add = gadd[threadIdx.x];
-      complete = atomicAdd(gcnt + g, add) + add == total;
-    }
-    __syncthreads();
-    if (complete) glist[atomicAdd(&gdone, 1)] = g;  // order irrelevant: slots are per group
-    __syncthreads();
-    if (threadIdx.x == 0) gcount = gdone;
-  }
-  __syncthreads();
+  unsigned* gcnt = reinterpret_cast<unsigned*>(gacc + ng * kKMax);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int ng = gcount;
-  if (ng > 0) __threadfence();  // acquire the other blocks' partials
-  for (int q = 0; q < ng; ++q) {
-    const int64_t g = glist[q];
-    const int64_t gb = g * kGroupRows, ge = (gb + kGroupRows < m) ? gb + kGroupRows : m;
-    double acc[K];
+  auto dot = [&](const double2 (&v)[8]) -> double {
+    double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-    for (int64_t r = gb + wid; r < ge; r += kWarps) {
-      const double* pr = part + r * nct;
-      double y0 = 0.0, y1 = 0.0;
-      int64_t t = lane;
-      for (; t + 32 < nct; t += 64) {
-        y0 += __ldcg(pr + t);
-        y1 += __ldcg(pr + t + 32);
+    for (int k = 0; k < 8; k += 2) {
+      const double2 x0 = *reinterpret_cast<const double2*>(xsl + 64 * k + 2 * lane);
+      const double2 x1 = *reinterpret_cast<const double2*>(xsl + 64 * (k + 1) + 2 * lane);
+      a0 = fma(v[k].x, x0.x, a0); a0 = fma(v[k].y, x0.y, a0);
+      a1 = fma(v[k + 1].x, x1.x, a1); a1 = fma(v[k + 1].y, x1.y, a1);
+    }
+    return warp_reduce(a0 + a1, RED_SUM);
+  };
+  for (int64_t u = U0; u < U1;) {
+    const int64_t g = (u / GU < ng - 1) ? u / GU : ng - 1;
+    const int64_t gb = g * kGroupRows, rows_g = (m - gb < kGroupRows) ? m - gb : kGroupRows;
+    const int64_t off = u - g * GU, ct = off / rows_g, rr = off - ct * rows_g;
+    const int64_t seg = (rows_g - rr < U1 - u) ? rows_g - rr : U1 - u;
+    const int64_t r0 = gb + rr, r1 = r0 + seg, cb = ct * TW;
+    const bool full = cb + TW <= n;
+    __syncthreads();  // previous slice consumed
+    for (int k = threadIdx.x; k < TW; k += kNT) xsl[k] = (cb + k < n) ? xs(__ldg(x + cb + k)) : 0.0;
+    __syncthreads();
+    int64_t r = r0 + wid;
+    if (full) {
+      for (; r + 8 * (R - 1) < r1; r += 8 * R) {
+        double2 v[R][8];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[q][k] = ld_stream2(A.a + (r + 8 * q) * lda + cb + 2 * lane + 64 * k);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const double sum = dot(v[q]);
+          if (lane == 0) part[(r + 8 * q) * nct + ct] = sum;
+        }
       }
-      if (t < nct) y0 += __ldcg(pr + t);
-      const double y = warp_reduce(y0 + y1, RED_SUM);
-      if (lane == 0) epi.elem(r, y, acc);
-    }
-    if (lane == 0) {
+      for (; r < r1; r += 8) {
+        double2 v[8];
 #pragma unroll
-      for (int k = 0; k < K; ++k) wacc[wid][k] = acc[k];
+        for (int k = 0; k < 8; ++k) v[k] = ld_stream2(A.a + r * lda + cb + 2 * lane + 64 * k);
+        const double sum = dot(v);
+        if (lane == 0) part[r * nct + ct] = sum;
+      }
+    } else {
+      for (; r < r1; r += 8) {
+        const double* row = A.a + r * lda + cb + 2 * lane;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t c = cb + 64 * k + 2 * lane;
+          if (c < n) a0 = fma(ld_stream(row + 64 * k), xsl[64 * k + 2 * lane], a0);
+          if (c + 1 < n) a1 = fma(ld_stream(row + 64 * k + 1), xsl[64 * k + 2 * lane + 1], a1);
+        }
+        const double sum = warp_reduce(a0 + a1, RED_SUM);
+        if (lane == 0) part[r * nct + ct] = sum;
+      }
     }
+    // the rows of this segment are in: count them for group g
+    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        double v = wacc[0][k];
-        for (int j = 1; j < kWarps; ++j) v = red_combine(epi.op(k), v, wacc[j][k]);
-        gacc[g * kKMax + k] = v;
-      }
-      gcnt[g] = 0u;  // self-reset for the next launch
+      __threadfence();
+      const unsigned add = (unsigned)seg;
+      sdone = (atomicAdd(gcnt + g, add) + add == (unsigned)(nct * rows_g)) ? 1 : 0;
     }
     __syncthreads();
+    if (sdone) {  // this block completed group g: combine it (thread per row, tiles in order)
+      __threadfence();
+      double acc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+      const int64_t row = gb + threadIdx.x;
+      if (threadIdx.x < rows_g) {
+        const double* pr = part + row * nct;
+        double y = __ldcg(pr);
+        for (int64_t t = 1; t < nct; ++t) y += __ldcg(pr + t);
+        epi.elem(row, y, acc);
+      }
+      block_reduce<K>(acc, sm, epi);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) gacc[g * kKMax + k] = acc[k];
+        gcnt[g] = 0u;  // self-reset for the next launch
+      }
+    }
+    u += seg;
   }
   if (arrive_last(wk.done, (unsigned)P, &sflag)) {
     double red[K];
-    reduce_partials<K>(gacc, nullptr, (int)tile_groups(m), red, sm, epi);
+    reduce_partials<K>(gacc, nullptr, (int)ng, red, sm, epi);
     if (threadIdx.x == 0) {
       ktimer_end(epi.timer());
       epi.finish(red);
