@@ -40,8 +40,12 @@ def ta_dense(a, b, eps, max_iters, sms=148):
     """Run the mirrored device TA (solve_adaptive, x0 = None) on a dense
     matrix.  Returns dict(x, status, iterations, residual_norm,
     normal_residual_norm, rho, x_norm, trace) with trace rows
-    (iter, tag, rho, gap_norm, c_norm)."""
+    (iter, tag, rho, gap_norm, c_norm).  Mirrors the tiled dense plans, which
+    the library picks for n >= 128 and m n >= 2048 (smaller or narrower
+    matrices run thread-per-row)."""
     a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[1] < 128 or a.size < 2048:
+        raise ValueError("the mirror models the tiled dense plans (n >= 128)")
     b = np.ascontiguousarray(b, dtype=np.float64)
     m, n = a.shape
     cap = int(max_iters) + 2

@@ -44,7 +44,10 @@ def test_c1_ta_500_bitwise():
 
 
 @pytest.mark.parametrize("m,n,seed,its", [(333, 777, 2, 150), (1000, 129, 3, 120), (517, 200, 5, 150),
-                                          (150, 130, 7, 700)])
+                                          (150, 130, 7, 700),
+                                          # A v group edges: > 256 row groups (strided slot
+                                          # reduction), fewer rows than one group over many tiles
+                                          (70001, 130, 11, 30), (3, 5000, 13, 40)])
 def test_odd_shapes_and_revalidation_bitwise(m, n, seed, its):
     w = W.dense_gaussian(m, n, seed=seed)
     _device_vs_mirror(w.a, w.b, 1e-12 * float(np.linalg.norm(w.b)), its)
