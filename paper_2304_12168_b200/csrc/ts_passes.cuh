@@ -210,7 +210,10 @@ struct CsrRows {
   // scipy csr_matvec order: sum = 0; sum += A_ij * x_j left to right; no FMA
   template <bool kCoh = false>
   __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
-    const int k0 = __ldg(rp + r), k1 = __ldg(rp + r + 1);
+    return row_serial_k<kCoh>(__ldg(rp + r), __ldg(rp + r + 1), x, xs);
+  }
+  template <bool kCoh = false>
+  __device__ __forceinline__ double row_serial_k(int k0, int k1, const double* x, const XS& xs) const {
     double s = 0.0;
     int k = k0;
     for (; k + 4 <= k1; k += 4) {
@@ -226,8 +229,23 @@ struct CsrRows {
 #pragma unroll
       for (int u = 0; u < 4; ++u) s = __dadd_rn(s, __dmul_rn(v[u], xs(xv[u])));
     }
-    for (; k < k1; ++k)
-      s = __dadd_rn(s, __dmul_rn(ld_stream(val + k), xs(ldx<kCoh>(x + ld_stream_i(ci + k)))));
+    // the last 0-3 entries: loads batched (one index -> gather round trip,
+    // not one per entry), sums still left to right
+    const int rem = k1 - k;
+    double v[3], xv[3];
+    int j[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (u < rem) {
+        v[u] = ld_stream(val + k + u);
+        j[u] = ld_stream_i(ci + k + u);
+      }
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (u < rem) xv[u] = ldx<kCoh>(x + j[u]);
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if (u < rem) s = __dadd_rn(s, __dmul_rn(v[u], xs(xv[u])));
     return s;
   }
 };
@@ -440,9 +458,12 @@ __global__ void __launch_bounds__(kNT, kFlatBlocks) k_rows_flat(Acc A, const dou
 }
 
 // ---------------------------------------------------------- k_rows_short ----
+// kb/ke: the thread's first CSR row bounds when the kernel loaded them
+// before its state read (-1: not loaded)
 template <class Acc, class Epi, bool kP>
 __device__ __forceinline__ void body_rows_short(const Acc& A, const double* __restrict__ x, XS xs,
-                                                Epi& epi, const Work& wk, int64_t b, int64_t P) {
+                                                Epi& epi, const Work& wk, int64_t b, int64_t P,
+                                                int kb = -1, int ke = -1) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
@@ -456,8 +477,14 @@ __device__ __forceinline__ void body_rows_short(const Acc& A, const double* __re
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  for (int64_t r = R0 + threadIdx.x; r < R1; r += kNT)
-    epi.elem(r, A.template row_serial<kP>(r, x, xs), acc);
+  int64_t r = R0 + threadIdx.x;
+  if constexpr (std::is_same_v<Acc, CsrRows>) {
+    if (kb >= 0 && r < R1) {
+      epi.elem(r, A.template row_serial_k<kP>(kb, ke, x, xs), acc);
+      r += kNT;
+    }
+  }
+  for (; r < R1; r += kNT) epi.elem(r, A.template row_serial<kP>(r, x, xs), acc);
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -470,11 +497,22 @@ template <class Acc, class Epi>
 __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const double* __restrict__ x, XS xs,
                                                     Epi epi, Work wk) {
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  // L2-resident passes are a chain of dependent loads: the first row's bounds
+  // do not depend on the state word, so both are in flight together
+  int kb = -1, ke = -1;
+  if constexpr (std::is_same_v<Acc, CsrRows>) {
+    const int64_t m = A.rows(), P = gridDim.x, b = blockIdx.x;
+    const int64_t r = m * b / P + threadIdx.x;
+    if (r < m * (b + 1) / P) {
+      kb = __ldg(A.rp + r);
+      ke = __ldg(A.rp + r + 1);
+    }
+  }
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
-  body_rows_short<Acc, Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
+  body_rows_short<Acc, Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x, kb, ke);
 }
 
 // ----------------------------------------------------------- k_rows_warp ----
