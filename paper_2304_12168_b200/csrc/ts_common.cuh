@@ -217,7 +217,7 @@ struct Work {
   double* facc;     // [pmax * kKMax] split-row / split-tile epilogue partials
   double* bpart;    // [pmax * 2] block boundary row-piece sums (first, last)
   double* tpart;    // [pmax * 2 * kCW] block boundary tile pieces
-  double* npart;    // [ntiles * m] dense A v per-(tile,row) partials (k_rows_tile)
+  double* npart;    // dense A v: [ntiles * m] per-(tile,row) partials, then group slots + counters
   unsigned* cnt;    // [pmax] split counters (self-resetting)
   unsigned* done;   // [4] completion counters (self-resetting)
   int pmax;

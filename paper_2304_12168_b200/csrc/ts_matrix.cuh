@@ -29,7 +29,7 @@ enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans):
 // tile partials, then the fused A v's group slots and counters (k_rows_tile_fused)
 inline int64_t npart_elems(int64_t m, int64_t n) {
-  const int64_t g = (m + 31) / 32;
+  const int64_t g = tile_groups(m);
   return ((n + 2 * kNT - 1) / (2 * kNT)) * m + g * kKMax + (g + 1) / 2;
 }
 

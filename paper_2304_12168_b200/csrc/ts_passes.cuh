@@ -1438,7 +1438,6 @@ __global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile(DenseRows A, co
 // k_rows_tile + k_tile_combine 137 us).  Work::npart = [m x tiles partials |
 // gacc | group counters] (zeroed once, self-resetting).
 constexpr int kGroupRows = kNT;  // rows per combine group: one per thread
-constexpr int kMaxGroupsPerBlock = 256;
 
 __host__ __device__ inline int64_t tile_groups(int64_t m) { return (m + kGroupRows - 1) / kGroupRows; }
 
