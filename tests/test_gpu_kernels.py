@@ -195,3 +195,46 @@ def test_prefetching_warp_kernel_bitwise_scipy():
     assert np.array_equal(dm.matvec(v), a @ v)
     w = rng.standard_normal(lp.shape[0])
     assert np.array_equal(dm2.rmatvec(w), w @ lp)
+
+
+def test_thread_row_kernel_tails_bitwise_scipy():
+    """The thread-per-row kernel (k_rows_short, L2-sized short-row plans)
+    loads a row's last 0-3 entries as one batch and its first row's bounds
+    before the state word: rows of every length 0..11 stay bitwise scipy in
+    both orientations."""
+    import paper_2304_12168_b200 as ts
+
+    a = _ragged(50_000, 40_000, seed=31, max_row=11, empty_frac=0.08)
+    assert a.nnz < (1 << 21)
+    dm = ts.DeviceMatrix(a)
+    rng = np.random.default_rng(9)
+    v = rng.standard_normal(a.shape[1])
+    w = rng.standard_normal(a.shape[0])
+    assert np.array_equal(dm.matvec(v), a @ v)
+    assert np.array_equal(dm.rmatvec(w), w @ a)
+
+
+def test_split_dense_av_matches_fused():
+    """TS_DENSE_N=split (tile kernel + combine kernel, the persistent loop's
+    bodies) agrees with the default one-kernel dense A v to rounding: only
+    the order of the per-row sum over tile partials differs."""
+    import paper_2304_12168_b200 as ts
+
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((2300, 1700))
+    os.environ["TS_DENSE_N"] = "split"
+    try:
+        d_split = ts.DeviceMatrix(a)
+    finally:
+        del os.environ["TS_DENSE_N"]
+    d_fused = ts.DeviceMatrix(a)
+    v = rng.standard_normal(1700)
+    y1, y2, ref = d_split.matvec(v), d_fused.matvec(v), a @ v
+    scale = np.abs(a) @ np.abs(v)
+    assert np.all(np.abs(y1 - ref) <= 1e-13 * scale)
+    assert np.all(np.abs(y2 - ref) <= 1e-13 * scale)
+    b = a @ np.ones(1700)
+    opts = ts.CenteringOptions(epsilon=1e-10, max_iters=15)
+    r1, r2 = ts.centering_solve(d_split, b, opts), ts.centering_solve(d_fused, b, opts)
+    assert r1.iterations == r2.iterations
+    assert np.linalg.norm(r1.x - r2.x) <= 1e-9 * np.linalg.norm(r2.x)
