@@ -13,7 +13,8 @@
  * once only the BLAS reduction order changes.
  *
  * Device code it restates (paper_2304_12168_b200/csrc/):
- *   k_cols_tile<Epi,2>          ts_passes.cuh  dense A^T v (512-column tiles)
+ *   k_cols_tile<Epi,2>          ts_passes.cuh  dense A^T v (512-column tiles; large A)
+ *   k_rows_tile_fused on A^T    ts_passes.cuh  dense A^T v of small A (PLAN_TRANS)
  *   k_rows_tile_fused           ts_passes.cuh  dense A v
  *   k_vec                       ts_passes.cuh  fused vector passes
  *   block_reduce, warp_reduce,  ts_common.cuh  fixed-order reductions
@@ -185,6 +186,7 @@ typedef void (*ElemFn)(void* ctx, int64_t i, double y, double* acc);
 typedef struct {
   const double* a;
   int64_t lda;
+  double* aT; /* PLAN_TRANS (small matrices): n x m transposed copy, else NULL */
   Geo g;
   int P_t, P_n, P_c;
   int64_t nct;
@@ -230,8 +232,14 @@ static int64_t cols_seg(const Dev* D, const double* x, double xs, int use_xs, in
 }
 
 /* k_cols_tile<Epi, 2>: y = A^T x (x on the m side), epilogue per column */
+static void rows_pass(Dev* D, const double* a, int64_t lda, int64_t m, int64_t n, const double* x,
+                      double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx, double* red);
 static void pass_T(Dev* D, const double* x, double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx,
                    double* red) {
+  if (D->aT) { /* PLAN_TRANS: the fused row-tile pass over the transposed copy */
+    rows_pass(D, D->aT, D->g.m, D->g.n, D->g.m, x, xs, use_xs, ops, elem, ctx, red);
+    return;
+  }
   const int64_t m = D->g.m, n = D->g.n;
   const int64_t nct = (n + TW - 1) / TW, U = nct * m;
   const int P = D->P_t;
@@ -300,9 +308,8 @@ static void pass_T(Dev* D, const double* x, double xs, int use_xs, const Ops* op
  * combine runs per 256-row group: one thread per row sums its tile partials
  * in tile order, the group's block_reduce lands in slot g, and the slots are
  * reduced in group order. */
-static void pass_N(Dev* D, const double* x, double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx,
-                   double* red) {
-  const int64_t m = D->g.m, n = D->g.n, lda = D->lda;
+static void rows_pass(Dev* D, const double* a, int64_t lda, int64_t m, int64_t n, const double* x,
+                      double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx, double* red) {
   const int64_t nct = (n + TW - 1) / TW;
   for (int64_t ct = 0; ct < nct; ++ct) {
     const int64_t cb = ct * TW;
@@ -315,7 +322,7 @@ static void pass_N(Dev* D, const double* x, double xs, int use_xs, const Ops* op
         xv[l][k][1] = (c + 1 < n) ? (use_xs ? xs * x[c + 1] : x[c + 1]) : 0.0;
       }
     for (int64_t r = 0; r < m; ++r) {
-      const double* row = D->a + r * lda + cb;
+      const double* row = a + r * lda + cb;
       double lane[32];
       for (int l = 0; l < 32; ++l) {
         double a0 = 0.0, a1 = 0.0;
@@ -359,6 +366,11 @@ static void pass_N(Dev* D, const double* x, double xs, int use_xs, const Ops* op
   }
   reduce_partials(gacc, NULL, (int)ng, ops, red);
   free(gacc);
+}
+
+static void pass_N(Dev* D, const double* x, double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx,
+                   double* red) {
+  rows_pass(D, D->a, D->lda, D->g.m, D->g.n, x, xs, use_xs, ops, elem, ctx, red);
 }
 
 /* k_vec: elem(ctx, i, 0, acc) over [0, len) */
@@ -484,7 +496,14 @@ int64_t ts_mirror_ta_dense(const double* a, int64_t m, int64_t n, const double* 
   D.P_c = combine_grid(&D.g);
   D.nct = (n + TW - 1) / TW;
   const int64_t pmax = (int64_t)sms * 8 + 8;
-  D.part = (double*)calloc((size_t)(D.nct * m), sizeof(double));
+  /* the library's PLAN_TRANS rule (ts_lib.cu, kTransBytes in ts_matrix.cuh) */
+  if (m >= 128 && n >= 128 && 8 * m * n <= (32ll << 20)) {
+    D.aT = (double*)malloc(sizeof(double) * (size_t)(m * n));
+    for (int64_t r = 0; r < m; ++r)
+      for (int64_t c = 0; c < n; ++c) D.aT[c * m + r] = a[r * n + c];
+  }
+  const int64_t nctT = (m + TW - 1) / TW;
+  D.part = (double*)calloc((size_t)(D.nct * m > nctT * n ? D.nct * m : nctT * n), sizeof(double));
   D.tpart = (double*)calloc((size_t)pmax * 2 * TW, sizeof(double));
   D.bacc = (double*)calloc((size_t)pmax * KMAX, sizeof(double));
   D.facc = (double*)calloc((size_t)pmax * KMAX, sizeof(double));
@@ -577,6 +596,7 @@ int64_t ts_mirror_ta_dense(const double* a, int64_t m, int64_t n, const double* 
   out[6] = s.gap_norm;
   out[7] = s.c_norm;
   free(D.part);
+  free(D.aT);
   free(D.tpart);
   free(D.bacc);
   free(D.facc);

@@ -465,6 +465,21 @@ __global__ void k_expand_rows(const int* rp, int64_t rows, int* rowid) {
        r += (int64_t)gridDim.x * blockDim.x)
     for (int k = rp[r]; k < rp[r + 1]; ++k) rowid[k] = (int)r;
 }
+// exact transposed copy (32 x 32 tiles through shared memory)
+__global__ void k_transpose(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n,
+                            double* __restrict__ t, int64_t ldt) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int64_t r = r0 + j, c = c0 + threadIdx.x;
+    if (r < m && c < n) tile[j][threadIdx.x] = a[r * lda + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int64_t c = c0 + j, r = r0 + threadIdx.x;
+    if (r < m && c < n) t[c * ldt + r] = tile[threadIdx.x][j];
+  }
+}
 __global__ void k_iota(int* v, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -522,7 +537,7 @@ static void free_matrix(Mat* A) {
   DeviceGuard g(A->dev);
   cudaDeviceSynchronize();
   destroy_instances(A);
-  void* ps[] = {A->a,   A->rp,  A->ci,  A->val, A->rpT, A->ciT, A->valT,
+  void* ps[] = {A->a,   A->aT,  A->rp,  A->ci,  A->val, A->rpT, A->ciT, A->valT,
                 A->tval, A->tci, A->trp, A->tblk};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -636,6 +651,11 @@ int ts_matrix_info(const ts_matrix* A, int64_t* m, int64_t* n, int64_t* nnz, int
 }
 
 static int finish_create(ts_matrix* A, cudaStream_t st, Arena& ar) {
+  if (A->kind == 0 && A->aT) {  // PLAN_TRANS: the transposed copy of the new entries
+    dim3 grid((unsigned)((A->n + 31) / 32), (unsigned)((A->m + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(A->a, A->lda, A->m, A->n, A->aT, A->ldaT);
+    TS_CUDA(cudaGetLastError());
+  }
   // Frobenius norm once (linalg.py:64-69); cached on the immutable handle
   Work wk;
   TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
@@ -728,6 +748,22 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
         A->planT.kind = PLAN_TMA;
         const int per_sm = std::max(1, std::min(2, (227 * 1024 - 4096) / kTmaSmem));
         A->planT.P = std::max(1, std::min(tile_grid(m, n, A->sms, 2), A->sms * per_sm));
+      }
+      // small dense A (<= kTransBytes, L2-sized): A^T v as the fused row-tile
+      // kernel over a transposed copy (C1: 7.3 vs 9.4 us per pass: no split-
+      // tile merges); TS_DENSE_T=cols keeps the column-tile kernel
+      if (!rc && m >= 128 && n >= 128 && 8 * m * n <= kTransBytes && !(te && !strcmp(te, "cols")) &&
+          A->planT.kind == PLAN_TILE && vw == 2) {
+        A->ldaT = m >= 64 ? (m + 15) / 16 * 16 : (m + 3) / 4 * 4;
+        if (dev_malloc(&A->aT, (size_t)A->ldaT * n * sizeof(double), device) != cudaSuccess) {
+          set_error("cudaMalloc(transposed dense %lld x %lld) failed", (long long)n, (long long)m);
+          rc = TS_ENOMEM;
+        } else {
+          if (A->ldaT != m) cudaMemsetAsync(A->aT, 0, (size_t)A->ldaT * n * sizeof(double), st);
+          A->planT.kind = PLAN_TRANS;
+          A->planT.P = tile_grid(n, m, A->sms, 2, kTileNBlocks);
+          A->npart = npart_elems(m, n) + npart_elems(n, m);  // disjoint A v / A^T v layouts
+        }
       }
       // A v in the A^T v tile geometry (measured faster than the flat split on
       // C2: 137 vs 145 us); TS_DENSE_N=flat selects the flat split

@@ -23,7 +23,8 @@
 namespace ts {
 
 enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4,
-                      PLAN_CTILE = 5, PLAN_STREAM = 6, PLAN_WROW = 7, PLAN_WARP_PF = 8 };
+                      PLAN_CTILE = 5, PLAN_STREAM = 6, PLAN_WROW = 7, PLAN_WARP_PF = 8,
+                      PLAN_TRANS = 9 };
 
 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans):
@@ -56,6 +57,10 @@ struct Mat {
   // dense
   double* a = nullptr;
   int64_t lda = 0;
+  // small (L2-sized) dense A: a transposed copy, so A^T v runs as the fused
+  // row-tile A v over it (PLAN_TRANS) instead of column tiles with split merges
+  double* aT = nullptr;
+  int64_t ldaT = 0;
   // csr + transposed csr
   int *rp = nullptr, *ci = nullptr, *rpT = nullptr, *ciT = nullptr;
   double *val = nullptr, *valT = nullptr;
@@ -145,6 +150,8 @@ inline int combine_grid(int64_t m, int sms) {
 // matrices feel it: for A^T v the column pieces of a tile are merged in block
 // order by one block, and C1 runs 9.5 us per A^T v with 32 rows per block vs
 // 15.7 us with 8 (16 and 64 were worse); A v is best at 8 (7.2 vs 9.1 us).
+// dense matrices up to this size keep a transposed copy for A^T v (PLAN_TRANS)
+constexpr int64_t kTransBytes = 32ll << 20;
 constexpr int kTileMinRowsN = 8;
 constexpr int kTileMinRowsT = 32;
 inline int tile_grid(int64_t m, int64_t n, int sms, int vw, int per_sm = kMinBlocks,
@@ -180,6 +187,13 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
                                                                  M.planN.wrow);
       else
         k_rows_short<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+    } else if (M.planT.kind == PLAN_TRANS) {
+      // its partials / group slots / counters live after the A v pass's: the
+      // counters must stay zero between launches (self-resetting)
+      Work wt = wk;
+      wt.npart = wk.npart + npart_elems(M.m, M.n);
+      k_rows_tile_fused<Epi><<<M.planT.P, kNT, 0, st>>>(DenseRows{M.aT, M.ldaT, M.n, M.m, 2}, x, xs,
+                                                        epi, wt);
     } else if (M.planT.kind == PLAN_TMA) {
       static bool attr_set = false;  // per process; the attribute is per function
       if (!attr_set) {

@@ -233,6 +233,13 @@ def test_split_dense_av_matches_fused():
     scale = np.abs(a) @ np.abs(v)
     assert np.all(np.abs(y1 - ref) <= 1e-13 * scale)
     assert np.all(np.abs(y2 - ref) <= 1e-13 * scale)
+    # A^T v of this L2-sized matrix runs over a transposed copy (PLAN_TRANS)
+    # with its own partial / counter layout next to the A v pass's
+    w = rng.standard_normal(2300)
+    for dm in (d_split, d_fused):
+        for _ in range(3):  # alternate the two passes: counters stay consistent
+            assert np.all(np.abs(dm.rmatvec(w) - a.T @ w) <= 1e-13 * (np.abs(a.T) @ np.abs(w)))
+            assert np.all(np.abs(dm.matvec(v) - ref) <= 1e-13 * scale)
     b = a @ np.ones(1700)
     opts = ts.CenteringOptions(epsilon=1e-10, max_iters=15)
     r1, r2 = ts.centering_solve(d_split, b, opts), ts.centering_solve(d_fused, b, opts)

@@ -41,7 +41,9 @@ for name, iters in (("c1", 40), ("c3", 30)):
 
 
 def test_persistent_cta_loop_window_parity():
-    env = dict(os.environ, TS_PERSIST="1")
+    # the persistent loop runs dense A^T v as column tiles: keep small dense
+    # matrices off the transposed-copy plan (PLAN_TRANS) it does not cover
+    env = dict(os.environ, TS_PERSIST="1", TS_DENSE_T="cols")
     out = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
