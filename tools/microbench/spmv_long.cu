@@ -3,6 +3,8 @@
 // flight, occupancy) and a column-tiled variant whose x gathers hit shared
 // memory.  Design study behind k_rows_flat<CsrRows> / k_csr_ctile; not part
 // of the library.  Row sums are compared against the flat kernel to 1e-13.
+// k_wrow_pfn / k_wrow_ix: block-size and index-only-prefetch sweeps of the
+// library loop (profiles/round1/spmv_long_variants.txt: all within 4 %).
 //
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
 //        -o tools/microbench/spmv_long tools/microbench/spmv_long.cu
@@ -99,6 +101,95 @@ __global__ void __launch_bounds__(256, NB) k_wrow_pf(const int* __restrict__ rp,
       double xv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) xv[u] = __ldg(x + j[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u & 3] = fma(v[u], xv[u], a[u & 3]);
+    }
+    const double s = warp_reduce((a[0] + a[1]) + (a[2] + a[3]), RED_SUM);
+    if (lane == 0) y[r] = s;
+  }
+}
+
+// k_wrow_pf with the block size as a parameter (occupancy at fixed registers)
+template <int U, int NT, int NB>
+__global__ void __launch_bounds__(NT, NB) k_wrow_pfn(const int* __restrict__ rp, const int* __restrict__ ci,
+                                                    const double* __restrict__ val, int m,
+                                                    const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * NT + threadIdx.x) >> 5, W = (gridDim.x * NT) >> 5;
+  for (int r = w; r < m; r += W) {
+    const int k0 = __ldg(rp + r), k1 = __ldg(rp + r + 1);
+    double a[4] = {0, 0, 0, 0};
+    double pv[U];
+    int pj[U];
+    int k = k0 + lane;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = k + 32 * u;
+      pv[u] = kk < k1 ? ld_stream(val + kk) : 0.0;
+      pj[u] = kk < k1 ? ld_stream_i(ci + kk) : 0;
+    }
+    for (; k < k1; k += 32 * U) {
+      double v[U];
+      int j[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = pv[u];
+        j[u] = pj[u];
+      }
+      const int kn = k + 32 * U;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = kn + 32 * u;
+        pv[u] = kk < k1 ? ld_stream(val + kk) : 0.0;
+        pj[u] = kk < k1 ? ld_stream_i(ci + kk) : 0;
+      }
+      double xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = __ldg(x + j[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u & 3] = fma(v[u], xv[u], a[u & 3]);
+    }
+    const double s = warp_reduce((a[0] + a[1]) + (a[2] + a[3]), RED_SUM);
+    if (lane == 0) y[r] = s;
+  }
+}
+
+// index-only prefetch: the next chunk's column indices are loaded ahead, the
+// current chunk's values are loaded together with its x gathers (both ~L2 /
+// DRAM latency), so fewer registers per entry in flight -> more warps
+template <int U, int NT, int NB>
+__global__ void __launch_bounds__(NT, NB) k_wrow_ix(const int* __restrict__ rp, const int* __restrict__ ci,
+                                                   const double* __restrict__ val, int m,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * NT + threadIdx.x) >> 5, W = (gridDim.x * NT) >> 5;
+  for (int r = w; r < m; r += W) {
+    const int k0 = __ldg(rp + r), k1 = __ldg(rp + r + 1);
+    double a[4] = {0, 0, 0, 0};
+    int pj[U];
+    int k = k0 + lane;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = k + 32 * u;
+      pj[u] = kk < k1 ? ld_stream_i(ci + kk) : -1;
+    }
+    for (; k < k1; k += 32 * U) {
+      int j[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) j[u] = pj[u];
+      const int kn = k + 32 * U;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = kn + 32 * u;
+        pj[u] = kk < k1 ? ld_stream_i(ci + kk) : -1;
+      }
+      double v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = j[u] >= 0;
+        v[u] = ok ? ld_stream(val + k + 32 * u) : 0.0;
+        xv[u] = ok ? __ldg(x + j[u]) : 0.0;
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) a[u & 3] = fma(v[u], xv[u], a[u & 3]);
     }
@@ -370,6 +461,11 @@ int main(int argc, char** argv) {
 #define WR(U, NB) { float t = timeit([&] { k_wrow<U, NB><<<sms * NB, 256>>>(drp, dci, dval, m, x, y); }, 20); report("wrow U" #U " " #NB "blk", t, y); }
 #define WP(U, NB) { float t = timeit([&] { k_wrow_pf<U, NB><<<sms * NB, 256>>>(drp, dci, dval, m, x, y); }, 20); report("wrow_pf U" #U " " #NB "blk", t, y); }
   WR(16, 2) WR(16, 4) WR(32, 2) WP(8, 4) WP(8, 2) WP(16, 2) WP(12, 3)
+  // occupancy / register-budget variants of the library loop (k_rows_wrow = pf U6, 256 x 3)
+#define WPN(U, NT, NB) { float t = timeit([&] { k_wrow_pfn<U, NT, NB><<<sms * NB, NT>>>(drp, dci, dval, m, x, y); }, 20); report("wrow_pf U" #U " " #NT "x" #NB, t, y); }
+#define WIX(U, NT, NB) { float t = timeit([&] { k_wrow_ix<U, NT, NB><<<sms * NB, NT>>>(drp, dci, dval, m, x, y); }, 20); report("wrow_ix U" #U " " #NT "x" #NB, t, y); }
+  WPN(6, 256, 3) WPN(6, 128, 7) WPN(6, 64, 14) WPN(4, 128, 8) WPN(8, 128, 6)
+  WIX(6, 256, 3) WIX(8, 256, 3) WIX(8, 256, 4) WIX(8, 128, 8) WIX(12, 256, 3) WIX(16, 256, 2) WIX(6, 128, 8)
   {
     double *bacc, *outp;
     unsigned* done;
