@@ -304,6 +304,24 @@ TS_API int ts_matrix_create_csr_pair(const int32_t* indptr, const int32_t* indic
                                      int device, void* stream, ts_matrix** out);
 TS_API int ts_matrix_set_row_shard(ts_matrix* a, ts_comm* comm, int64_t n_global, int64_t row_offset,
                                    double frobenius_global);
+/* Row-block sharding of a tall matrix (m >> n; north_star "tall matrices are
+ * row-sharded symmetrically"): rank p owns rows [off, off + m_p) of A with
+ * all n columns (a normal matrix handle).  The mirror image of column
+ * sharding: x, x0, c and the Krylov q-vectors are replicated; b, b', r, gap
+ * and the p-vectors are the rank's row block; A v is local, A^T v sums an
+ * n-vector over ranks in rank order (fused, deterministic), every m-space
+ * reduction is summed over ranks.  Replaces the unsharded linalg.py:45-56
+ * A^T r of every solver for this layout. */
+TS_API int ts_matrix_set_tall_shard(ts_matrix* a, ts_comm* comm, int64_t m_global, int64_t row_offset,
+                                    double frobenius_global);
+/* Emulated world: `world` communicators of ONE process on one device (out
+ * receives `world` handles, rank order), for running the sharded device code
+ * at world > 1 on a single GPU.  Each rank's solves run on their own host
+ * thread; every exchange is ordered on the host between the producer and the
+ * consumer kernels instead of spinning on device flags (kernels that wait on
+ * one another must not share a GPU).  Results are bit-identical to a world of
+ * the same size across GPUs. */
+TS_API int ts_comm_create_local(int device, int world, int64_t vec_capacity, ts_comm** out);
 
 /* ---- solvers --------------------------------------------------------------- */
 TS_API int ts_cta_solve(const ts_matrix* a, const double* b, const ts_cta_options* opts, double* x_out,

@@ -25,7 +25,8 @@ EXPORTS = (
     "ts_comm_create", "ts_comm_connect", "ts_comm_destroy", "ts_matrix_set_shard",
     "ts_pool_trim", "ts_host_alloc", "ts_host_free",
     "ts_mm_parse", "ts_mm_coo", "ts_mm_dense", "ts_mm_to_device", "ts_mm_free",
-    "ts_matrix_create_csr_pair", "ts_matrix_set_row_shard",
+    "ts_matrix_create_csr_pair", "ts_matrix_set_row_shard", "ts_matrix_set_tall_shard",
+    "ts_comm_create_local",
     "ts_matrix_gen_stencil5", "ts_matrix_gen_clement",
 )
 
@@ -125,6 +126,8 @@ def _declare(lib):
         "ts_comm_destroy": ([_P], C.c_int),
         "ts_matrix_set_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
         "ts_matrix_set_row_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
+        "ts_matrix_set_tall_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
+        "ts_comm_create_local": ([C.c_int, C.c_int, _I64, _P], C.c_int),
         "ts_matrix_gen_stencil5": ([_I64, _D, _D, _D, _D, _D, _I32, C.c_int, _P, C.POINTER(_P)],
                                    C.c_int),
         "ts_matrix_gen_clement": ([_I64, C.c_int, _P, C.POINTER(_P)], C.c_int),

@@ -23,7 +23,21 @@
 // a rank can only reach the producer of epoch e+2 after every peer arrived at
 // e+1, i.e. after they finished reading epoch e's buffers.  AR grids never
 // exceed one resident wave, so block 0 (the announcer) is always running.
+//
+// Emulated worlds (ts_comm_create_local): W ranks of one process on ONE GPU,
+// each solved by its own host thread.  Kernels that spin on each other must
+// not share a GPU, so there the device barrier does not wait: every exchange
+// is ordered on the host instead (LocalGroup::exchange: each rank records an
+// event after its producer kernel, all ranks meet, each rank's stream waits
+// on every rank's event before the consumer kernel).  Everything else — the
+// symmetric slots and their epoch parity, rank-ordered sums, deferred
+// scalars, halo copies, peer reads — is the same device code as across GPUs.
 #pragma once
+
+#include <chrono>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
 
 #include "ts_state.cuh"
 
@@ -41,6 +55,41 @@ struct CommDev {
   unsigned long long* epoch = nullptr;    // local exchange counter
   double* sym = nullptr;                  // local symmetric buffer [2 * slot]
   size_t vec_cap = 0;                     // vector capacity per slot
+  int emulated = 0;                       // ranks share this GPU: exchanges are host-ordered
+};
+
+// host rendezvous of an emulated world (one process, one GPU, W host threads)
+struct LocalGroup {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool broken = false;
+  std::vector<cudaEvent_t> ev;  // per rank: its last producer kernel
+  explicit LocalGroup(int w) : world(w), ev((size_t)w, nullptr) {}
+  ~LocalGroup() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  // false: a rank did not arrive within the timeout (the world is broken)
+  bool meet() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
+    const unsigned long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
 };
 
 struct Comm {
@@ -52,6 +101,29 @@ struct Comm {
   double** psym_d = nullptr;
   unsigned long long** pflags_d = nullptr;
   std::vector<void*> opened;
+  std::shared_ptr<LocalGroup> local;  // emulated world (nullptr: one rank per GPU)
+  // emulated world: order this rank's next kernel after every rank's last one
+  int exchange(cudaStream_t s) const {
+    if (!local) return 0;
+    if (cudaEventRecord(local->ev[rank], s) != cudaSuccess) {
+      set_error("exchange: cudaEventRecord failed");
+      return TS_ECUDA;
+    }
+    if (!local->meet()) {
+      set_error("emulated world: a rank did not reach the exchange");
+      return TS_ECUDA;
+    }
+    for (int q = 0; q < world; ++q)
+      if (q != rank && cudaStreamWaitEvent(s, local->ev[q], 0) != cudaSuccess) {
+        set_error("exchange: cudaStreamWaitEvent failed");
+        return TS_ECUDA;
+      }
+    if (!local->meet()) {  // every rank queued its waits before any event is re-recorded
+      set_error("emulated world: a rank did not reach the exchange");
+      return TS_ECUDA;
+    }
+    return 0;
+  }
   CommDev dev_view() const {
     CommDev c;
     c.rank = rank;
@@ -63,6 +135,7 @@ struct Comm {
     c.epoch = epoch;
     c.sym = sym;
     c.vec_cap = vec_cap;
+    c.emulated = local ? 1 : 0;
     return c;
   }
 };
@@ -81,8 +154,13 @@ __device__ __forceinline__ double ld_peer(const double* p) {
   return v;
 }
 
-// every block: announce (block 0) and wait for all ranks at epoch e
+// every block: announce (block 0) and wait for all ranks at epoch e (an
+// emulated world is ordered by the host: nothing to wait for)
 __device__ __forceinline__ void comm_barrier(const CommDev& c, unsigned long long e) {
+  if (c.emulated) {
+    __syncthreads();
+    return;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     __threadfence_system();
     for (int q = 0; q < c.world; ++q) st_release_sys(c.pflags[q] + c.rank, e);
@@ -190,19 +268,24 @@ __global__ void __launch_bounds__(kNT) k_ar_scalars(Epi epi, CommDev c, unsigned
 // neighbour's head into the vector's halo padding (x[-hw, 0) and
 // x[n, n + hw)).  One block; a pass whose epilogue is inactive skips it on
 // every rank alike (the state is replicated), so epochs stay in step.
+// phase: 1 publish, 2 barrier + copy-in, 3 both (an emulated world launches
+// the two halves apart, with the host exchange between them).
 template <class Epi>
-__global__ void __launch_bounds__(kNT) k_halo(Epi epi, double* x, int64_t n, int64_t hw, CommDev c) {
+__global__ void __launch_bounds__(kNT) k_halo(Epi epi, double* x, int64_t n, int64_t hw, CommDev c, int phase) {
   __shared__ int live;
   if (threadIdx.x == 0) live = epi.active();
   __syncthreads();
   if (!live) return;
   const unsigned long long e = *c.epoch + 1;
   const size_t base = slot_base(c, e);
-  for (int64_t i = threadIdx.x; i < hw; i += kNT) {
-    c.sym[base + i] = x[i];                // head: the left neighbour's right halo
-    c.sym[base + hw + i] = x[n - hw + i];  // tail: the right neighbour's left halo
+  if (phase & 1) {
+    for (int64_t i = threadIdx.x; i < hw; i += kNT) {
+      c.sym[base + i] = x[i];                // head: the left neighbour's right halo
+      c.sym[base + hw + i] = x[n - hw + i];  // tail: the right neighbour's left halo
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  if (!(phase & 2)) return;
   comm_barrier(c, e);
   for (int64_t i = threadIdx.x; i < hw; i += kNT) {
     x[-hw + i] = c.rank > 0 ? ld_peer(c.psym[c.rank - 1] + base + hw + i) : 0.0;

@@ -60,8 +60,6 @@ constexpr int kKMax = 8;          // max reduction slots per pass
 constexpr int kCW = 4 * kNT;      // max dense A^T tile width (columns): up to 4 per thread
 constexpr int kTMax = 8;          // max CTA order supported on device
 constexpr int kEpiSmem = kTMax * kTMax + 16;  // per-block scratch for Epi::prepare
-constexpr int kCtTW = 8192;       // column-tiled CSR: tile width (x slice 64 KB in smem)
-constexpr int kCtBlocksPerSM = 3; // 3 x 64 KB x slices per SM
 
 enum RedOp : int { RED_SUM = 0, RED_MIN = 1 };
 
@@ -221,7 +219,6 @@ struct Work {
   unsigned* cnt;    // [pmax] split counters (self-resetting)
   unsigned* done;   // [4] completion counters (self-resetting)
   int pmax;
-  struct GridBar* gbar = nullptr;  // set inside the persistent loop (phase barrier)
 };
 
 // All threads: returns true in every thread of the last block to arrive.
@@ -258,10 +255,9 @@ __device__ __forceinline__ void reduce_partials(const double* bacc, const double
   block_reduce<K>(out, sm, ops);
 }
 
-// ------------------------------------------------ persistent-loop plumbing ----
-// Inside one cooperative persistent kernel the solver vectors are rewritten
-// between phases, so x-vector loads must not use the non-coherent read-only
-// path there: kCoh selects L2-coherent loads (the pass kernels keep __ldg).
+// ---------------------------------------------------------- vector loads ----
+// kCoh selects L2-coherent loads for vectors rewritten while a kernel runs;
+// the pass kernels read their input vector through the read-only path.
 template <bool kCoh>
 __device__ __forceinline__ double ldx(const double* p) {
   if constexpr (kCoh) return __ldcg(p);
@@ -271,62 +267,6 @@ template <bool kCoh>
 __device__ __forceinline__ double2 ldx2(const double* p) {
   if constexpr (kCoh) return __ldcg(reinterpret_cast<const double2*>(p));
   else return __ldg(reinterpret_cast<const double2*>(p));
-}
-
-// Generation barrier over the whole cooperative grid.
-struct GridBar {
-  unsigned count;  // arrivals in the current generation
-  unsigned gen;    // generation, bumped by the last arriver
-  unsigned abort;  // watchdog tripped: every waiter leaves
-  unsigned pad;
-};
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-constexpr unsigned long long kWatchdogNs = 20ull * 1000000000ull;
-
-// Thread 0: arrive; returns true in the last arriver.  *gen0 = generation
-// observed before arriving (cannot advance until this block has arrived).
-__device__ __forceinline__ bool bar_arrive(GridBar* g, unsigned nblocks, unsigned* gen0) {
-  *gen0 = *reinterpret_cast<volatile unsigned*>(&g->gen);
-  __threadfence();
-  return atomicAdd(&g->count, 1u) == nblocks - 1;
-}
-// Thread 0 of the last arriver: open the next generation.
-__device__ __forceinline__ void bar_release(GridBar* g, unsigned gen0) {
-  g->count = 0u;
-  __threadfence();
-  st_release_gpu(&g->gen, gen0 + 1u);
-}
-// Thread 0 of the others: wait for the release (bounded by the watchdog).
-__device__ __forceinline__ void bar_wait(GridBar* g, unsigned gen0) {
-  const unsigned long long t0 = globaltimer();
-  unsigned spins = 0;
-  while (ld_acquire_gpu(&g->gen) == gen0) {
-    if ((++spins & 63u) == 0u) {
-      if (*reinterpret_cast<volatile unsigned*>(&g->abort)) break;
-      if (globaltimer() - t0 > kWatchdogNs) {
-        atomicExch(&g->abort, 1u);
-        break;
-      }
-    }
-  }
-  __threadfence();
-}
-// Plain grid barrier (all threads of every block).
-__device__ __forceinline__ void grid_sync(GridBar* g) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned gen0;
-    if (bar_arrive(g, gridDim.x, &gen0)) bar_release(g, gen0);
-    else bar_wait(g, gen0);
-  }
-  __syncthreads();
 }
 
 inline int ceil_div_i(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

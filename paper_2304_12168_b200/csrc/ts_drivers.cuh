@@ -73,9 +73,17 @@ static SolveState* pinned_state() {
   return hs;
 }
 
-// count every launch we enqueue; on a column-sharded matrix, A v becomes
-// [local partial -> symmetric buffer] + [k_ar_vec with the epilogue] and A^T v
-// becomes [local pass, finisher deferred] + [k_ar_scalars]
+// Sharded passes.  Every launch we enqueue is counted.  The exchange step of
+// a pass follows its layout:
+//  * column blocks (wide A): A v = [local partial -> symmetric slot] +
+//    [k_ar_vec: rank-ordered m-vector sum + the real epilogue]; A^T v is local
+//    with its finisher deferred to k_ar_scalars;
+//  * tall row blocks: the mirror image — A^T v sums an n-vector over ranks,
+//    A v is local with its scalars summed;
+//  * square banded row blocks: k_halo brings the neighbours' edges into the
+//    input vector's padding, the pass is local, every scalar is summed.
+// In an emulated world (ranks sharing one GPU) the host orders each exchange
+// (Comm::exchange) between producer and consumer kernels.
 inline int ar_grid(int64_t len, int sms) {
   int64_t g = (len + kNT * 4 - 1) / (kNT * 4);
   const int64_t cap = (int64_t)sms * 2;
@@ -91,30 +99,47 @@ static int pass(const Mat& M, int trans, const double* x, XS xs, const Epi& e, c
   Epi e2 = e;
   if constexpr (std::is_base_of<EpiBase, Epi>::value) e2.tclass = trans ? 1 : 0;
   if (!M.comm) return launch_pass(M, trans, x, xs, e2, w, s);
-  const CommDev cd = M.comm->dev_view();
+  const Comm& C = *M.comm;
+  const CommDev cd = C.dev_view();
   ++g_launches;
   if (M.row_shard) {  // halo in, local pass, every reduction slot summed over ranks
-    g_launches += 1;
-    k_halo<Epi><<<1, kNT, 0, s>>>(e2, const_cast<double*>(x), M.m, M.halo, cd);
+    double* xm = const_cast<double*>(x);
+    if (C.local) {
+      g_launches += 2;
+      k_halo<Epi><<<1, kNT, 0, s>>>(e2, xm, M.m, M.halo, cd, 1);
+      TS_CHECK(C.exchange(s));
+      k_halo<Epi><<<1, kNT, 0, s>>>(e2, xm, M.m, M.halo, cd, 2);
+    } else {
+      g_launches += 1;
+      k_halo<Epi><<<1, kNT, 0, s>>>(e2, xm, M.m, M.halo, cd, 3);
+    }
     EpiDefer<Epi> d{e2, cd};
     TS_CHECK(launch_pass(M, trans, x, xs, d, w, s));
+    TS_CHECK(C.exchange(s));
     k_ar_scalars<Epi><<<1, kNT, 0, s>>>(e2, cd, all_slots<Epi::K>());
     TS_CUDA(cudaGetLastError());
     return 0;
   }
-  if (!trans) {
-    if (M.m > (int64_t)cd.vec_cap) TS_INVAL("communicator vector capacity too small");
+  const bool vec_sum = M.tall_shard ? trans != 0 : trans == 0;
+  if (vec_sum) {
+    const int64_t len = trans ? M.n : M.m;
+    if (len > (int64_t)cd.vec_cap) TS_INVAL("communicator vector capacity too small");
     EpiSymStore<Epi> ps{e2, cd};
-    TS_CHECK(launch_pass(M, 0, x, xs, ps, w, s));
-    k_ar_vec<Epi><<<ar_grid(M.m, M.sms), kNT, 0, s>>>(M.m, e2, w, cd);
+    TS_CHECK(launch_pass(M, trans, x, xs, ps, w, s));
+    TS_CHECK(C.exchange(s));
+    k_ar_vec<Epi><<<ar_grid(len, M.sms), kNT, 0, s>>>(len, e2, w, cd);
   } else {
     EpiDefer<Epi> d{e2, cd};
-    TS_CHECK(launch_pass(M, 1, x, xs, d, w, s));
+    TS_CHECK(launch_pass(M, trans, x, xs, d, w, s));
+    TS_CHECK(C.exchange(s));
     k_ar_scalars<Epi><<<1, kNT, 0, s>>>(e2, cd, all_slots<Epi::K>());
   }
   TS_CUDA(cudaGetLastError());
   return 0;
 }
+// vector passes: Epi::kShardMask marks the slots that reduce over n-space;
+// they are per-rank partials on column blocks, the other (m-space) slots on
+// tall row blocks, every slot on square row blocks
 template <class Epi>
 static int vecpass(const Mat& M, int64_t len, const Epi& e, const Work& w, cudaStream_t s) {
   ++g_launches;
@@ -124,12 +149,14 @@ static int vecpass(const Mat& M, int64_t len, const Epi& e, const Work& w, cudaS
     e2.tclass = 2;
     mask = Epi::kShardMask;
   }
-  if (M.comm && M.row_shard) mask = all_slots<Epi::K>();  // both vector spaces are split
+  if (M.comm && M.row_shard) mask = all_slots<Epi::K>();
+  else if (M.comm && M.tall_shard) mask = all_slots<Epi::K>() & ~mask;
   if (!M.comm || !mask) return launch_vec(len, M.sms, e2, w, s);
   const CommDev cd = M.comm->dev_view();
   ++g_launches;
   EpiDefer<Epi> d{e2, cd};
   TS_CHECK(launch_vec(len, M.sms, d, w, s));
+  TS_CHECK(M.comm->exchange(s));
   k_ar_scalars<Epi><<<1, kNT, 0, s>>>(e2, cd, mask);
   TS_CUDA(cudaGetLastError());
   return 0;
@@ -156,8 +183,6 @@ struct Instance {
   double *xs = nullptr;
   KrylovPtrs kp;
   ProbePtrs pp = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  // persistent loop barrier (lazily allocated)
-  GridBar* gbar = nullptr;
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -378,17 +403,16 @@ struct SolveCtx {
     return 0;
   }
 
-  int run(const BodyFn& body, const GraphFn& gbody,
-          const std::function<int(cudaStream_t)>& maint, const BodyFn* persist = nullptr) {
+  int run(const BodyFn& body, const GraphFn& gbody, const std::function<int(cudaStream_t)>& maint) {
     TS_CHECK(read_state());
     TS_CHECK(flush());
     static const bool no_graph = getenv("TS_NO_GRAPH") != nullptr;
+    // an emulated world's exchanges are host-ordered: one iteration per launch
+    const bool direct = no_graph || (M.comm && M.comm->local);
     while (hs->status == TS_RUNNING) {
       if (hs->maint != MAINT_NONE) {
         TS_CHECK(maint(st));
-      } else if (persist && !no_graph) {
-        TS_CHECK((*persist)(st));
-      } else if (!no_graph) {
+      } else if (!direct) {
         if (!I->exec) TS_CHECK(I->build(gbody));
         TS_CUDA(cudaGraphLaunch(I->exec, st));
       } else {
@@ -535,7 +559,7 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
   s0.max_iters = a.max_iters;
   s0.halvings_left = std::max(0, a.halvings);
   s0.a_fro = a.gram ? M.fro * M.fro : M.fro;
-  s0.m_rows = M.row_shard ? M.m_global : mo;
+  s0.m_rows = M.comm ? (a.gram ? M.n_global : M.m_global) : mo;
   s0.n_cols = M.comm ? M.n_global : no;
   TS_CHECK(c.init(s0, trace, trace_cap));
   SolveState* ds = I->ds;
@@ -713,104 +737,6 @@ static int cta_step_kernels(const Mat& M, const Instance* I, int npairs, int gra
   return vecpass(M, std::max(M.m, M.n), eu, I->wk, s);
 }
 
-// ---- persistent CTA loop (csrc/ts_persist.cuh) ------------------------------
-// TS_PERSIST=1 runs the CTA loop as one cooperative kernel where the plans
-// allow it (opt-in: measured slower than the graph path, see ts_persist.cuh).
-static int persist_mode() {
-  static const int v = [] {
-    const char* e = getenv("TS_PERSIST");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-static bool pdir_from(const Mat& M, int trans, int Pg, PDir* D) {
-  if (M.kind == 0) {
-    D->d = M.dense();
-    if (trans) {
-      if (M.planT.kind != PLAN_TILE || M.planT.vw != 2) return false;
-      D->kind = PK_COLS;
-      D->P = std::min(M.planT.P, Pg);
-    } else {
-      if (M.planN.kind != PLAN_TILE) return false;
-      D->kind = PK_TILE;
-      D->P = std::min(M.planN.P, Pg);
-      D->Pc = std::min(combine_grid(M.m, M.sms), Pg);
-      D->nct = (M.n + 2 * kNT - 1) / (2 * kNT);
-    }
-    return true;
-  }
-  const RowPlan& pl = trans ? M.planT : M.planN;
-  D->c = trans ? M.csrT() : M.csr();
-  if (pl.kind == PLAN_SHORT) D->kind = PK_SHORT;
-  else if (pl.kind == PLAN_WARP) D->kind = PK_WARP;
-  else return false;
-  D->P = std::min(pl.P, Pg);
-  return true;
-}
-
-// co-resident grid of the persistent kernel (cooperative launch requirement)
-static int persist_grid(const Mat& M) {
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cta_loop, kNT, 0) != cudaSuccess) nb = 0;
-    per_sm = std::min(nb, blocks_per_sm());
-  }
-  return per_sm * M.sms;
-}
-
-// the loop's stack frame (epilogue objects, the kernel-argument copy) must fit
-// the per-thread stack limit: size it explicitly for the cooperative launch
-static int persist_stack() {
-  static int rc = -1;
-  if (rc < 0) {
-    cudaFuncAttributes fa;
-    size_t cur = 0;
-    rc = 0;
-    if (cudaFuncGetAttributes(&fa, k_cta_loop) != cudaSuccess ||
-        cudaDeviceGetLimit(&cur, cudaLimitStackSize) != cudaSuccess) {
-      rc = 1;
-    } else if (cur < fa.localSizeBytes + 512) {
-      if (cudaDeviceSetLimit(cudaLimitStackSize, fa.localSizeBytes + 512) != cudaSuccess) rc = 1;
-    }
-  }
-  return rc;
-}
-
-static bool cta_persist_setup(const Mat& M, Instance* I, const CtaArgs& a, CtaLoop* L) {
-  const int mode = persist_mode();
-  if (mode != 1 || a.enhanced || M.comm || a.t_max > kTMax) return false;
-  const int Pg = persist_grid(M);
-  if (Pg <= 0 || persist_stack() != 0) return false;
-  PDir T, N;
-  if (a.gram && !pdir_from(M, 1, Pg, &T)) return false;
-  if (!pdir_from(M, 0, Pg, &N)) return false;
-  if (!I->gbar && I->alloc(&I->gbar, 1)) return false;
-  L->st = I->ds;
-  L->kp = I->kp;
-  L->x = I->x;
-  L->m = M.m;
-  L->n = M.n;
-  L->gram = a.gram;
-  L->T = T;
-  L->N = N;
-  L->Pm = std::min(vec_grid(M.m, M.sms), Pg);
-  L->Pmn = std::min(vec_grid(std::max(M.m, M.n), M.sms), Pg);
-  L->wk = I->wk;
-  L->wk.gbar = I->gbar;
-  return true;
-}
-
-static int cta_persist_launch(const Mat& M, Instance* I, CtaLoop& L, cudaStream_t s) {
-  ++g_launches;
-  TS_CUDA(cudaMemsetAsync(I->gbar, 0, sizeof(GridBar), s));
-  void* args[] = {&L};
-  TS_CUDA(cudaLaunchCooperativeKernel((const void*)k_cta_loop, dim3(persist_grid(M)), dim3(kNT), args,
-                                      0, s));
-  return 0;
-}
-
 static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double* x_out,
                      ts_trace_row* trace, int64_t trace_cap, ts_result* res, cudaStream_t st) {
   const int key[4] = {2, a.gram, a.t_max, a.enhanced};
@@ -833,7 +759,7 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   s0.accel_ratio = a.accel_ratio;
   s0.rcond = a.rcond;
   s0.a_fro = M.fro;
-  s0.m_rows = M.row_shard ? M.m_global : M.m;
+  s0.m_rows = M.comm ? M.m_global : M.m;
   s0.n_cols = M.comm ? M.n_global : M.n;
   s0.warm = 1;
   s0.enhanced = a.enhanced;
@@ -885,10 +811,7 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     er.st = ds; er.b = I->b; er.r = I->kp.p[0];
     return pass(M, 0, I->x, XS{}, er, wk, s);
   };
-  CtaLoop loop;
-  const bool use_persist = cta_persist_setup(M, I, a, &loop);
-  BodyFn persist = [&](cudaStream_t s) -> int { return cta_persist_launch(M, I, loop, s); };
-  TS_CHECK(c.run(body, gbody, maint, use_persist ? &persist : nullptr));
+  TS_CHECK(c.run(body, gbody, maint));
   if (!c.hs->trivial) {
     EpiFinalR efr;
     efr.st = ds; efr.b = I->b; efr.fr = I->fr;
@@ -918,9 +841,17 @@ extern "C" {
   do {                                       \
     if (!(A)) TS_INVAL("null matrix handle"); \
   } while (0)
+// the one-shot operator calls stage x into unpadded scratch and run one
+// rank's pass alone: a shard handle (halo padding, collective exchanges)
+// must go through the collective solvers instead
+#define TS_CHECK_UNSHARDED(A)                                                              \
+  do {                                                                                     \
+    if ((A)->comm) TS_INVAL("operator calls are not supported on a sharded matrix handle"); \
+  } while (0)
 
 int ts_matvec(const ts_matrix* A, const double* x, double* y, void* stream) {
   TS_CHECK_HANDLE(A);
+  TS_CHECK_UNSHARDED(A);
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
   {
@@ -941,6 +872,7 @@ int ts_matvec(const ts_matrix* A, const double* x, double* y, void* stream) {
 
 int ts_rmatvec(const ts_matrix* A, const double* x, double* y, void* stream) {
   TS_CHECK_HANDLE(A);
+  TS_CHECK_UNSHARDED(A);
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
   {
@@ -961,6 +893,7 @@ int ts_rmatvec(const ts_matrix* A, const double* x, double* y, void* stream) {
 
 int ts_gram_matvec(const ts_matrix* A, const double* x, double* y, void* stream) {
   TS_CHECK_HANDLE(A);
+  TS_CHECK_UNSHARDED(A);
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
   {
@@ -1227,6 +1160,63 @@ int ts_comm_create(int device, int rank, int world, int64_t vec_capacity, ts_com
   return 0;
 }
 
+// An emulated world: `world` ranks of this process on one device, each with
+// its own symmetric slots, flags and epoch; peers are plain device pointers
+// and every exchange is ordered on the host (LocalGroup, csrc/ts_comm.cuh).
+// Each rank's solves must run on their own host thread.
+int ts_comm_create_local(int device, int world, int64_t vec_capacity, ts_comm** out) {
+  if (!out) TS_INVAL("null argument");
+  if (world < 1 || world > kMaxRanks) TS_INVAL("world %d outside 1..%d", world, kMaxRanks);
+  if (vec_capacity < 1) TS_INVAL("vector capacity must be positive");
+  DeviceGuard g(device);
+  auto grp = std::make_shared<LocalGroup>(world);
+  std::vector<Comm*> cs;
+  auto fail = [&](const char* what, cudaError_t e) {
+    set_error("%s failed: %s", what, cudaGetErrorString(e));
+    for (Comm* c : cs) {
+      for (void* p : {(void*)c->sym, (void*)c->flags, (void*)c->epoch, (void*)c->psym_d, (void*)c->pflags_d})
+        if (p) cudaFree(p);
+      delete c;
+    }
+    return TS_ECUDA;
+  };
+  const size_t slot = (size_t)vec_capacity + kArScalars;
+  cudaError_t e;
+  for (int r = 0; r < world; ++r) {
+    Comm* c = new Comm();
+    cs.push_back(c);
+    c->dev = device;
+    c->rank = r;
+    c->world = world;
+    c->vec_cap = (size_t)vec_capacity;
+    c->local = grp;
+    if ((e = cudaMalloc(&c->sym, 2 * slot * sizeof(double))) != cudaSuccess) return fail("cudaMalloc(sym)", e);
+    if ((e = cudaMalloc(&c->flags, 256)) != cudaSuccess) return fail("cudaMalloc(flags)", e);
+    if ((e = cudaMalloc(&c->epoch, sizeof(unsigned long long))) != cudaSuccess) return fail("cudaMalloc(epoch)", e);
+    cudaMemset(c->sym, 0, 2 * slot * sizeof(double));
+    cudaMemset(c->flags, 0, 256);
+    cudaMemset(c->epoch, 0, sizeof(unsigned long long));
+    if ((e = cudaEventCreateWithFlags(&grp->ev[r], cudaEventDisableTiming)) != cudaSuccess)
+      return fail("cudaEventCreate", e);
+  }
+  std::vector<double*> psym(world);
+  std::vector<unsigned long long*> pflags(world);
+  for (int r = 0; r < world; ++r) {
+    psym[r] = cs[r]->sym;
+    pflags[r] = cs[r]->flags;
+  }
+  for (Comm* c : cs) {
+    if ((e = cudaMalloc(&c->psym_d, world * sizeof(double*))) != cudaSuccess) return fail("cudaMalloc", e);
+    if ((e = cudaMalloc(&c->pflags_d, world * sizeof(unsigned long long*))) != cudaSuccess)
+      return fail("cudaMalloc", e);
+    cudaMemcpy(c->psym_d, psym.data(), world * sizeof(double*), cudaMemcpyHostToDevice);
+    cudaMemcpy(c->pflags_d, pflags.data(), world * sizeof(unsigned long long*), cudaMemcpyHostToDevice);
+  }
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("comm init", e);
+  for (int r = 0; r < world; ++r) out[r] = reinterpret_cast<ts_comm*>(cs[r]);
+  return 0;
+}
+
 int ts_comm_connect(ts_comm* h, const void* all_handles) {
   Comm* c = reinterpret_cast<Comm*>(h);
   if (!c || !all_handles) TS_INVAL("null argument");
@@ -1283,9 +1273,35 @@ int ts_matrix_set_shard(ts_matrix* A, ts_comm* h, int64_t n_global, int64_t col_
   destroy_instances(A);  // instances bake the (un)sharded kernel sequence
   A->comm = c;
   A->n_global = c ? n_global : A->n;
+  A->m_global = A->m;
   A->col_off = c ? col_offset : 0;
+  A->row_off = 0;
   A->row_shard = 0;
+  A->tall_shard = 0;
   if (c) A->fro = fro_global;
+  return 0;
+}
+
+int ts_matrix_set_tall_shard(ts_matrix* A, ts_comm* h, int64_t m_global, int64_t row_offset,
+                             double fro_global) {
+  TS_CHECK_HANDLE(A);
+  Comm* c = reinterpret_cast<Comm*>(h);
+  if (!c) TS_INVAL("row sharding needs a communicator");
+  if (c->dev != A->dev) TS_INVAL("communicator and matrix live on different devices");
+  if (A->halo) TS_INVAL("a halo (banded) row block takes ts_matrix_set_row_shard");
+  if (row_offset < 0 || row_offset + A->m > m_global)
+    TS_INVAL("shard rows [%lld, %lld) outside 0..%lld", (long long)row_offset,
+             (long long)(row_offset + A->m), (long long)m_global);
+  if (A->n > (int64_t)c->vec_cap) TS_INVAL("communicator vector capacity below n");
+  destroy_instances(A);
+  A->comm = c;
+  A->tall_shard = 1;
+  A->row_shard = 0;
+  A->m_global = m_global;
+  A->n_global = A->n;
+  A->row_off = row_offset;
+  A->col_off = 0;
+  A->fro = fro_global;
   return 0;
 }
 
@@ -1305,6 +1321,7 @@ int ts_matrix_set_row_shard(ts_matrix* A, ts_comm* h, int64_t n_global, int64_t 
   destroy_instances(A);
   A->comm = c;
   A->row_shard = 1;
+  A->tall_shard = 0;
   A->n_global = n_global;
   A->m_global = n_global;
   A->row_off = row_offset;

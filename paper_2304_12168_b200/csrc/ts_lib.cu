@@ -15,7 +15,6 @@
 
 #include "ts_cta.cuh"
 #include "ts_comm.cuh"
-#include "ts_persist.cuh"
 #include "ts_mmio.cuh"
 
 namespace ts {
@@ -133,12 +132,13 @@ static cudaError_t dev_malloc(T** p, size_t bytes, int dev) {
 }
 
 static void free_plan(RowPlan& p) {
-  if (p.wrow) cudaFree(p.wrow);
-  if (p.chunks) cudaFree(p.chunks);
-  if (p.blk) cudaFree(p.blk);
+  for (void* q : {(void*)p.wrow, (void*)p.sell_sp, (void*)p.sell_ci, (void*)p.sell_val})
+    if (q) cudaFree(q);
   p.wrow = nullptr;
-  p.chunks = nullptr;
-  p.blk = nullptr;
+  p.sell_sp = nullptr;
+  p.sell_ci = nullptr;
+  p.sell_val = nullptr;
+  p.sell_slots = 0;
 }
 
 // Dense upload: one linear copy when both sides are contiguous, else row slabs
@@ -163,18 +163,19 @@ static cudaError_t upload_rows(double* dst, int64_t dld, const double* src, int6
 
 // a new plan replaces `old` in place when the geometry is unchanged (cached
 // graphs bake the grid and the plan-table pointer); false: geometry changed
-static bool adopt_plan(RowPlan& old, RowPlan& nw, cudaStream_t st) {
-  const bool same = old.kind == nw.kind && old.P == nw.P && old.vw == nw.vw &&
-                    old.nchunks == nw.nchunks && (old.wrow != nullptr) == (nw.wrow != nullptr) &&
-                    (old.chunks != nullptr) == (nw.chunks != nullptr);
+static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st) {
+  const bool same = old.kind == nw.kind && old.P == nw.P && (old.wrow != nullptr) == (nw.wrow != nullptr) &&
+                    old.sell_slots == nw.sell_slots && (old.sell_sp != nullptr) == (nw.sell_sp != nullptr);
   if (same) {
     if (nw.wrow)
       cudaMemcpyAsync(old.wrow, nw.wrow, (size_t)nw.P * kWarps * sizeof(int),
                       cudaMemcpyDeviceToDevice, st);
-    if (nw.chunks) {
-      cudaMemcpyAsync(old.chunks, nw.chunks, (size_t)(nw.nchunks + 1) * sizeof(int2),
+    if (nw.sell_sp) {
+      cudaMemcpyAsync(old.sell_sp, nw.sell_sp, (size_t)((rows + 31) / 32 + 1) * sizeof(int),
                       cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(old.blk, nw.blk, (size_t)(nw.P + 1) * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.sell_ci, nw.sell_ci, (size_t)nw.sell_slots * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.sell_val, nw.sell_val, (size_t)nw.sell_slots * sizeof(double),
+                      cudaMemcpyDeviceToDevice, st);
     }
     cudaStreamSynchronize(st);
     free_plan(nw);
@@ -273,78 +274,23 @@ static void flat_ranges(int64_t E, int64_t P, int64_t b, int wid, int64_t* s, in
   *e = S0 + L * (wid + 1) / kWarps;
 }
 
-// Chunks of <= kStRows rows and <= kStCap entries (greedy, in row order), and
-// an entry-balanced contiguous run of chunks per block (k_rows_stream).
-static int plan_rows_stream(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* out,
-                            cudaStream_t st) {
-  RowPlan p;
-  p.kind = PLAN_STREAM;
-  std::vector<int2> ch;
-  ch.reserve((size_t)(nnz / kStCap + rows / kStRows + 2));
-  int64_t r = 0;
-  while (r < rows) {
-    ch.push_back(make_int2((int)r, rp[r]));
-    int64_t e = r + 1;  // one row always fits (max row length <= kStCap)
-    while (e < rows && e - r < kStRows && rp[e + 1] - rp[r] <= kStCap) ++e;
-    r = e;
-  }
-  ch.push_back(make_int2((int)rows, (int)nnz));
-  p.nchunks = (int)ch.size() - 1;
-  const int64_t pmax = (int64_t)sms * kStBlocks;
-  p.P = (int)std::max<int64_t>(1, std::min<int64_t>(pmax, p.nchunks));
-  std::vector<int> blk((size_t)p.P + 1);
-  for (int b = 0; b <= p.P; ++b) {
-    if (b == p.P) {
-      blk[b] = p.nchunks;
-      continue;
-    }
-    const int64_t target = nnz * b / p.P;
-    int lo = 0, hi = p.nchunks;  // first chunk starting at or after target
-    while (lo < hi) {
-      const int mid = (lo + hi) / 2;
-      if (ch[mid].y < target) lo = mid + 1; else hi = mid;
-    }
-    blk[b] = lo;
-  }
-  for (int b = 1; b <= p.P; ++b) blk[b] = std::max(blk[b], blk[b - 1]);
-  TS_CUDA(cudaMalloc(&p.chunks, ch.size() * sizeof(int2)));
-  TS_CUDA(cudaMalloc(&p.blk, blk.size() * sizeof(int)));
-  TS_CUDA(cudaMemcpyAsync(p.chunks, ch.data(), ch.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-  TS_CUDA(cudaMemcpyAsync(p.blk, blk.data(), blk.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  TS_CUDA(cudaStreamSynchronize(st));
-  *out = p;
-  return 0;
-}
-
 int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* out,
                   cudaStream_t st) {
   RowPlan p;
   const int64_t pmax = resident_blocks(sms);
   const bool long_rows = rows > 0 && nnz / rows >= 32 && nnz >= (int64_t)kWarps * 256;
   if (!long_rows) {
-    // warp-cooperative short rows (TS_CSR_SHORT=thread selects the
-    // thread-per-row kernel, kept for comparison)
-    // thread-per-row for small (L2-resident, latency-bound) matrices, the
-    // coalesced warp-cooperative kernel once the pass is HBM-bound.
-    // TS_CSR_SHORT=thread|warp forces one (kernel comparisons).
+    // thread-per-row CSR for small (L2-resident, latency-bound) matrices, the
+    // sliced-ELL copy (coalesced, no row-pointer chase) once the pass is
+    // HBM-bound; TS_CSR_SHORT=thread|sell forces one (kernel comparisons).
+    // The SELL tables are built by build_sell() on the device arrays.
     const char* force = getenv("TS_CSR_SHORT");
     bool thread_rows = nnz < ((int64_t)1 << 21);
     if (force && !strcmp(force, "thread")) thread_rows = true;
-    if (force && (!strcmp(force, "warp") || !strcmp(force, "stream"))) thread_rows = false;
-    p.kind = thread_rows ? PLAN_SHORT : PLAN_WARP;
-    // TS_CSR_SHORT=pf: the prefetching warp kernel (opt-in: 39.0 vs 37.9 us on
-    // C5's A^T v inside the library, despite 33.6 vs 41 us in the microbench)
-    if (!thread_rows && force && !strcmp(force, "pf")) p.kind = PLAN_WARP_PF;
-    int64_t g = thread_rows ? (rows + kNT - 1) / kNT : (rows + kNT * 4 - 1) / (kNT * 4);
+    if (force && !strcmp(force, "sell")) thread_rows = false;
+    p.kind = thread_rows ? PLAN_SHORT : PLAN_SELL;
+    const int64_t g = thread_rows ? (rows + kNT - 1) / kNT : ((rows + 31) / 32 + kWarps - 1) / kWarps;
     p.P = (int)std::max<int64_t>(1, std::min(g, pmax));
-    // TS_CSR_SHORT=stream: the TMA-streamed chunk kernel (opt-in: bitwise
-    // equal, 16.5 vs 16.6 us bare on C4 in tools/microbench/spmv_short.cu, but
-    // 23.7 vs 21.6 us inside CTA solves, whose epilogues delay its refills)
-    if (!thread_rows && force && !strcmp(force, "stream")) {
-      int64_t maxlen = 0;
-      for (int64_t r = 0; r < rows; ++r) maxlen = std::max<int64_t>(maxlen, rp[r + 1] - rp[r]);
-      if (maxlen <= kStCap) return plan_rows_stream(rp, rows, nnz, sms, out, st);
-    }
     *out = p;
     return 0;
   }
@@ -378,28 +324,15 @@ int plan_rows_csr(const int* rp, int64_t rows, int64_t nnz, int sms, RowPlan* ou
   return 0;
 }
 
-int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t st) {
+int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t) {
   RowPlan p;
-  const int64_t pmax = resident_blocks(sms);
-  const int64_t E = m * n;
-  if (n < 128 || E < (int64_t)kWarps * 256) {
+  if (n < 128 || m * n < (int64_t)kWarps * 256) {
     p.kind = PLAN_SHORT;
-    p.P = (int)std::max<int64_t>(1, std::min((m + kNT - 1) / kNT, pmax));
-    *out = p;
-    return 0;
+    p.P = (int)std::max<int64_t>(1, std::min((m + kNT - 1) / kNT, (int64_t)resident_blocks(sms)));
+  } else {
+    p.kind = PLAN_TILE;
+    p.P = tile_grid(m, n, sms, kTileNBlocks);
   }
-  p.kind = PLAN_FLAT;
-  p.P = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * kFlatBlocks, E / ((int64_t)kWarps * 256)));
-  std::vector<int> wr((size_t)p.P * kWarps);
-  for (int64_t b = 0; b < p.P; ++b)
-    for (int w = 0; w < kWarps; ++w) {
-      int64_t s, e;
-      flat_ranges(E, p.P, b, w, &s, &e);
-      wr[b * kWarps + w] = (int)(s / n);
-    }
-  TS_CUDA(cudaMalloc(&p.wrow, wr.size() * sizeof(int)));
-  TS_CUDA(cudaMemcpyAsync(p.wrow, wr.data(), wr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  TS_CUDA(cudaStreamSynchronize(st));
   *out = p;
   return 0;
 }
@@ -503,21 +436,28 @@ __global__ void k_rowptr_from_keys(const int* keys, int64_t nnz, int64_t ncols, 
   }
 }
 
-__global__ void k_tile_keys(const int* ci, int64_t nnz, int* tkey) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
-       k += (int64_t)gridDim.x * blockDim.x)
-    tkey[k] = ci[k] / kCtTW;
+// sliced-ELL copy (k_rows_sell): 32 x the longest row of each 32-row slice
+__global__ void k_sell_width(const int* rp, int64_t rows, int64_t nsl, int* w32) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= nsl; q += (int64_t)gridDim.x * blockDim.x) {
+    int w = 0;
+    if (q < nsl)
+      for (int64_t r = q * 32; r < rows && r < q * 32 + 32; ++r) w = max(w, rp[r + 1] - rp[r]);
+    w32[q] = 32 * w;
+  }
 }
-__global__ void k_gather_ctile(const int* perm, const int* rowid, const int* ci, const double* val,
-                               int64_t nnz, int64_t m, double* tval, uint16_t* tci, int* qkey) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int k = perm[j];
-    const int c = ci[k];
-    const int t = c / kCtTW;
-    tval[j] = val[k];
-    tci[j] = (uint16_t)(c - t * kCtTW);
-    qkey[j] = (int)(t * m + rowid[k]);
+// slot (slice q, entry k, lane l) = sp[q] + 32 k + l <- entry k of row 32 q + l
+__global__ void k_sell_fill(const int* rp, const int* ci, const double* val, int64_t rows, int64_t nsl,
+                            const int* sp, int* sci, double* sval) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nsl * 32; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = t >> 5, r = t;
+    const int l = (int)(t & 31);
+    const int b0 = sp[q], w = (sp[q + 1] - b0) >> 5;
+    const int k0 = r < rows ? rp[r] : 0, len = r < rows ? rp[r + 1] - k0 : 0;
+    for (int k = 0; k < w; ++k) {
+      const int64_t d = (int64_t)b0 + 32 * k + l;
+      sci[d] = k < len ? ci[k0 + k] : kSellPad;
+      sval[d] = k < len ? val[k0 + k] : 0.0;
+    }
   }
 }
 
@@ -526,6 +466,48 @@ static int grid_for(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4096));
 }
 
+// The sliced-ELL tables of a PLAN_SELL orientation, from its CSR on the
+// device (no-op for other plans): slice widths on the device, the offsets
+// scanned on the host in 64 bits (a padded size past the int32 slot range
+// falls back to the thread-per-row kernel), then the fill on the device.
+static int build_sell(RowPlan& p, const int* rp, const int* ci, const double* val, int64_t rows, int sms, int dev,
+                      cudaStream_t st) {
+  if (p.kind != PLAN_SELL) return 0;
+  const int64_t nsl = (rows + 31) / 32;
+  std::vector<int> w((size_t)nsl + 1);
+  {
+    Arena ar(st);
+    int* w32;
+    TS_CHECK(ar.get(&w32, (size_t)nsl + 1));
+    k_sell_width<<<grid_for(nsl + 1), 256, 0, st>>>(rp, rows, nsl, w32);
+    TS_CUDA(cudaGetLastError());
+    TS_CUDA(d2h_pinned(w.data(), w32, ((size_t)nsl + 1) * sizeof(int), st));
+  }
+  int64_t total = 0;
+  for (int64_t q = 0; q <= nsl; ++q) {
+    const int64_t wq = w[q];
+    w[q] = (int)std::min<int64_t>(total, INT32_MAX);
+    total += wq;
+  }
+  if (total >= (int64_t)INT32_MAX) {  // slot offsets are int: keep the CSR kernel
+    p.kind = PLAN_SHORT;
+    p.P = (int)std::max<int64_t>(1, std::min<int64_t>((rows + kNT - 1) / kNT, resident_blocks(sms)));
+    return 0;
+  }
+  const size_t slots = (size_t)std::max<int64_t>(total, 1);
+  if (dev_malloc(&p.sell_sp, ((size_t)nsl + 1) * sizeof(int), dev) != cudaSuccess ||
+      dev_malloc(&p.sell_ci, slots * sizeof(int), dev) != cudaSuccess ||
+      dev_malloc(&p.sell_val, slots * sizeof(double), dev) != cudaSuccess) {
+    set_error("cudaMalloc for the sliced-ELL copy (%lld slots) failed", (long long)total);
+    return TS_ENOMEM;
+  }
+  p.sell_slots = total;
+  TS_CUDA(cudaMemcpyAsync(p.sell_sp, w.data(), ((size_t)nsl + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+  k_sell_fill<<<grid_for(nsl * 32), 256, 0, st>>>(rp, ci, val, rows, nsl, p.sell_sp, p.sell_ci, p.sell_val);
+  TS_CUDA(cudaGetLastError());
+  TS_CUDA(cudaStreamSynchronize(st));  // the host offsets leave scope
+  return 0;
+}
 }  // namespace ts
 
 using namespace ts;
@@ -538,7 +520,7 @@ static void free_matrix(Mat* A) {
   cudaDeviceSynchronize();
   destroy_instances(A);
   void* ps[] = {A->a,   A->aT,  A->rp,  A->ci,  A->val, A->rpT, A->ciT, A->valT,
-                A->tval, A->tci, A->trp, A->tblk};
+                nullptr};
   for (void* p : ps)
     if (p) cudaFree(p);
   free_plan(A->planN);
@@ -562,7 +544,7 @@ int ts_device_count(int* count) {
 // storage pool (see retire_take); everything else is freed.
 static int matrix_release(ts_matrix* A, bool complete) {
   if (!A) return 0;
-  if (complete && matrix_pool_enabled() && !A->comm && !A->tval && A->halo == 0) {
+  if (complete && matrix_pool_enabled() && !A->comm && A->halo == 0) {
     {
       DeviceGuard g(A->dev);
       cudaDeviceSynchronize();  // no solve may still read the storage
@@ -734,26 +716,13 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
     A->npart = npart_elems(m, n);
     if (!rc) rc = plan_rows_dense(m, n, A->sms, &A->planN, st);
     if (!rc) {
-      // 128-bit loads; TS_DENSE_VW=4 selects the 256-bit variants (measured slower)
-      const char* e = getenv("TS_DENSE_VW");
-      const int vw = (e && atoi(e) == 4) ? 4 : 2;
-      A->planN.vw = vw;
       A->planT.kind = PLAN_TILE;
-      A->planT.vw = vw;
-      A->planT.P = tile_grid(m, n, A->sms, vw, vw == 2 ? kTileTBlocks : kMinBlocks, kTileMinRowsT);
-      // TMA-streamed A^T v: TS_DENSE_T=tma (measured ~4 % slower than the
-      // register-staged tile kernel on C2, kept for experiments)
-      const char* te = getenv("TS_DENSE_T");
-      if (te && !strcmp(te, "tma") && vw == 2) {
-        A->planT.kind = PLAN_TMA;
-        const int per_sm = std::max(1, std::min(2, (227 * 1024 - 4096) / kTmaSmem));
-        A->planT.P = std::max(1, std::min(tile_grid(m, n, A->sms, 2), A->sms * per_sm));
-      }
+      A->planT.P = tile_grid(m, n, A->sms, kTileTBlocks, kTileMinRowsT);
       // small dense A (<= kTransBytes, L2-sized): A^T v as the fused row-tile
       // kernel over a transposed copy (C1: 7.3 vs 9.4 us per pass: no split-
       // tile merges); TS_DENSE_T=cols keeps the column-tile kernel
-      if (!rc && m >= 128 && n >= 128 && 8 * m * n <= kTransBytes && !(te && !strcmp(te, "cols")) &&
-          A->planT.kind == PLAN_TILE && vw == 2) {
+      const char* te = getenv("TS_DENSE_T");
+      if (m >= 128 && n >= 128 && 8 * m * n <= kTransBytes && !(te && !strcmp(te, "cols"))) {
         A->ldaT = m >= 64 ? (m + 15) / 16 * 16 : (m + 3) / 4 * 4;
         if (dev_malloc(&A->aT, (size_t)A->ldaT * n * sizeof(double), device) != cudaSuccess) {
           set_error("cudaMalloc(transposed dense %lld x %lld) failed", (long long)n, (long long)m);
@@ -761,19 +730,9 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
         } else {
           if (A->ldaT != m) cudaMemsetAsync(A->aT, 0, (size_t)A->ldaT * n * sizeof(double), st);
           A->planT.kind = PLAN_TRANS;
-          A->planT.P = tile_grid(n, m, A->sms, 2, kTileNBlocks);
+          A->planT.P = tile_grid(n, m, A->sms, kTileNBlocks);
           A->npart = npart_elems(m, n) + npart_elems(n, m);  // disjoint A v / A^T v layouts
         }
-      }
-      // A v in the A^T v tile geometry (measured faster than the flat split on
-      // C2: 137 vs 145 us); TS_DENSE_N=flat selects the flat split
-      const char* fe = getenv("TS_DENSE_N");
-      if (A->planN.kind == PLAN_FLAT && !(fe && !strcmp(fe, "flat"))) {
-        A->planN.kind = PLAN_TILE;
-        A->planN.P = tile_grid(m, n, A->sms, 2, kTileNBlocks);
-        // one-kernel A v (k_rows_tile_fused); TS_DENSE_N=split keeps the tile +
-        // combine kernels
-        A->planN.fused = !(fe && !strcmp(fe, "split"));
       }
     }
     if (!rc) rc = finish_create(A, st, ar);
@@ -846,8 +805,11 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       if ((rc = ar.get(&rng, 2))) return fail(rc);
       EpiIdxRange er{A->ci, rng};
       if ((rc = launch_vec(nnz, A->sms, er, wk, st))) return fail(rc);
-      double hr[2];
-      d2h_pinned(hr, rng, sizeof(hr), st);
+      double hr[2] = {0.0, 0.0};
+      if (d2h_pinned(hr, rng, sizeof(hr), st) != cudaSuccess) {
+        set_error("CSR index range read-back failed: %s", cudaGetErrorString(cudaGetLastError()));
+        return fail(TS_ECUDA);
+      }
       if (hr[0] < 0 || hr[1] >= (double)n) {
         set_error("CSR column index out of range [0, %lld)", (long long)n);
         return fail(TS_EINVAL);
@@ -873,43 +835,6 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       }
       k_gather_T<<<grid_for(nnz), 256, 0, st>>>(perm_out, rowid, A->val, A->ciT, A->valT, nnz);
       k_rowptr_from_keys<<<grid_for(nnz + 1), 256, 0, st>>>(keys_out, nnz, n, A->rpT);
-      // column-tiled copy for wide long-row A v (C5-like: x does not fit a cache)
-      // opt-in (TS_CSR_CTILE=1): on C5 it measured 101 us vs 64 us for the flat
-      // long-row kernel (partials + combine + 64 KB smem occupancy outweigh the
-      // shared-memory gathers); kept for further work
-      const char* ce = getenv("TS_CSR_CTILE");
-      const int64_t nct = (n + kCtTW - 1) / kCtTW;
-      const bool want_ct = (ce && !strcmp(ce, "1")) && m > 0 && nnz / m >= 32 &&
-                           n > 2 * (int64_t)kCtTW && nct * m + 1 < (int64_t)INT32_MAX;
-      if (want_ct) {
-        int *tkey, *qkey;
-        if ((rc = ar.get(&tkey, nz)) || (rc = ar.get(&qkey, nz))) return fail(rc);
-        if (cudaMalloc(&A->tval, nz * sizeof(double)) != cudaSuccess ||
-            cudaMalloc(&A->tci, nz * sizeof(uint16_t)) != cudaSuccess ||
-            cudaMalloc(&A->trp, (nct * m + 1) * sizeof(int)) != cudaSuccess) {
-          set_error("cudaMalloc for the column-tiled CSR failed");
-          return fail(TS_ENOMEM);
-        }
-        k_tile_keys<<<grid_for(nnz), 256, 0, st>>>(A->ci, nnz, tkey);
-        k_iota<<<grid_for(nnz), 256, 0, st>>>(perm_in, nnz);
-        int tbits = 1;
-        while (tbits < 31 && ((int64_t)1 << tbits) < nct) ++tbits;
-        size_t tb2 = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey, keys_out, perm_in, perm_out, (int)nnz, 0,
-                                        tbits, st);
-        void* tmp2 = tmp;
-        if (tb2 > tmp_bytes && (rc = ar.get((char**)&tmp2, tb2))) return fail(rc);
-        size_t tb3 = std::max(tb2, tmp_bytes);
-        if (cub::DeviceRadixSort::SortPairs(tmp2, tb3, tkey, keys_out, perm_in, perm_out, (int)nnz, 0,
-                                            tbits, st) != cudaSuccess) {
-          set_error("radix sort for the column-tiled CSR failed");
-          return fail(TS_ECUDA);
-        }
-        k_gather_ctile<<<grid_for(nnz), 256, 0, st>>>(perm_out, rowid, A->ci, A->val, nnz, m, A->tval,
-                                                     A->tci, qkey);
-        k_rowptr_from_keys<<<grid_for(nnz + 1), 256, 0, st>>>(qkey, nnz, nct * m, A->trp);
-        A->ct_nct = (int)nct;
-      }
     } else {
       cudaMemsetAsync(A->rpT, 0, (n + 1) * sizeof(int), st);
     }
@@ -929,34 +854,16 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
         free_plan(pN);
         return fail(rc);
       }
-      const bool keepN = adopt_plan(A->planN, pN, st);
-      const bool keepT = adopt_plan(A->planT, pT, st);
+      if ((rc = build_sell(pN, A->rp, A->ci, A->val, m, A->sms, device, st)) ||
+          (rc = build_sell(pT, A->rpT, A->ciT, A->valT, n, A->sms, device, st))) {
+        free_plan(pN);
+        free_plan(pT);
+        return fail(rc);
+      }
+      const bool keepN = adopt_plan(A->planN, pN, m, st);
+      const bool keepT = adopt_plan(A->planT, pT, n, st);
       // a recycled handle's instances bake the old launch geometry
       if (reuse && !(keepN && keepT)) destroy_instances(A);
-    }
-    if (A->ct_nct > 0) {
-      // nnz-balanced (tile, row) unit ranges, one per block
-      const int64_t U = (int64_t)A->ct_nct * m;
-      std::vector<int> trp_h((size_t)U + 1);
-      cudaMemcpy(trp_h.data(), A->trp, (U + 1) * sizeof(int), cudaMemcpyDeviceToHost);
-      const int P = A->sms * kCtBlocksPerSM;
-      std::vector<int> blk((size_t)P + 1);
-      for (int b = 0; b <= P; ++b) {
-        const int64_t target = nnz * b / P;
-        blk[b] = b == P ? (int)U
-                        : (int)(std::lower_bound(trp_h.begin(), trp_h.end() - 1, (int)target) -
-                                trp_h.begin());
-      }
-      for (int b = 1; b <= P; ++b) blk[b] = std::max(blk[b], blk[b - 1]);
-      if (cudaMalloc(&A->tblk, (P + 1) * sizeof(int)) != cudaSuccess ||
-          cudaMemcpy(A->tblk, blk.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice) !=
-              cudaSuccess) {
-        set_error("column-tiled CSR plan upload failed");
-        return fail(TS_ECUDA);
-      }
-      A->planN.kind = PLAN_CTILE;
-      A->planN.P = P;
-      A->npart = U;
     }
     if (nnz > 0) {
       if ((rc = finish_create(A, st, ar))) return fail(rc);
@@ -1057,8 +964,14 @@ int ts_matrix_create_csr_pair(const int32_t* indptr, const int32_t* indices, con
       free_plan(pN);
       return fail(rc);
     }
-    adopt_plan(A->planN, pN, st);
-    adopt_plan(A->planT, pT, st);
+    if ((rc = build_sell(pN, A->rp, A->ci, A->val, m, A->sms, device, st)) ||
+        (rc = build_sell(pT, A->rpT, A->ciT, A->valT, m, A->sms, device, st))) {
+      free_plan(pN);
+      free_plan(pT);
+      return fail(rc);
+    }
+    adopt_plan(A->planN, pN, m, st);
+    adopt_plan(A->planT, pT, m, st);
     if (nnz > 0) {
       if ((rc = finish_create(A, st, ar))) return fail(rc);
     } else {

@@ -22,9 +22,14 @@
 
 namespace ts {
 
-enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WARP = 3, PLAN_TMA = 4,
-                      PLAN_CTILE = 5, PLAN_STREAM = 6, PLAN_WROW = 7, PLAN_WARP_PF = 8,
-                      PLAN_TRANS = 9 };
+// PLAN_FLAT   CSR rows with >= 32 entries on average, irregular lengths (k_rows_flat)
+// PLAN_SHORT  thread per row, L2-resident (k_rows_short; dense n < 128 too)
+// PLAN_TILE   dense A v (k_rows_tile_fused) / dense A^T v (k_cols_tile)
+// PLAN_WROW   long CSR rows of near-uniform length (k_rows_wrow)
+// PLAN_TRANS  small dense A^T v over a transposed copy (k_rows_tile_fused)
+// PLAN_SELL   short CSR rows, HBM-sized: sliced-ELL copy (k_rows_sell)
+enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WROW = 7, PLAN_TRANS = 9,
+                      PLAN_SELL = 10 };
 
 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans):
@@ -38,12 +43,11 @@ struct RowPlan {
   int kind = PLAN_SHORT;
   int P = 1;            // blocks
   int* wrow = nullptr;  // device [P * kWarps] (PLAN_FLAT)
-  int vw = 2;           // dense: columns per 128/256-bit load
-  int fused = 0;        // dense PLAN_TILE A v: one kernel (k_rows_tile_fused)
-  // PLAN_STREAM: chunk table (first row, first entry) and per-block chunk runs
-  int nchunks = 0;
-  int2* chunks = nullptr;  // device [nchunks + 1]
-  int* blk = nullptr;      // device [P + 1]
+  // PLAN_SELL: the sliced-ELL copy of this orientation (see k_rows_sell)
+  int64_t sell_slots = 0;  // padded entries
+  int* sell_sp = nullptr;  // device [ceil(rows / 32) + 1]
+  int* sell_ci = nullptr;  // device [sell_slots]
+  double* sell_val = nullptr;
 };
 
 struct Instance;  // cached solver instance (ts_drivers.cuh)
@@ -67,15 +71,8 @@ struct Mat {
   double fro = 0.0;
   RowPlan planN, planT;
   int Pmax = 0;  // largest grid any pass of this matrix uses
-  // per-(tile,row) partials a solve's Work needs (dense tile A v, column-tiled CSR)
+  // per-(tile,row) partials a solve's Work needs (dense tile A v)
   int64_t npart = 0;
-  // column-tiled CSR for wide sparse A v (PLAN_CTILE): entries grouped by
-  // column tile (stable: row-major inside a tile), 16-bit in-tile column index
-  int ct_nct = 0;
-  double* tval = nullptr;
-  uint16_t* tci = nullptr;
-  int* trp = nullptr;   // [ct_nct * m + 1] start of (tile, row) in tval/tci
-  int* tblk = nullptr;  // [P + 1] first (tile,row) unit of each block (nnz-balanced)
   // column shard of a matrix split over ranks (nullptr: unsharded)
   Comm* comm = nullptr;
   int64_t n_global = 0, col_off = 0;
@@ -84,11 +81,14 @@ struct Mat {
   // past either end, served from neighbours before every pass (k_halo)
   int row_shard = 0;
   int64_t halo = 0, m_global = 0, row_off = 0;
+  // tall row-block shard: rows [row_off, row_off + m) of A with all n columns;
+  // x-space is replicated, b-space split; A^T v sums an n-vector over ranks
+  int tall_shard = 0;
   // solver instances (buffers + instantiated graphs) cached per solver shape
   std::mutex cache_mu;
   std::vector<Instance*> cache;
 
-  DenseRows dense(int vw = 2) const { return DenseRows{a, lda, m, n, vw}; }
+  DenseRows dense() const { return DenseRows{a, lda, m, n}; }
   CsrRows csr() const { return CsrRows{rp, ci, val, m, nnz}; }
   CsrRows csrT() const { return CsrRows{rpT, ciT, valT, n, nnz}; }
 };
@@ -138,13 +138,6 @@ inline int vec_grid(int64_t len, int sms, int per_sm = 0) {
   return (int)g;
 }
 
-// warp-per-row combine: enough warps for the rows, at most one resident wave
-inline int combine_grid(int64_t m, int sms) {
-  int64_t g = (m + kWarps - 1) / kWarps;
-  const int64_t cap = resident_blocks(sms);
-  return (int)std::max<int64_t>(1, std::min(g, cap));
-}
-
 // per_sm: resident blocks per SM of the tile kernel (one full wave);
 // min_rows: rows of a tile per block at least.  Only small (L2-resident)
 // matrices feel it: for A^T v the column pieces of a tile are merged in block
@@ -154,9 +147,8 @@ inline int combine_grid(int64_t m, int sms) {
 constexpr int64_t kTransBytes = 32ll << 20;
 constexpr int kTileMinRowsN = 8;
 constexpr int kTileMinRowsT = 32;
-inline int tile_grid(int64_t m, int64_t n, int sms, int vw, int per_sm = kMinBlocks,
-                     int min_rows = kTileMinRowsN) {
-  const int64_t tw = (int64_t)vw * kNT;
+inline int tile_grid(int64_t m, int64_t n, int sms, int per_sm = kMinBlocks, int min_rows = kTileMinRowsN) {
+  const int64_t tw = 2 * kNT;
   const int64_t nct = (n + tw - 1) / tw;
   const int64_t U = nct * m;
   int64_t g = U / min_rows;
@@ -173,18 +165,8 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
                 cudaStream_t st) {
   if (M.kind == 0) {
     if (!trans) {
-      if (M.planN.kind == PLAN_TILE && M.planN.fused) {
+      if (M.planN.kind == PLAN_TILE)
         k_rows_tile_fused<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
-      } else if (M.planN.kind == PLAN_TILE) {
-        const int64_t nct = (M.n + 2 * kNT - 1) / (2 * kNT);
-        k_rows_tile<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk.npart);
-        k_tile_combine<Epi><<<combine_grid(M.m, M.sms), kNT, 0, st>>>(M.m, nct, wk.npart, epi, wk);
-      } else if (M.planN.kind == PLAN_FLAT && M.planN.vw == 4)
-        k_rows_flat<DenseRows4, Epi><<<M.planN.P, kNT, 0, st>>>(DenseRows4{M.dense()}, x, xs, epi,
-                                                                  wk, M.planN.wrow);
-      else if (M.planN.kind == PLAN_FLAT)
-        k_rows_flat<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk,
-                                                                 M.planN.wrow);
       else
         k_rows_short<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
     } else if (M.planT.kind == PLAN_TRANS) {
@@ -192,50 +174,20 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
       // counters must stay zero between launches (self-resetting)
       Work wt = wk;
       wt.npart = wk.npart + npart_elems(M.m, M.n);
-      k_rows_tile_fused<Epi><<<M.planT.P, kNT, 0, st>>>(DenseRows{M.aT, M.ldaT, M.n, M.m, 2}, x, xs,
-                                                        epi, wt);
-    } else if (M.planT.kind == PLAN_TMA) {
-      static bool attr_set = false;  // per process; the attribute is per function
-      if (!attr_set) {
-        cudaFuncSetAttribute(k_cols_tma<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-        attr_set = true;
-      }
-      k_cols_tma<Epi><<<M.planT.P, kNT, kTmaSmem, st>>>(M.dense(), x, xs, epi, wk);
-    } else if (M.planT.vw == 4) {
-      k_cols_tile<Epi, 4><<<M.planT.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+      k_rows_tile_fused<Epi><<<M.planT.P, kNT, 0, st>>>(DenseRows{M.aT, M.ldaT, M.n, M.m}, x, xs, epi, wt);
     } else {
       k_cols_tile<Epi, 2><<<M.planT.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
     }
   } else {
     const RowPlan& pl = trans ? M.planT : M.planN;
     const CsrRows acc = trans ? M.csrT() : M.csr();
-    if (pl.kind == PLAN_CTILE) {
-      static bool attr_set = false;
-      if (!attr_set) {
-        cudaFuncSetAttribute(k_csr_ctile<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kCtTW * (int)sizeof(double));
-        attr_set = true;
-      }
-      k_csr_ctile<Epi><<<pl.P, kNT, kCtTW * sizeof(double), st>>>(
-          CtileRows{M.tval, M.tci, M.trp, M.tblk, M.m, M.n, M.ct_nct}, x, xs, epi, wk.npart);
-      k_tile_combine<Epi><<<combine_grid(M.m, M.sms), kNT, 0, st>>>(M.m, M.ct_nct, wk.npart, epi, wk);
-    } else if (pl.kind == PLAN_FLAT)
+    if (pl.kind == PLAN_SELL)
+      k_rows_sell<Epi><<<pl.P, kNT, 0, st>>>(SellRows{pl.sell_sp, pl.sell_ci, pl.sell_val, acc.m}, x, xs,
+                                             epi, wk);
+    else if (pl.kind == PLAN_FLAT)
       k_rows_flat<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk, pl.wrow);
-    else if (pl.kind == PLAN_WARP)
-      k_rows_warp<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
     else if (pl.kind == PLAN_WROW)
       k_rows_wrow<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
-    else if (pl.kind == PLAN_WARP_PF)
-      k_rows_warp_pf<Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
-    else if (pl.kind == PLAN_STREAM) {
-      static bool attr_set = false;
-      if (!attr_set) {
-        cudaFuncSetAttribute(k_rows_stream<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStSmem);
-        attr_set = true;
-      }
-      k_rows_stream<Epi><<<pl.P, kNT, kStSmem, st>>>(StreamRows{acc.rp, acc.ci, acc.val, pl.chunks, pl.blk},
-                                                     x, xs, epi, wk);
-    }
     else
       k_rows_short<CsrRows, Epi><<<pl.P, kNT, 0, st>>>(acc, x, xs, epi, wk);
   }

@@ -2,22 +2,26 @@
 // epilogue fused in, and a deterministic multi-slot reduction whose last
 // arriving block runs a scalar finisher (the solver state machine).
 //
-//   k_rows_flat  y = M v, M row-major (dense rows or CSR).  The flat element
-//                range [0, E) is split into equal contiguous ranges per block
-//                and per warp, so every launch is perfectly load balanced for
-//                any row-length distribution; rows cut by a warp boundary are
-//                merged inside the block, rows cut by a block boundary are
-//                merged by the last block to arrive on that row (counter per
-//                end block).  Used for dense A v (n >= 128) and CSR rows with
-//                >= 32 nnz on average (C5's A v: ~1000 nnz / row).
-//   k_rows_short one thread per row, sequential left-to-right sum without FMA
-//                contraction: bitwise identical to scipy's csr_matvec for
-//                CSR (C3/C4 rows, C5's transposed CSR = CSC columns).
-//   k_cols_tile  y = A^T v for dense row-major A without materialising A^T:
-//                512-column tiles, the (tile, row) unit space split evenly over
-//                blocks, partial tiles at block boundaries merged by the last
-//                arriving block.  Fixed-order, no atomics on values.
-//   k_vec        fused elementwise vector pass (+ reductions, + finisher).
+//   k_rows_flat       y = M v, CSR with long irregular rows.  The flat entry
+//                     range [0, E) is split into equal contiguous ranges per
+//                     block and per warp, so every launch is load balanced for
+//                     any row-length distribution; rows cut by a warp boundary
+//                     are merged inside the block, rows cut by a block boundary
+//                     by the last block to arrive on that row.
+//   k_rows_wrow       long CSR rows of near-uniform length (C5's A v): warp per
+//                     row with the next chunks' loads in flight.
+//   k_rows_short      one thread per row, sequential left-to-right sum without
+//                     FMA: bitwise scipy csr_matvec; L2-resident matrices (C3).
+//   k_rows_sell       one thread per row over a sliced-ELL copy, bitwise
+//                     scipy; HBM-sized short rows (C4, C5's A^T v).
+//   k_rows_tile_fused dense A v: 512-column tiles, group-major (tile, row)
+//                     units, groups combined by the block that completes them.
+//   k_cols_tile       y = A^T v for dense row-major A without materialising
+//                     A^T: 512-column tiles, the (tile, row) unit space split
+//                     evenly over blocks, partial tiles at block boundaries
+//                     merged by the last arriving block.
+//   k_vec             fused elementwise vector pass (+ reductions, + finisher).
+// Every reduction has a fixed order; no atomics on values.
 //
 // Epilogue contract (class Epi):
 //   static constexpr int K;               reduction slots (<= kKMax)
@@ -64,97 +68,7 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 struct DenseRows {
   const double* a;
   int64_t lda, m, n;
-  int vw = 2;  // 4: 256-bit loads in the flat A v (requires lda % 4 == 0); see DenseRows4
-  __device__ __forceinline__ int64_t rbeg(int64_t r) const { return r * n; }
-  __device__ __forceinline__ int64_t rend(int64_t r) const { return (r + 1) * n; }
-  __device__ __forceinline__ int64_t total() const { return m * n; }
   __device__ __forceinline__ int64_t rows() const { return m; }
-  // lane partial of sum_{k0<=k<k1} a[r, k - r n] * xs(x[k - r n])
-  __device__ __forceinline__ double seg(int64_t r, int64_t k0, int64_t k1, const double* x,
-                                        const XS& xs, int lane) const {
-    const int64_t c0 = k0 - r * n, c1 = k1 - r * n;
-    const double* row = a + r * lda;
-    double h = 0.0, t = 0.0;
-    int64_t c = c0;
-    if (c & 1) {
-      if (lane == 0) h = row[c] * xs(__ldg(x + c));
-      ++c;
-    }
-    const int64_t npair = (c1 - c) >> 1;
-    const int64_t cend = c + 2 * npair;
-    if (cend < c1 && lane == 0) t = row[cend] * xs(__ldg(x + cend));
-    const double* rp = row + c;
-    const double* xp = x + c;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int64_t p = lane;
-    for (; p + 224 < npair; p += 256) {
-      double2 v[8], xv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = ld_stream2(rp + 2 * (p + 32 * u));
-#ifdef TS_EXP_NOX
-#pragma unroll
-      for (int u = 0; u < 8; ++u) xv[u] = make_double2(1.0 + u, 2.0 - u);
-#else
-#pragma unroll
-      for (int u = 0; u < 8; ++u) xv[u] = ldg2(xp + 2 * (p + 32 * u));
-#endif
-#pragma unroll
-      for (int u = 0; u < 8; u += 4) {
-        a0 = fma(v[u].x, xs(xv[u].x), a0); a0 = fma(v[u].y, xs(xv[u].y), a0);
-        a1 = fma(v[u + 1].x, xs(xv[u + 1].x), a1); a1 = fma(v[u + 1].y, xs(xv[u + 1].y), a1);
-        a2 = fma(v[u + 2].x, xs(xv[u + 2].x), a2); a2 = fma(v[u + 2].y, xs(xv[u + 2].y), a2);
-        a3 = fma(v[u + 3].x, xs(xv[u + 3].x), a3); a3 = fma(v[u + 3].y, xs(xv[u + 3].y), a3);
-      }
-    }
-    for (; p < npair; p += 32) {
-      double2 v0 = ld_stream2(rp + 2 * p);
-      double2 x0 = ldg2(xp + 2 * p);
-      a0 = fma(v0.x, xs(x0.x), a0); a0 = fma(v0.y, xs(x0.y), a0);
-    }
-    return ((a0 + a1) + (a2 + a3)) + (h + t);
-  }
-  // 256-bit variant: quads of 4 columns, kQ quads of A + kQ of x per lane in flight
-  static constexpr int kQ = 2;
-  __device__ __forceinline__ double seg4(int64_t r, int64_t k0, int64_t k1, const double* x,
-                                         const XS& xs, int lane) const {
-    const int64_t c0 = k0 - r * n, c1 = k1 - r * n;
-    const double* row = a + r * lda;
-    double h = 0.0, t = 0.0;
-    int64_t c = (c0 + 3) & ~(int64_t)3;
-    if (c > c1) c = c1;
-    if (lane < c - c0) h = row[c0 + lane] * xs(__ldg(x + c0 + lane));  // <= 3 head elements
-    const int64_t nq = (c1 - c) >> 2;
-    const int64_t cend = c + 4 * nq;
-    if (lane < c1 - cend) t = row[cend + lane] * xs(__ldg(x + cend + lane));  // <= 3 tail
-    const double* rp = row + c;
-    const double* xp = x + c;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int64_t q = lane;
-    for (; q + 32 * (kQ - 1) < nq; q += 32 * kQ) {
-      double v[kQ][4], xv[kQ][4];
-#pragma unroll
-      for (int u = 0; u < kQ; ++u) ld_stream4(rp + 4 * (q + 32 * u), v[u]);
-#pragma unroll
-      for (int u = 0; u < kQ; ++u) ldg4(xp + 4 * (q + 32 * u), xv[u]);
-#pragma unroll
-      for (int u = 0; u < kQ; ++u) {
-        a0 = fma(v[u][0], xs(xv[u][0]), a0);
-        a1 = fma(v[u][1], xs(xv[u][1]), a1);
-        a2 = fma(v[u][2], xs(xv[u][2]), a2);
-        a3 = fma(v[u][3], xs(xv[u][3]), a3);
-      }
-    }
-    for (; q < nq; q += 32) {
-      double v[4], xv[4];
-      ld_stream4(rp + 4 * q, v);
-      ldg4(xp + 4 * q, xv);
-      a0 = fma(v[0], xs(xv[0]), a0);
-      a1 = fma(v[1], xs(xv[1]), a1);
-      a2 = fma(v[2], xs(xv[2]), a2);
-      a3 = fma(v[3], xs(xv[3]), a3);
-    }
-    return ((a0 + a1) + (a2 + a3)) + (h + t);
-  }
   // whole row, one thread, column order (short-row path)
   template <bool kCoh = false>
   __device__ __forceinline__ double row_serial(int64_t r, const double* x, const XS& xs) const {
@@ -162,14 +76,6 @@ struct DenseRows {
     double s = 0.0;
     for (int64_t c = 0; c < n; ++c) s = fma(row[c], xs(ldx<kCoh>(x + c)), s);
     return s;
-  }
-};
-
-// A v with 256-bit loads: same geometry, seg() -> seg4()
-struct DenseRows4 : DenseRows {
-  __device__ __forceinline__ double seg(int64_t r, int64_t k0, int64_t k1, const double* x,
-                                        const XS& xs, int lane) const {
-    return seg4(r, k0, k1, x, xs, lane);
   }
 };
 
@@ -272,38 +178,6 @@ __device__ __forceinline__ void finish_last(Epi& epi, const Work& wk, const doub
     __syncthreads();
     epi.finish_block();
   }
-}
-
-// Persistent loop: end of a pass phase (all threads of every block of the
-// cooperative grid).  The last block to arrive reduces the first `nb` blocks'
-// partials in the same fixed order, runs the finisher and finish_block, then
-// opens the next generation; the others wait for it.  One atomic per block
-// per phase replaces a kernel boundary.
-template <class Epi>
-__device__ void phase_end(Epi& epi, const Work& wk, const double* facc, int nb) {
-  constexpr int K = Epi::K;
-  __shared__ double sm[kWarps * kKMax];
-  __shared__ int slast;
-  unsigned gen0 = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) slast = bar_arrive(wk.gbar, gridDim.x, &gen0) ? 1 : 0;
-  __syncthreads();
-  if (slast) {
-    __threadfence();
-    double red[K];
-    reduce_partials<K>(wk.bacc, facc, nb, red, sm, epi);
-    if (threadIdx.x == 0) {
-      ktimer_end(epi.timer());
-      epi.finish(red);
-    }
-    __syncthreads();
-    epi.finish_block();
-    __syncthreads();
-    if (threadIdx.x == 0) bar_release(wk.gbar, gen0);
-  } else if (threadIdx.x == 0) {
-    bar_wait(wk.gbar, gen0);
-  }
-  __syncthreads();
 }
 
 // ----------------------------------------------------------- k_rows_flat ----
@@ -515,106 +389,33 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const dou
   body_rows_short<Acc, Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x, kb, ke);
 }
 
-// ----------------------------------------------------------- k_rows_warp ----
-// Short CSR rows, warp-cooperative: a warp owns 32 consecutive rows; their
-// contiguous nnz range is streamed in coalesced chunks (values, indices,
-// gathered x), the exact products v * x are staged in shared memory, and each
-// lane then adds ITS row's products left to right without FMA — the same
-// operation sequence as scipy's csr_matvec, so the result is bitwise the
-// reference's, with coalesced HBM traffic instead of per-thread strided rows.
-constexpr int kWCh = 256;  // products staged per warp per chunk
+// ----------------------------------------------------------- k_rows_sell ----
+// Short CSR rows, HBM-sized (C4 both ways, C5's A^T v): a sliced-ELL copy
+// (SELL-32) built once at matrix creation.  Slice s holds rows [32 s, 32 s +
+// 32) interleaved — entry k of row 32 s + l sits at sp[s] + 32 k + l — padded
+// to the slice's longest row with column kSellPad.  One thread per row: every
+// load of a warp is one coalesced request, no row pointers are chased, and
+// each thread adds ITS row's products left to right without FMA, skipping the
+// padding — scipy's csr_matvec operation sequence, so the result is bitwise
+// the reference's.  tools/microbench/spmv_sell.cu (cold L2): C4 28.7 -> 22.6
+// us, C5^T 46.1 -> 30.8 us against the warp-cooperative CSR kernel it
+// replaces.
+constexpr int kSellPad = INT32_MIN;  // padding column (local indices of row shards may be negative)
+constexpr int kSellU = 8;            // entries of a row in flight per thread
 
-template <class Epi, bool kP>
-__device__ __forceinline__ void body_rows_warp(const CsrRows& A, const double* __restrict__ x, XS xs,
-                                               Epi& epi, const Work& wk, int64_t b, int64_t P) {
-  constexpr int K = Epi::K;
-  __shared__ double sm[kWarps * kKMax];
-  __shared__ double buf[kWarps][kWCh];
-  __shared__ int sflag;
-  xs.load();
-  ktimer_begin(epi.timer());
-  __shared__ double epi_smem[kEpiSmem];
-  epi.prepare(epi_smem);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t m = A.m;
-  const int64_t ngroups = (m + 31) / 32;
-  const int64_t W = P * kWarps, w = b * kWarps + wid;
-  const int64_t g0 = ngroups * w / W, g1 = ngroups * (w + 1) / W;  // contiguous groups per warp
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  double* sb = buf[wid];
-  for (int64_t g = g0; g < g1; ++g) {
-    const int64_t r = g * 32 + lane;
-    const bool live = r < m;
-    const int64_t rlast = (g * 32 + 32 < m) ? g * 32 + 32 : m;
-    const int kb = live ? __ldg(A.rp + r) : 0;
-    const int ke = live ? __ldg(A.rp + r + 1) : 0;
-    const int gb = __shfl_sync(0xffffffffu, kb, 0);
-    const int ge = __ldg(A.rp + rlast);
-    double sum = 0.0;
-    for (int cs = gb; cs < ge; cs += kWCh) {
-      constexpr int J = kWCh / 32;
-      double vv[J], xv[J];
-      int cc[J];
-#pragma unroll
-      for (int j = 0; j < J; ++j) {  // independent loads first ...
-        const int k = cs + j * 32 + lane;
-        const bool ok = k < ge;
-        vv[j] = ok ? ld_stream(A.val + k) : 0.0;
-        cc[j] = ok ? ld_stream_i(A.ci + k) : 0;
-      }
-#pragma unroll
-      for (int j = 0; j < J; ++j) xv[j] = ldx<kP>(x + cc[j]);  // ... then the gathers
-#pragma unroll
-      for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xs(xv[j]));
-      __syncwarp();
-      const int lo = kb > cs ? kb : cs;
-      const int hi = ke < cs + kWCh ? ke : cs + kWCh;
-      for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, sb[k - cs]);
-      __syncwarp();
-    }
-    if (live) epi.elem(r, sum, acc);
-  }
-  block_reduce<K>(acc, sm, epi);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
-  }
-  if constexpr (!kP) finish_last(epi, wk, nullptr, (int)P, sm, &sflag);
-}
+struct SellRows {
+  const int* sp;      // [nslices + 1] padded entry offsets (multiples of 32)
+  const int* ci;      // column per slot, kSellPad on padding
+  const double* val;  // value per slot (0 on padding)
+  int64_t m;
+};
 
 template <class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp(CsrRows A, const double* __restrict__ x,
-                                                             XS xs, Epi epi, Work wk) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
-  body_rows_warp<Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
-}
-
-// ------------------------------------------------------- k_rows_warp_pf ----
-// k_rows_warp with software prefetch, for short rows of >= 8 entries whose x
-// gathers are scattered (C5's A^T v: 10 entries per column at random rows):
-// chunks are kWpfJ x 32 entries, and the NEXT chunk's values and indices (of
-// this group, else of the next group) are loaded before the current chunk's
-// gathers, so a warp always has matrix loads in flight.  Same products, same
-// per-row left-to-right sums without FMA as k_rows_warp: bitwise scipy.
-// tools/microbench/spmv_short.cu, C5^T-like: 33.6 us vs 41 us, but inside the
-// library on C5's A^T v 39.0 vs 37.9 us for k_rows_warp: opt-in
-// (TS_CSR_SHORT=pf).
-constexpr int kWpfJ = 6;
-
-template <class Epi>
-__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp_pf(CsrRows A, const double* __restrict__ x,
-                                                                XS xs, Epi epi, Work wk) {
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_sell(SellRows A, const double* __restrict__ x, XS xs,
+                                                             Epi epi, Work wk) {
   constexpr int K = Epi::K;
-  constexpr int J = kWpfJ, CH = 32 * J;
+  constexpr int U = kSellU;
   __shared__ double sm[kWarps * kKMax];
-  __shared__ double buf[kWarps][CH];
   __shared__ int sflag;
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) {
@@ -626,66 +427,35 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_warp_pf(CsrRows A, con
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t m = A.m, ngroups = (m + 31) / 32;
-  const int64_t W = (int64_t)gridDim.x * kWarps, w = (int64_t)blockIdx.x * kWarps + wid;
-  const int64_t g0 = ngroups * w / W, g1 = ngroups * (w + 1) / W;
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (A.m + 31) >> 5;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  double* sb = buf[wid];
-  double pv[J];
-  int pc[J];
-  auto load = [&](int cs, int ge) {
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int k = cs + j * 32 + lane;
-      const bool ok = k < ge;
-      pv[j] = ok ? ld_stream(A.val + k) : 0.0;
-      pc[j] = ok ? ld_stream_i(A.ci + k) : 0;
-    }
-  };
-  auto bounds = [&](int64_t g, int* gb, int* ge) {
-    const int64_t rf = g * 32, rl = (rf + 32 < m) ? rf + 32 : m;
-    *gb = __ldg(A.rp + rf);
-    *ge = __ldg(A.rp + rl);
-  };
-  int gb = 0, ge = 0;
-  if (g0 < g1) {
-    bounds(g0, &gb, &ge);
-    load(gb, ge);
-  }
-  for (int64_t g = g0; g < g1; ++g) {
-    const int64_t r = g * 32 + lane;
-    const bool live = r < m;
-    const int kb = live ? __ldg(A.rp + r) : 0, ke = live ? __ldg(A.rp + r + 1) : 0;
-    int ngb = 0, nge = 0;
-    const bool more = g + 1 < g1;
-    if (more) bounds(g + 1, &ngb, &nge);
+  for (int64_t s = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); s < nsl; s += W) {
+    const int b0 = __ldg(A.sp + s);
+    const int wd = (__ldg(A.sp + s + 1) - b0) >> 5;
+    const int* cp = A.ci + b0 + lane;
+    const double* vp = A.val + b0 + lane;
     double sum = 0.0;
-    for (int cs = gb; cs < ge; cs += CH) {
-      double vv[J];
-      int cc[J];
+    for (int k0 = 0; k0 < wd; k0 += U) {
+      double v[U], xv[U];
+      int c[U];
 #pragma unroll
-      for (int j = 0; j < J; ++j) {
-        vv[j] = pv[j];
-        cc[j] = pc[j];
+      for (int u = 0; u < U; ++u) {  // independent loads first ...
+        const bool ok = k0 + u < wd;
+        c[u] = ok ? ld_stream_i(cp + 32 * (k0 + u)) : kSellPad;
+        v[u] = ok ? ld_stream(vp + 32 * (k0 + u)) : 0.0;
       }
-      if (cs + CH < ge) load(cs + CH, ge);
-      else if (more) load(ngb, nge);
-      double xv[J];
 #pragma unroll
-      for (int j = 0; j < J; ++j) xv[j] = __ldg(x + cc[j]);
+      for (int u = 0; u < U; ++u) xv[u] = c[u] != kSellPad ? __ldg(x + c[u]) : 0.0;  // ... then the gathers
 #pragma unroll
-      for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xs(xv[j]));
-      __syncwarp();
-      const int lo = kb > cs ? kb : cs, hi = ke < cs + CH ? ke : cs + CH;
-      for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, sb[k - cs]);
-      __syncwarp();
+      for (int u = 0; u < U; ++u)
+        if (c[u] != kSellPad) sum = __dadd_rn(sum, __dmul_rn(v[u], xs(xv[u])));
     }
-    if (live) epi.elem(r, sum, acc);
-    gb = ngb;
-    ge = nge;
+    const int64_t r = s * 32 + lane;
+    if (r < A.m) epi.elem(r, sum, acc);
   }
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {
@@ -765,125 +535,6 @@ __global__ void __launch_bounds__(kNT, kWrowBlocks) k_rows_wrow(CsrRows A, const
     }
     const double sum = warp_reduce((a[0] + a[1]) + (a[2] + a[3]), RED_SUM);
     if (lane == 0) epi.elem(r, sum, acc);
-  }
-  block_reduce<K>(acc, sm, epi);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
-  }
-  finish_last(epi, wk, nullptr, (int)gridDim.x, sm, &sflag);
-}
-
-// --------------------------------------------------------- k_rows_stream ----
-// Short CSR rows streamed through shared memory by the Tensor Memory
-// Accelerator.  The rows are cut (once, at plan time) into chunks of at most
-// kStRows rows and kStCap entries; a block owns a contiguous, entry-balanced
-// run of chunks.  One thread keeps kStStages chunks in flight with
-// cp.async.bulk copies of the chunk's values, column indices and row
-// pointers (three contiguous byte ranges) completing on a per-stage mbarrier,
-// so HBM sees deep sequential streams that do not wait on the gathers.  The
-// block then forms the exact products v * x in place (all threads, batched
-// gathers) and each thread adds ITS row's products left to right without FMA
-// — scipy's csr_matvec operation sequence, so the result is bitwise the
-// reference's.  Used for HBM-sized short-row matrices (C4; C5's A^T v).
-constexpr int kStCap = 1024;   // entries per chunk
-constexpr int kStRows = 256;   // rows per chunk
-constexpr int kStStages = 4;   // chunks in flight per block
-constexpr int kStBlocks = 4;   // resident blocks per SM (4 x 53.5 KB of stages)
-struct __align__(16) StStage {
-  double val[kStCap + 2];  // +2: the copy starts at the 16-B boundary below e0
-  int idx[kStCap + 4];
-  int rp[kStRows + 8];
-};
-constexpr int kStSmem = kStStages * (int)sizeof(StStage);
-static_assert(sizeof(StStage) % 16 == 0, "stage must keep 16-B alignment");
-
-struct StreamRows {
-  const int* rp;
-  const int* ci;
-  const double* val;
-  const int2* chunks;  // [nchunks + 1] (first row, first entry) of each chunk
-  const int* blk;      // [P + 1] first chunk of each block
-};
-
-template <class Epi>
-__global__ void __launch_bounds__(kNT, kStBlocks) k_rows_stream(StreamRows A, const double* __restrict__ x,
-                                                               XS xs, Epi epi, Work wk) {
-  constexpr int K = Epi::K;
-  extern __shared__ __align__(128) unsigned char st_raw[];
-  StStage* stg = reinterpret_cast<StStage*>(st_raw);
-  __shared__ __align__(8) unsigned long long full[kStStages];
-  __shared__ double sm[kWarps * kKMax];
-  __shared__ int sflag;
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
-  const int tid = threadIdx.x;
-  const int c0 = __ldg(A.blk + blockIdx.x), c1 = __ldg(A.blk + blockIdx.x + 1);
-  auto issue = [&](int c, int s) {  // thread 0: bring chunk c into stage s
-    const int2 a = __ldg(A.chunks + c), z = __ldg(A.chunks + c + 1);
-    const int e0v = a.y & ~1, e0i = a.y & ~3, r0 = a.x & ~3;
-    const unsigned bv = (unsigned)(((z.y - e0v) * 8 + 15) & ~15);
-    const unsigned bi = (unsigned)(((z.y - e0i) * 4 + 15) & ~15);
-    const unsigned br = (unsigned)(((z.x + 1 - r0) * 4 + 15) & ~15);
-    mbar_expect_tx(&full[s], bv + bi + br);
-    bulk_g2s(stg[s].val, A.val + e0v, bv, &full[s]);
-    bulk_g2s(stg[s].idx, A.ci + e0i, bi, &full[s]);
-    bulk_g2s(stg[s].rp, A.rp + r0, br, &full[s]);
-  };
-  if (tid == 0) {
-    for (int s = 0; s < kStStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-    for (int s = 0; s < kStStages && c0 + s < c1; ++s) issue(c0 + s, s);
-  }
-  xs.load();
-  ktimer_begin(epi.timer());
-  __shared__ double epi_smem[kEpiSmem];
-  epi.prepare(epi_smem);
-  __syncthreads();
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  int2 a = c0 < c1 ? __ldg(A.chunks + c0) : make_int2(0, 0);
-  for (int c = c0, g = 0; c < c1; ++c, ++g) {
-    const int s = g % kStStages;
-    const int2 z = __ldg(A.chunks + c + 1);
-    const int ne = z.y - a.y, nr = z.x - a.x;
-    mbar_wait(&full[s], (unsigned)((g / kStStages) & 1));
-    double* sv = stg[s].val + (a.y & 1);
-    const int* si = stg[s].idx + (a.y & 3);
-    const int* sr = stg[s].rp + (a.x & 3);
-    // exact products in place; four independent gathers in flight per thread
-    for (int k0 = tid; k0 < ne; k0 += 4 * kNT) {
-      double xv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = k0 + u * kNT;
-        xv[u] = k < ne ? __ldg(x + si[k]) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = k0 + u * kNT;
-        if (k < ne) sv[k] = __dmul_rn(sv[k], xs(xv[u]));
-      }
-    }
-    __syncthreads();
-    for (int r = tid; r < nr; r += kNT) {
-      const int kb = sr[r] - a.y, ke = sr[r + 1] - a.y;
-      double sum = 0.0;
-      for (int k = kb; k < ke; ++k) sum = __dadd_rn(sum, sv[k]);
-      epi.elem((int64_t)a.x + r, sum, acc);
-    }
-    __syncthreads();  // stage consumed by every thread
-    if (tid == 0 && c + kStStages < c1) {
-      // the generic-proxy product stores must be ordered before the async
-      // proxy overwrites the stage
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(c + kStStages, s);
-    }
-    a = z;
   }
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {
@@ -1041,389 +692,6 @@ __global__ void __launch_bounds__(kNT, kTileTBlocks) k_cols_tile(DenseRows A, co
   body_cols_tile<Epi, VW, false, kTileTRows>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
 }
 
-// ------------------------------------------------------------ k_cols_tma ----
-// Dense A^T v streamed by the Tensor Memory Accelerator: the block's (tile,
-// row) units are fetched as 4 KB row chunks with cp.async.bulk into a ring of
-// kTmaStages stages x kTmaRows rows in shared memory (one producer thread,
-// mbarrier transaction counts), so the memory system sees deep, contiguous
-// per-block streams with no register staging; 256 consumer threads own two
-// columns each and accumulate from shared memory.  Partial tiles at block
-// boundaries are merged exactly like k_cols_tile (same reduction order).
-#ifndef TS_TMA_ROWS
-#define TS_TMA_ROWS 8
-#endif
-#ifndef TS_TMA_STAGES
-#define TS_TMA_STAGES 3
-#endif
-constexpr int kTmaRows = TS_TMA_ROWS;
-constexpr int kTmaStages = TS_TMA_STAGES;
-constexpr int kTmaTW = 2 * kNT;  // tile width (columns)
-constexpr int kTmaSmem = kTmaStages * kTmaRows * kTmaTW * 8;
-
-template <class Epi>
-__global__ void __launch_bounds__(kNT, 2) k_cols_tma(DenseRows A, const double* __restrict__ x, XS xs,
-                                                    Epi epi, Work wk) {
-  constexpr int K = Epi::K;
-  extern __shared__ __align__(128) double ring[];  // [stage][row][kTmaTW]
-  __shared__ __align__(8) unsigned long long full[kTmaStages];
-  __shared__ double sm[kWarps * kKMax];
-  __shared__ int sflag;
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
-  xs.load();
-  KTimer* kt = epi.timer();
-  ktimer_begin(kt);
-  __shared__ double epi_smem[kEpiSmem];
-  epi.prepare(epi_smem);
-  __syncthreads();
-  const int64_t m = A.m, n = A.n, lda = A.lda;
-  const int64_t nct = (n + kTmaTW - 1) / kTmaTW;
-  const int64_t U = nct * m;
-  const int64_t P = gridDim.x, b = blockIdx.x;
-  const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  // The unit range is consumed as groups of <= kTmaRows rows that never cross a
-  // tile boundary; group g covers units [gstart(g), gstart(g) + grows(g)).
-  // Producer state walks the same sequence ahead of the consumers.
-  auto group_at = [&](int64_t u, int64_t* ct, int64_t* r, int* rows) {
-    *ct = u / m;
-    *r = u - *ct * m;
-    int64_t left = m - *r;
-    if (U1 - u < left) left = U1 - u;
-    *rows = (int)(left < kTmaRows ? left : kTmaRows);
-  };
-  auto issue = [&](int64_t u, int stage) {
-    int64_t ct, r;
-    int rows;
-    group_at(u, &ct, &r, &rows);
-    const int64_t cb = ct * kTmaTW;
-    const int64_t cols = (n - cb < kTmaTW) ? n - cb : kTmaTW;
-    const unsigned bytes = (unsigned)(((cols * 8) + 15) & ~15);  // tail rounds into the lda padding
-    mbar_expect_tx(&full[stage], bytes * rows);
-    for (int i = 0; i < rows; ++i)
-      bulk_g2s(ring + ((size_t)stage * kTmaRows + i) * kTmaTW, A.a + (r + i) * lda + cb, bytes,
-               &full[stage]);
-    return (int64_t)rows;
-  };
-  int64_t pu = U0;  // producer position
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kTmaStages && pu < U1; ++s) pu += issue(pu, s);
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  long long ct_first = -1, ct_last = -1;
-  int64_t cu = U0;  // consumer position
-  int g = 0;
-  while (cu < U1) {
-    // one segment = one tile, rows r0..r1 of this block's range
-    const int64_t ct = cu / m, r0 = cu - ct * m;
-    const int64_t r1 = (m < r0 + (U1 - cu)) ? m : r0 + (U1 - cu);
-    const int64_t c = ct * kTmaTW + 2 * threadIdx.x;
-    const bool two = c + 1 < n, one = c < n;
-    double ax0 = 0.0, ay0 = 0.0, ax1 = 0.0, ay1 = 0.0;
-    for (int64_t r = r0; r < r1;) {
-      const int stage = g % kTmaStages;
-      const unsigned phase = (unsigned)((g / kTmaStages) & 1);
-      const int rows = (int)((r1 - r < kTmaRows) ? r1 - r : kTmaRows);
-      double xr_[kTmaRows];  // x for this group, fetched before waiting on the data
-#pragma unroll
-      for (int i = 0; i < kTmaRows; ++i) xr_[i] = (i < rows) ? xs(__ldg(x + r + i)) : 0.0;
-      mbar_wait(&full[stage], phase);
-      const double* sbuf = ring + (size_t)stage * kTmaRows * kTmaTW + 2 * threadIdx.x;
-#pragma unroll
-      for (int i = 0; i < kTmaRows; ++i) {
-        if (i < rows) {
-          const double xr = xr_[i];
-          const double2 v = *reinterpret_cast<const double2*>(sbuf + (size_t)i * kTmaTW);
-          if (i & 1) {
-            if (one) ax1 = fma(v.x, xr, ax1);
-            if (two) ay1 = fma(v.y, xr, ay1);
-          } else {
-            if (one) ax0 = fma(v.x, xr, ax0);
-            if (two) ay0 = fma(v.y, xr, ay0);
-          }
-        }
-      }
-      __syncthreads();  // stage consumed: refill it
-      if (threadIdx.x == 0 && pu < U1) pu += issue(pu, stage);
-      r += rows;
-      ++g;
-    }
-    const double sx = ax0 + ax1, sy = ay0 + ay1;
-    if (r0 == 0 && r1 == m) {
-      if (one) epi.elem(c, sx, acc);
-      if (two) epi.elem(c + 1, sy, acc);
-    } else {
-      const int which = (r0 > 0) ? 0 : 1;  // 0: tile began in an earlier block
-      double* dst = wk.tpart + ((size_t)b * 2 + which) * kCW + 2 * threadIdx.x;
-      dst[0] = sx;
-      dst[1] = sy;
-      if (which == 0) ct_first = ct; else ct_last = ct;
-    }
-    cu += r1 - r0;
-  }
-  // split-tile merges (as k_cols_tile)
-  bool end_block = false;
-  if (ct_first >= 0 && ct_first * m + m <= U1) end_block = true;
-  for (int which = 0; which < 2; ++which) {
-    const long long ct = which == 0 ? ct_first : ct_last;
-    if (ct < 0) continue;
-    const int64_t ba = blk_of(ct * m, U, P), bb = blk_of(ct * m + m - 1, U, P);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned prev = atomicAdd(wk.cnt + bb, 1u);
-      sflag = (prev == (unsigned)(bb - ba));
-    }
-    __syncthreads();
-    if (sflag) {
-      __threadfence();
-      const int64_t c = ct * kTmaTW + 2 * threadIdx.x;
-      double y0 = __ldcg(wk.tpart + ((size_t)ba * 2 + 1) * kCW + 2 * threadIdx.x);
-      double y1 = __ldcg(wk.tpart + ((size_t)ba * 2 + 1) * kCW + 2 * threadIdx.x + 1);
-      for (int64_t q = ba + 1; q <= bb; ++q) {
-        y0 += __ldcg(wk.tpart + ((size_t)q * 2) * kCW + 2 * threadIdx.x);
-        y1 += __ldcg(wk.tpart + ((size_t)q * 2) * kCW + 2 * threadIdx.x + 1);
-      }
-      double facc[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) facc[k] = red_identity(epi.op(k));
-      if (c < n) epi.elem(c, y0, facc);
-      if (c + 1 < n) epi.elem(c + 1, y1, facc);
-      block_reduce<K>(facc, sm, epi);
-      if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) wk.facc[bb * kKMax + k] = facc[k];
-        wk.cnt[bb] = 0u;
-      }
-    }
-  }
-  block_reduce<K>(acc, sm, epi);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      wk.bacc[b * kKMax + k] = acc[k];
-      if (!end_block) wk.facc[b * kKMax + k] = red_identity(epi.op(k));
-    }
-  }
-  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
-    double red[K];
-    reduce_partials<K>(wk.bacc, wk.facc, (int)P, red, sm, epi);
-    if (threadIdx.x == 0) {
-      ktimer_end(kt);
-      epi.finish(red);
-    }
-    __syncthreads();
-    epi.finish_block();
-  }
-}
-
-// ----------------------------------------------------------- k_csr_ctile ----
-// Wide CSR A v (C5: 10^4 rows x 10^6 columns, ~1000 nnz per row) over a
-// column-tiled copy of A: the entries of column tile t (kCtTW columns) form a
-// CSR of their own, rows in order, 16-bit in-tile column indices.  A block
-// owns an nnz-balanced run of (tile, row) units; per tile it stages the tile's
-// slice of v in shared memory once, so every gather is a shared-memory read
-// instead of a random L2 sector (the untiled kernel's limiter).  Each warp
-// streams 32 rows' entries coalesced, stages the exact products, and lane l
-// adds row l's products left to right.  part[t * m + r] is then summed over
-// tiles in order by k_tile_combine.
-struct CtileRows {
-  const double* val;
-  const uint16_t* ci;
-  const int* rp;    // [nct * m + 1]
-  const int* blk;   // [P + 1]
-  int64_t m, n;
-  int nct;
-};
-
-template <class Epi>
-__global__ void __launch_bounds__(kNT, kCtBlocksPerSM) k_csr_ctile(CtileRows A, const double* __restrict__ x,
-                                                                 XS xs, Epi epi, double* __restrict__ part) {
-  extern __shared__ __align__(128) double xsm[];  // [kCtTW] raw tile slice of v (TMA)
-  __shared__ double buf[kWarps][kWCh];
-  __shared__ __align__(8) unsigned long long xbar;
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) return;  // k_tile_combine owns idle()
-  xs.load();
-  ktimer_begin(epi.timer());
-  __shared__ double epi_smem[kEpiSmem];
-  epi.prepare(epi_smem);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t m = A.m;
-  const int64_t q0 = A.blk[blockIdx.x], q1 = A.blk[blockIdx.x + 1];
-  if (threadIdx.x == 0) {
-    mbar_init(&xbar, 1);
-    fence_mbar_init();
-  }
-  double* sb = buf[wid];
-  unsigned phase = 0;
-  for (int64_t q = q0; q < q1;) {
-    const int64_t t = q / m;
-    const int64_t ra = q - t * m;
-    const int64_t rb = (q1 - t * m < m) ? q1 - t * m : m;  // rows [ra, rb) of tile t
-    const int64_t cb = t * (int64_t)kCtTW;
-    const int64_t cw = (A.n - cb < kCtTW) ? A.n - cb : kCtTW;
-    __syncthreads();  // previous slice fully consumed (and barrier init visible)
-    if (threadIdx.x == 0) {  // one bulk copy brings the whole slice
-      const unsigned bytes = (unsigned)((cw * 8 + 15) & ~15);
-      mbar_expect_tx(&xbar, bytes);
-      bulk_g2s(xsm, x + cb, bytes, &xbar);
-    }
-    const int* rp = A.rp + t * m;
-    const int64_t ngroups = (rb - ra + 31) / 32;
-    // row pointers of the warp's first group while the slice is in flight
-    int64_t g = wid;
-    int kb = 0, ke = 0, ge = 0;
-    auto fetch = [&](int64_t gg) {
-      const int64_t r = ra + gg * 32 + lane;
-      const int64_t rlast = (ra + gg * 32 + 32 < rb) ? ra + gg * 32 + 32 : rb;
-      kb = (r < rb) ? __ldg(rp + r) : 0;
-      ke = (r < rb) ? __ldg(rp + r + 1) : 0;
-      ge = __ldg(rp + rlast);
-    };
-    if (g < ngroups) fetch(g);
-    mbar_wait(&xbar, phase);
-    phase ^= 1u;
-    for (; g < ngroups; g += kWarps) {
-      const int64_t r = ra + g * 32 + lane;
-      const bool live = r < rb;
-      const int gb = __shfl_sync(0xffffffffu, kb, 0);
-      const int my_kb = kb, my_ke = ke, my_ge = ge;
-      if (g + kWarps < ngroups) fetch(g + kWarps);  // next group's pointers in flight
-      double sum = 0.0;
-      for (int cs = gb; cs < my_ge; cs += kWCh) {
-        constexpr int J = kWCh / 32;
-        double vv[J];
-        int cc[J];
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const int k = cs + j * 32 + lane;
-          const bool ok = k < my_ge;
-          vv[j] = ok ? ld_stream(A.val + k) : 0.0;
-          cc[j] = ok ? (int)__ldg(A.ci + k) : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < J; ++j) sb[j * 32 + lane] = __dmul_rn(vv[j], xs(xsm[cc[j]]));
-        __syncwarp();
-        const int lo = my_kb > cs ? my_kb : cs;
-        const int hi = my_ke < cs + kWCh ? my_ke : cs + kWCh;
-        for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, sb[k - cs]);
-        __syncwarp();
-      }
-      if (live) part[r * A.nct + t] = sum;
-    }
-    q = t * m + rb;
-  }
-}
-
-// ----------------------------------------------------------- k_rows_tile ----
-// Dense A v in the A^T v kernel's geometry: 512-column tiles, the (tile, row)
-// unit space split evenly over blocks, so both passes stream A with the same
-// coalesced 4 KB row chunks.  A warp keeps its tile's slice of v in registers
-// (loaded once per segment) and reduces one row chunk per step; the per-(tile,
-// row) sums go to `part` and k_tile_combine adds them in tile order.
-// The tile's 512-entry slice of v is staged once per segment in shared
-// memory (registers then hold only matrix data), and each warp keeps R row
-// chunks (R x 4 KB) in flight.  tools/microbench/dense_av.cu on C2: 141 us
-// with the slice in registers and one chunk per warp at 4 blocks/SM, 124 us
-// (6.44 TB/s) with R = 2 at 2 blocks/SM; every variant yields the same partials
-// bit for bit (each row chunk is reduced by the same lane FMA chain + xor tree).
-constexpr int kTileNBlocks = 2;  // k_rows_tile blocks per SM (128 registers)
-constexpr int kTileNRows = 2;    // row chunks in flight per warp
-
-template <class Epi, bool kP, int R = 1>
-__device__ __forceinline__ void body_rows_tile(const DenseRows& A, const double* __restrict__ x, XS xs,
-                                               Epi& epi, double* __restrict__ part, int64_t b, int64_t P) {
-  constexpr int TW = 2 * kNT;  // 512 columns: 16 per lane, 8 x 128-bit loads per row chunk
-  __shared__ __align__(16) double xsl[TW];
-  xs.load();
-  ktimer_begin(epi.timer());
-  __shared__ double epi_smem[kEpiSmem];
-  epi.prepare(epi_smem);
-  const int64_t m = A.m, n = A.n, lda = A.lda;
-  const int64_t nct = (n + TW - 1) / TW;
-  const int64_t U = nct * m;
-  const int64_t U0 = U * b / P, U1 = U * (b + 1) / P;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  auto dot = [&](const double2 (&v)[8]) -> double {
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; k += 2) {
-      const double2 x0 = *reinterpret_cast<const double2*>(xsl + 64 * k + 2 * lane);
-      const double2 x1 = *reinterpret_cast<const double2*>(xsl + 64 * (k + 1) + 2 * lane);
-      a0 = fma(v[k].x, x0.x, a0); a0 = fma(v[k].y, x0.y, a0);
-      a1 = fma(v[k + 1].x, x1.x, a1); a1 = fma(v[k + 1].y, x1.y, a1);
-    }
-    return warp_reduce(a0 + a1, RED_SUM);
-  };
-  for (int64_t u = U0; u < U1;) {
-    const int64_t ct = u / m, r0 = u - ct * m;
-    const int64_t r1 = (m < r0 + (U1 - u)) ? m : r0 + (U1 - u);
-    const int64_t cb = ct * TW;
-    const bool full = cb + TW <= n;
-    __syncthreads();  // previous slice consumed
-    for (int k = threadIdx.x; k < TW; k += kNT) {
-      const int64_t c = cb + k;
-      xsl[k] = (c < n) ? xs(ldx<kP>(x + c)) : 0.0;
-    }
-    __syncthreads();
-    int64_t r = r0 + wid;
-    if (full) {
-      for (; r + 8 * (R - 1) < r1; r += 8 * R) {
-        double2 v[R][8];
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) v[q][k] = ld_stream2(A.a + (r + 8 * q) * lda + cb + 2 * lane + 64 * k);
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const double sum = dot(v[q]);
-          if (lane == 0) part[(r + 8 * q) * nct + ct] = sum;
-        }
-      }
-      for (; r < r1; r += 8) {
-        double2 v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = ld_stream2(A.a + r * lda + cb + 2 * lane + 64 * k);
-        const double sum = dot(v);
-        if (lane == 0) part[r * nct + ct] = sum;
-      }
-    } else {
-      for (; r < r1; r += 8) {
-        const double* row = A.a + r * lda + cb + 2 * lane;
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int64_t c = cb + 64 * k + 2 * lane;
-          if (c < n) a0 = fma(ld_stream(row + 64 * k), xsl[64 * k + 2 * lane], a0);
-          if (c + 1 < n) a1 = fma(ld_stream(row + 64 * k + 1), xsl[64 * k + 2 * lane + 1], a1);
-        }
-        const double sum = warp_reduce(a0 + a1, RED_SUM);
-        if (lane == 0) part[r * nct + ct] = sum;
-      }
-    }
-    u += r1 - r0;
-  }
-}
-
-template <class Epi>
-__global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile(DenseRows A, const double* __restrict__ x,
-                                                               XS xs, Epi epi, double* __restrict__ part) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) return;  // k_tile_combine owns idle()
-  body_rows_tile<Epi, false, kTileNRows>(A, x, xs, epi, part, blockIdx.x, gridDim.x);
-}
-
 // ------------------------------------------------------ k_rows_tile_fused ----
 // Dense A v in ONE kernel.  The (tile, row) units are ordered group-major:
 // 256-row groups one after another, inside a group tile by tile, so a group's
@@ -1438,6 +706,11 @@ __global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile(DenseRows A, co
 // k_rows_tile + k_tile_combine 137 us).  Work::npart = [m x tiles partials |
 // gacc | group counters] (zeroed once, self-resetting).
 constexpr int kGroupRows = kNT;  // rows per combine group: one per thread
+// tools/microbench/dense_av.cu on C2: 141 us with the slice in registers and
+// one chunk per warp at 4 blocks/SM, 124 us (6.44 TB/s) with 2 row chunks in
+// flight per warp at 2 blocks/SM
+constexpr int kTileNBlocks = 2;  // blocks per SM (128 registers)
+constexpr int kTileNRows = 2;    // row chunks in flight per warp
 
 __host__ __device__ inline int64_t tile_groups(int64_t m) { return (m + kGroupRows - 1) / kGroupRows; }
 
@@ -1577,62 +850,6 @@ __global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile_fused(DenseRows
     __syncthreads();
     epi.finish_block();
   }
-}
-
-// y_r = sum over tiles of part[r][tile] (row-major partials): one warp per
-// row, lane-strided sums then the fixed xor tree; then the pass epilogue
-template <class Epi, bool kP>
-__device__ __forceinline__ void body_tile_combine(int64_t m, int64_t nct, const double* __restrict__ part,
-                                                  Epi& epi, const Work& wk, int64_t b, int64_t P) {
-  constexpr int K = Epi::K;
-  __shared__ double sm[kWarps * kKMax];
-  __shared__ double wacc[kWarps][K];
-  __shared__ int sflag;
-  __shared__ double epi_smem[kEpiSmem];
-  epi.prepare(epi_smem);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  const int64_t W = P * kWarps;
-  for (int64_t r = b * kWarps + wid; r < m; r += W) {
-    const double* pr = part + r * nct;
-    double y0 = 0.0, y1 = 0.0;
-    int64_t t = lane;
-    for (; t + 32 < nct; t += 64) {
-      y0 += __ldcg(pr + t);
-      y1 += __ldcg(pr + t + 32);
-    }
-    if (t < nct) y0 += __ldcg(pr + t);
-    const double y = warp_reduce(y0 + y1, RED_SUM);
-    if (lane == 0) epi.elem(r, y, acc);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) wacc[wid][k] = acc[k];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double v = wacc[0][k];
-      for (int j = 1; j < kWarps; ++j) v = red_combine(epi.op(k), v, wacc[j][k]);
-      wk.bacc[b * kKMax + k] = v;
-    }
-  }
-  if constexpr (!kP) finish_last(epi, wk, nullptr, (int)P, sm, &sflag);
-}
-
-template <class Epi>
-__global__ void __launch_bounds__(kNT) k_tile_combine(int64_t m, int64_t nct, const double* __restrict__ part,
-                                                     Epi epi, Work wk) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
-  body_tile_combine<Epi, false>(m, nct, part, epi, wk, blockIdx.x, gridDim.x);
 }
 
 // ----------------------------------------------------------------- k_vec ----

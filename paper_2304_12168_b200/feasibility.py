@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _native as N
 from ._solve import build_result, host_vec, rows_to_trace, trace_buffer
-from .linalg import as_device_matrix, frobenius_norm, matvec, norm2, shape_of
+from .linalg import as_device_matrix, frobenius_norm, local_rows, matvec, norm2, shape_of
 from .results import FEASIBILITY_TRACE_COLUMNS, SolveResult
 
 
@@ -53,6 +53,7 @@ def nonnegative_feasibility(a, b, eps, rho_max=None, max_iters=100_000) -> Solve
         if norm2(b) == 0.0:
             raise ValueError("b must be nonzero")
         raise ValueError("rho_max must be positive")
+    b = local_rows(a, b)  # row layouts keep their block of b
     dm, gram = as_device_matrix(a)
     nn = dm.shape[1]
     o = N.LpOptions()

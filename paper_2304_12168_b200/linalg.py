@@ -167,7 +167,7 @@ def as_device_matrix(a):
         return a, False
     if isinstance(a, GramProduct):
         return a.device_matrix, True
-    if type(a).__name__ in ("ShardedMatrix", "RowShardedMatrix"):
+    if getattr(a, "_ts_shard", False):  # shard.py layouts
         return a.device_matrix, False
     if isinstance(a, np.ndarray) or sparse.issparse(a) or _is_torch(a):
         return DeviceMatrix(a), False
@@ -179,20 +179,20 @@ def as_device_matrix(a):
 
 
 def local_slice(a, v, n_local: int):
-    """For a sharded matrix, this rank's slice of an n-vector given either
-    globally or already locally; identity otherwise."""
-    if v is None or type(a).__name__ not in ("ShardedMatrix", "RowShardedMatrix"):
+    """For a sharded matrix, this rank's part of an n-space vector given
+    either globally or already locally; identity otherwise."""
+    if v is None or not getattr(a, "_ts_shard", False):
         return v
-    arr = np.asarray(v, dtype=np.float64)
-    return a.local(arr) if arr.shape == (a.n_global,) else arr
+    return a.local_x(v)
 
 
 def local_rows(a, b):
-    """For a row-block sharded matrix, this rank's block of an m-vector (b);
-    identity otherwise (column shards keep m-vectors replicated)."""
-    if b is None or type(a).__name__ != "RowShardedMatrix":
+    """For a sharded matrix, this rank's part of an m-space vector (b): its
+    block on row layouts, the whole vector on column blocks; identity for
+    unsharded operands."""
+    if b is None or not getattr(a, "_ts_shard", False):
         return b
-    return a.local(b)
+    return np.ascontiguousarray(a.local_b(b), dtype=np.float64)
 
 
 def matvec(a, v) -> np.ndarray:

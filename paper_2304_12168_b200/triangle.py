@@ -89,6 +89,7 @@ def solve_in_ball(a, b, rho, eps, eps_prime=None, max_iters=100_000, x0=None) ->
         if norm2(b) == 0.0:
             raise ValueError("b must be nonzero")
         raise ValueError("rho must be positive")
+    b = local_rows(a, b)  # row layouts keep their block of b
     dm, gram, mo, nn = _dims(a)
     o = N.BallOptions()
     o.rho = float(rho)

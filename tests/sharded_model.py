@@ -224,3 +224,95 @@ def cta_row_sharded(rows_ext, cols_ext, hw, b_loc, epsilon, max_iters, t_max=5):
     atf = cols_ext @ _halo(fr, hw)
     return dict(status=status, iterations=it, x=x, residual_norm=math.sqrt(_dot_rows(fr, fr)),
                 normal_residual_norm=math.sqrt(_dot_rows(atf, atf)))
+
+
+# ------------------------------------------------------- tall row blocks ----
+# Row-block sharding of a tall matrix (TallShardedMatrix): each rank holds
+# A[r0:r1, :]; x-space vectors are replicated, b-space vectors split; A v is
+# local, A^T r = sum_p A_p^T r_p is an all-reduce of n-vectors, every b-space
+# dot / norm a scalar all-reduce, every x-space one local (replicated).
+
+def _rmv_tall(a_loc, r_loc):
+    return _ar(_rmv(a_loc, r_loc))
+
+
+def cta_tall_sharded(a_loc, b_loc, epsilon, max_iters, t_max=5):
+    """centering_solve (centering.py:263-358, Gram mode) on tall row blocks."""
+    x = np.zeros(a_loc.shape[1])
+    r = b_loc.copy()
+    bn = math.sqrt(_dot_rows(b_loc, b_loc))
+    eps_abs = epsilon * bn
+    m_glob = int(_ar(float(len(b_loc)))[0])
+    sched = port.schedule(min(t_max, m_glob))
+    status, it = "iteration_cap", 0
+    while it < max_iters:
+        rn = math.sqrt(_dot_rows(r, r))
+        if rn <= eps_abs:
+            status = "approx_solution"
+            break
+        t = next(sched)
+        p, q = [r], []
+        for _ in range(t):
+            q.append(_rmv_tall(a_loc, p[-1]))  # replicated n-vector
+            p.append(a_loc @ q[-1])            # local rows
+        phi = np.array([_dot_rows(p[k // 2], p[k - k // 2]) for k in range(1, 2 * t + 1)])
+        if phi[1] == 0.0:
+            status = "normal_eq_solution"
+            break
+        atr = float(np.linalg.norm(q[0]))
+        pick = None
+        for order in range(t, 0, -1):
+            al = port.hankel_coeffs(phi, order)
+            cand = r.copy()
+            for i in range(order):
+                cand -= al[i] * p[i + 1]
+            cn = math.sqrt(_dot_rows(cand, cand))
+            if pick is None or cn < pick[0]:
+                pick = (cn, order, al, cand)
+            if cn <= rn * (1.0 + 1e-13):
+                pick = (cn, order, al, cand)
+                break
+        if atr * atr <= eps_abs * eps_abs:
+            status = "normal_eq_solution"
+            break
+        _, order, al, r = pick
+        for i in range(order):
+            x = x + al[i] * q[i]
+        it += 1
+    fr = b_loc - a_loc @ x
+    return dict(status=status, iterations=it, x=x, residual_norm=math.sqrt(_dot_rows(fr, fr)),
+                normal_residual_norm=float(np.linalg.norm(_rmv_tall(a_loc, fr))))
+
+
+def ta_tall_sharded(a_loc, b_loc, eps, max_iters):
+    """solve_adaptive (triangle.py:170-251) on tall row blocks."""
+    x = np.zeros(a_loc.shape[1])
+    bp = np.zeros(len(b_loc))
+    rho = 0.0
+    events = []
+    status, it = "iteration_cap", 0
+    while it < max_iters:
+        gap = b_loc - bp
+        if math.sqrt(_dot_rows(gap, gap)) <= eps:
+            status = "approx_solution"
+            break
+        c = _rmv_tall(a_loc, gap)
+        cn = float(np.linalg.norm(c))
+        if cn <= eps:
+            status = "normal_eq_solution"
+            break
+        gb = _dot_rows(gap, b_loc)
+        if rho > 0.0 and rho * cn >= gb:
+            pre = (rho / cn) * c
+            d = a_loc @ pre - bp
+            al = min(1.0, max(0.0, _dot_rows(gap, d) / _dot_rows(d, d)))
+            bp = bp + al * d
+            x = (1.0 - al) * x + al * pre
+            events.append("pivot")
+        else:
+            rho = max(2.0 * rho, gb / cn)
+            events.append("expand")
+        it += 1
+    fr = b_loc - a_loc @ x
+    return dict(status=status, iterations=it, x=x, events=events,
+                residual_norm=math.sqrt(_dot_rows(fr, fr)))

@@ -1,11 +1,11 @@
 """Kernel-level device checks that the golden cases (all small) do not reach:
 
-* the TMA-streamed short-row CSR kernel (k_rows_stream, the plan for
-  HBM-sized short-row matrices such as C4 and C5's A^T v) must be bitwise
-  equal to scipy's csr_matvec order for A v and to the reference's
-  ``v @ csr`` row-order scatter for A^T v (linalg.py:42,55) on ragged
-  inputs: empty rows, rows at the chunk-size limit, a single row, rows whose
-  entries straddle 16-byte boundaries;
+* the sliced-ELL short-row CSR kernel (k_rows_sell, the plan for HBM-sized
+  short-row matrices such as C4 and C5's A^T v) must be bitwise equal to
+  scipy's csr_matvec order for A v and to the reference's ``v @ csr``
+  row-order scatter for A^T v (linalg.py:42,55) on ragged inputs: empty
+  rows, one very long row in a slice of short ones, a single row, a last
+  slice with fewer than 32 rows;
 * matrix handles recycled by the storage pool (same shape, new entries,
   same or different sparsity) give the same answers as fresh handles;
 * pinned result vectors come back correct and are recycled.
@@ -21,7 +21,7 @@ import scipy.sparse as sparse
 
 pytestmark = pytest.mark.gpu
 
-K_ST_CAP = 1024  # kStCap in csrc/ts_passes.cuh
+LONG = 1024  # a row far longer than its slice neighbours (padding-heavy slice)
 
 
 def _ragged(m, n, seed, max_row=40, empty_frac=0.1, long_rows=()):
@@ -42,11 +42,12 @@ def _ragged(m, n, seed, max_row=40, empty_frac=0.1, long_rows=()):
     return sparse.csr_array((vals, (rows, cols)), shape=(m, n))
 
 
-def _stream_matrix(a):
+def _forced_matrix(a, plan):
+    """DeviceMatrix with the short-row plan forced (plans are chosen at creation)."""
     import paper_2304_12168_b200 as ts
 
     old = os.environ.get("TS_CSR_SHORT")
-    os.environ["TS_CSR_SHORT"] = "stream"
+    os.environ["TS_CSR_SHORT"] = plan
     try:
         return ts.DeviceMatrix(a)
     finally:
@@ -56,20 +57,25 @@ def _stream_matrix(a):
             os.environ["TS_CSR_SHORT"] = old
 
 
+def _sell_matrix(a):
+    return _forced_matrix(a, "sell")
+
+
 CASES = [
     ("ragged", dict(m=3000, n=2000, seed=1)),
     ("wide", dict(m=500, n=40000, seed=2, max_row=200)),
     ("tall_short", dict(m=50000, n=300, seed=3, max_row=6, empty_frac=0.3)),
-    ("cap_rows", dict(m=4000, n=5000, seed=4, long_rows=((0, K_ST_CAP), (17, K_ST_CAP - 1),
-                                                         (3999, K_ST_CAP), (2000, 1000)))),
-    ("single_row", dict(m=1, n=3000, seed=5, max_row=K_ST_CAP, empty_frac=0.0)),
+    ("long_in_slice", dict(m=4001, n=5000, seed=4, long_rows=((0, LONG), (17, LONG - 1),
+                                                              (4000, LONG), (2000, 1000)))),
+    ("single_row", dict(m=1, n=3000, seed=5, max_row=LONG, empty_frac=0.0)),
+    ("all_empty_slices", dict(m=3000, n=700, seed=6, max_row=3, empty_frac=0.9)),
 ]
 
 
 @pytest.mark.parametrize("name,kw", CASES, ids=[c[0] for c in CASES])
-def test_stream_kernel_bitwise_scipy(name, kw):
+def test_sell_kernel_bitwise_scipy(name, kw):
     a = _ragged(**kw)
-    dm = _stream_matrix(a)
+    dm = _sell_matrix(a)
     rng = np.random.default_rng(99)
     v = rng.standard_normal(a.shape[1])
     w = rng.standard_normal(a.shape[0])
@@ -87,24 +93,16 @@ def test_stream_kernel_bitwise_scipy(name, kw):
         assert np.array_equal(dm.rmatvec(w), w @ a)
 
 
-def test_stream_kernel_cta_matches_warp_kernel():
-    """A whole CTA solve on the streamed plan matches the warp-kernel plan: both
-    add every row in scipy's order (bitwise products), only the fused scalar
-    reductions (phi, norms) group rows differently."""
+def test_sell_kernel_cta_matches_thread_kernel():
+    """A whole CTA solve on the sliced-ELL plan matches the thread-per-row CSR
+    plan: both add every row in scipy's order (bitwise products), only the
+    fused scalar reductions (phi, norms) group rows differently."""
     import paper_2304_12168_b200 as ts
     from paper_2304_12168_b200 import workloads as W
 
     w = W.convdiff_upwind(60)  # 3600 x 3600 five-point operator
-    dm_s = _stream_matrix(w.a)
-    old = os.environ.get("TS_CSR_SHORT")
-    os.environ["TS_CSR_SHORT"] = "warp"
-    try:
-        dm_w = ts.DeviceMatrix(w.a.copy())
-    finally:
-        if old is None:
-            del os.environ["TS_CSR_SHORT"]
-        else:
-            os.environ["TS_CSR_SHORT"] = old
+    dm_s = _sell_matrix(w.a)
+    dm_w = _forced_matrix(w.a.copy(), "thread")
     opts = ts.CenteringOptions(epsilon=1e-8, max_iters=60)
     rs = ts.centering_solve(dm_s, w.b, opts)
     rw = ts.centering_solve(dm_w, w.b, opts)
@@ -147,10 +145,10 @@ def test_pool_recycles_dense_and_csr():
             if s2.nnz != nnz:
                 continue
     v = rng.standard_normal(3000)
-    e1 = _stream_matrix(s1)
+    e1 = _sell_matrix(s1)
     assert np.array_equal(e1.matvec(v), s1 @ v)
     del e1
-    e2 = _stream_matrix(s2)
+    e2 = _sell_matrix(s2)  # recycled storage; the SELL tables are rebuilt
     assert np.array_equal(e2.matvec(v), s2 @ v)
     assert np.array_equal(e2.rmatvec(np.ones(4000)), np.ones(4000) @ s2)
 
@@ -173,28 +171,27 @@ def test_pinned_results_are_recycled():
     assert np.linalg.norm(a @ r.x - b) == pytest.approx(r.residual_norm, rel=1e-9, abs=1e-12)
 
 
-def test_prefetching_warp_kernel_bitwise_scipy():
-    """The prefetching short-row kernel (k_rows_warp_pf, opt-in
-    TS_CSR_SHORT=pf) on HBM-sized rows of >= 8 entries (C5's A^T v shape):
-    bitwise scipy in both orientations, incl. empty rows and rows spanning
-    several prefetch chunks."""
+def test_sell_is_the_default_for_hbm_sized_short_rows():
+    """Without overrides, HBM-sized short rows (nnz >= 2^21) take the
+    sliced-ELL plan in both orientations: bitwise scipy, incl. empty rows and
+    rows far longer than their slice neighbours (C5's A^T v shape: 10 random
+    entries per row of the transpose)."""
     import paper_2304_12168_b200 as ts
 
     a = _ragged(300_000, 20_000, seed=21, max_row=24, empty_frac=0.05,
                 long_rows=((5, 700), (299_999, 400), (150_000, 193)))
-    assert a.nnz >= (1 << 21) and a.nnz >= 8 * a.shape[0]
-    os.environ["TS_CSR_SHORT"] = "pf"
-    try:
-        dm = ts.DeviceMatrix(a)
-        lp = sparse.random_array((2000, 400_000), density=0.005, random_state=22, format="csr")
-        dm2 = ts.DeviceMatrix(lp)
-    finally:
-        del os.environ["TS_CSR_SHORT"]
+    assert a.nnz >= (1 << 21)
+    dm = ts.DeviceMatrix(a)
+    lp = sparse.random_array((2000, 400_000), density=0.005, random_state=22, format="csr")
+    dm2 = ts.DeviceMatrix(lp)
     rng = np.random.default_rng(8)
     v = rng.standard_normal(a.shape[1])
     assert np.array_equal(dm.matvec(v), a @ v)
     w = rng.standard_normal(lp.shape[0])
     assert np.array_equal(dm2.rmatvec(w), w @ lp)
+    # the LP pivot's c+ transform (v -> s * max(v, 0)) rides on the gathers
+    r = ts.nonnegative_feasibility(dm2, lp @ np.abs(rng.standard_normal(lp.shape[1])), eps=1e-9, max_iters=50)
+    assert r.iterations >= 1
 
 
 def test_thread_row_kernel_tails_bitwise_scipy():
@@ -214,34 +211,25 @@ def test_thread_row_kernel_tails_bitwise_scipy():
     assert np.array_equal(dm.rmatvec(w), w @ a)
 
 
-def test_split_dense_av_matches_fused():
-    """TS_DENSE_N=split (tile kernel + combine kernel, the persistent loop's
-    bodies) agrees with the default one-kernel dense A v to rounding: only
-    the order of the per-row sum over tile partials differs."""
+def test_dense_av_and_transposed_atv_alternate():
+    """Dense A v (one fused kernel) and A^T v of an L2-sized matrix (over a
+    transposed copy, PLAN_TRANS, with its own partial / counter layout next
+    to the A v pass's) stay correct when the two passes alternate: the
+    self-resetting group counters of one never leak into the other."""
     import paper_2304_12168_b200 as ts
 
     rng = np.random.default_rng(12)
     a = rng.standard_normal((2300, 1700))
-    os.environ["TS_DENSE_N"] = "split"
-    try:
-        d_split = ts.DeviceMatrix(a)
-    finally:
-        del os.environ["TS_DENSE_N"]
-    d_fused = ts.DeviceMatrix(a)
+    dm = ts.DeviceMatrix(a)
     v = rng.standard_normal(1700)
-    y1, y2, ref = d_split.matvec(v), d_fused.matvec(v), a @ v
-    scale = np.abs(a) @ np.abs(v)
-    assert np.all(np.abs(y1 - ref) <= 1e-13 * scale)
-    assert np.all(np.abs(y2 - ref) <= 1e-13 * scale)
-    # A^T v of this L2-sized matrix runs over a transposed copy (PLAN_TRANS)
-    # with its own partial / counter layout next to the A v pass's
     w = rng.standard_normal(2300)
-    for dm in (d_split, d_fused):
-        for _ in range(3):  # alternate the two passes: counters stay consistent
-            assert np.all(np.abs(dm.rmatvec(w) - a.T @ w) <= 1e-13 * (np.abs(a.T) @ np.abs(w)))
-            assert np.all(np.abs(dm.matvec(v) - ref) <= 1e-13 * scale)
+    ref = a @ v
+    scale = np.abs(a) @ np.abs(v)
+    for _ in range(3):
+        assert np.all(np.abs(dm.rmatvec(w) - a.T @ w) <= 1e-13 * (np.abs(a.T) @ np.abs(w)))
+        assert np.all(np.abs(dm.matvec(v) - ref) <= 1e-13 * scale)
     b = a @ np.ones(1700)
     opts = ts.CenteringOptions(epsilon=1e-10, max_iters=15)
-    r1, r2 = ts.centering_solve(d_split, b, opts), ts.centering_solve(d_fused, b, opts)
+    r1, r2 = ts.centering_solve(dm, b, opts), ts.centering_solve(ts.DeviceMatrix(a), b, opts)
     assert r1.iterations == r2.iterations
-    assert np.linalg.norm(r1.x - r2.x) <= 1e-9 * np.linalg.norm(r2.x)
+    assert np.array_equal(r1.x, r2.x)

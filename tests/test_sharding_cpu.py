@@ -57,6 +57,17 @@ def _worker(rank, world, port, case, outdir):
         hw = int(t.item())
         rows_ext, cols_ext = SM.shifted_blocks(rows, cols, c0, hw)
         out = SM.cta_row_sharded(rows_ext, cols_ext, hw, w.b[c0:c1], 1e-8, 40)
+    elif case in ("cta_tall", "ta_tall"):  # tall row blocks, n-vector all-reduce
+        from paper_2304_12168_b200.shard import row_block
+
+        rng = np.random.default_rng(13)
+        a = rng.standard_normal((300, 70))
+        b = a @ rng.standard_normal(70)
+        c0, c1 = column_range(300, world, rank)
+        if case == "cta_tall":
+            out = SM.cta_tall_sharded(row_block(a, c0, c1), b[c0:c1], 1e-8, 60)
+        else:
+            out = SM.ta_tall_sharded(row_block(a, c0, c1), b[c0:c1], 1e-8 * np.linalg.norm(b), 40)
     else:  # lp_sparse: the C5 family (cone stall)
         w = W.lp_columns(60, 3000, 10, seed=5)
         c0, c1 = column_range(w.a.shape[1], world, rank)
@@ -68,7 +79,8 @@ def _worker(rank, world, port, case, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["cta_dense", "ta_dense", "lp_sparse", "cta_rows_convdiff"])
+@pytest.mark.parametrize("case", ["cta_dense", "ta_dense", "lp_sparse", "cta_rows_convdiff",
+                                  "cta_tall", "ta_tall"])
 def test_sharded_decomposition_matches_oracle(case, tmp_path):
     import torch.multiprocessing as mp
 
@@ -80,6 +92,9 @@ def test_sharded_decomposition_matches_oracle(case, tmp_path):
                        join=True, start_method="spawn")
     parts = [np.load(os.path.join(tmp_path, f"{case}_{r}.npz")) for r in range(world)]
     x = np.concatenate([p["x"] for p in parts])
+    if case.endswith("_tall"):  # x is replicated on tall row blocks
+        assert np.array_equal(parts[0]["x"], parts[1]["x"])
+        x = parts[0]["x"]
     if case == "cta_dense":
         w = W.dense_lowrank(60, 240, 24, seed=3)
         ref = port.cta_solve(w.a, w.b, epsilon=1e-8, max_iters=200)
@@ -89,6 +104,12 @@ def test_sharded_decomposition_matches_oracle(case, tmp_path):
     elif case == "cta_rows_convdiff":
         w = W.convdiff_upwind(24, seed=2)
         ref = port.cta_solve(w.a, w.b, epsilon=1e-8, max_iters=40)
+    elif case.endswith("_tall"):
+        rng = np.random.default_rng(13)
+        a = rng.standard_normal((300, 70))
+        b = a @ rng.standard_normal(70)
+        ref = (port.cta_solve(a, b, epsilon=1e-8, max_iters=60) if case == "cta_tall" else
+               port.ta_adaptive(a, b, eps=1e-8 * np.linalg.norm(b), max_iters=40))
     else:
         w = W.lp_columns(60, 3000, 10, seed=5)
         ref = port.lp_feasibility(w.a, w.b, eps=1e-6 * np.linalg.norm(w.b), max_iters=1000)
