@@ -20,16 +20,19 @@ the per-step solve time.
   the timed solves by the library's per-class kernel timers (%globaltimer,
   earliest block start to the finishing block), algorithmic bytes
   8mn + 8(m+n) per launch, peak = MEASURED_PEAKS.json hbm_gbs.
-* cpu_baseline: the oracle port (same numpy/OpenBLAS calls as the reference)
-  on the host cores, bounded sample.
-* --impl reference: the reference's CPU algorithm (oracle port) timed for
-  K steps on the host; rank 0 only.
+* cpu_baseline / --impl reference: the REAL reference package (``trisolve``,
+  installed into baseline/_ref by ``pip install --target``; kind
+  "reference") through its public API on the host cores, rank 0 only,
+  bounded sample; the oracle port (same numpy/OpenBLAS/scipy calls) only
+  when baseline/_ref is absent (kind "port").  Both arms print the same
+  ``config`` dict.
 
 N > 1 (torchrun): ONE sharded solve over all ranks (strong scaling): column
 blocks (rank p holds A[:, p n/N : (p+1) n/N]; every A v is a fused
 fixed-rank-order all-reduce over NVLink peer memory), or for C4 row blocks
 (a halo exchange with each neighbour before every pass, scalar all-reduces);
-value = the solve's iterations / max time.
+value = the solve's iterations / max time.  Communicators are per process
+and each rank's block is sliced once, outside every timed region.
 """
 
 from __future__ import annotations
@@ -93,6 +96,41 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def load_reference():
+    """The reference package from baseline/_ref (None when not installed)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "trisolve")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import trisolve
+
+        return trisolve
+    except Exception:
+        return None
+
+
+def host_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"os_cpu_count": os.cpu_count(), "cpu_model": model, "blas_threads": blas_threads()}
+
+
+def config_dict(cfg):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": cfg["desc"], "step": "one full solve, reference stopping rule",
+            "l2": "no flush: matrix larger than L2" if cfg["gen"] in ("c2", "c4", "c5")
+                  else "no flush: L2-resident matrix (latency-bound config)"}
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -142,6 +180,10 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()  # the sampler is live before the timed region starts
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -181,16 +223,38 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- reference ---
-def run_oracle_step(cfg, w, bounded=False):
-    from oracle import port
-
+def run_cpu_step(cfg, w, bounded=False):
+    """One solve on the host: the real reference package when installed,
+    else the oracle port.  Returns (result dict, kind)."""
     bn = float(np.linalg.norm(w.b))
     cap = cfg["cpu_max_iters"] if bounded else cfg["max_iters"]
+    ref = load_reference()
+    if ref is not None:
+        if cfg["solver"] == "cta":
+            r = ref.centering_solve(w.a, w.b, ref.CenteringOptions(epsilon=cfg["eps"], max_iters=cap))
+        elif cfg["solver"] == "ta":
+            r = ref.solve_adaptive(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
+        else:
+            r = ref.nonnegative_feasibility(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
+        return {"status": r.status, "iterations": r.iterations}, "reference"
+    from oracle import port
+
     if cfg["solver"] == "cta":
-        return port.cta_solve(w.a, w.b, epsilon=cfg["eps"], max_iters=cap)
-    if cfg["solver"] == "ta":
-        return port.ta_adaptive(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
-    return port.lp_feasibility(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
+        out = port.cta_solve(w.a, w.b, epsilon=cfg["eps"], max_iters=cap)
+    elif cfg["solver"] == "ta":
+        out = port.ta_adaptive(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
+    else:
+        out = port.lp_feasibility(w.a, w.b, eps=cfg["eps"] * bn, max_iters=cap)
+    return out, "port"
+
+
+def cpu_sample_text(cfg, out, kind, cores, steps):
+    what = ("the reference package (baseline/_ref trisolve, public API)" if kind == "reference"
+            else "oracle/port.py (the reference's numpy/OpenBLAS/scipy calls)")
+    sparse_note = "; scipy sparse kernels are single-threaded" if cfg["gen"] in ("c3", "c4", "c5") else ""
+    return (f"{steps} solve(s) of the workload capped at {cfg['cpu_max_iters']} iterations "
+            f"(last: {out['iterations']} iterations, {out['status']}) with {what}, "
+            f"OpenBLAS {cores} threads{sparse_note}")
 
 
 def reference_arm(args, cfg):
@@ -198,12 +262,12 @@ def reference_arm(args, cfg):
     if rank != 0:
         return 0
     w = make_workload(cfg)
-    for _ in range(min(args.warmup, 1)):
-        run_oracle_step(cfg, w, bounded=True)
+    for _ in range(args.warmup):
+        run_cpu_step(cfg, w, bounded=True)
     iters = 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        out = run_oracle_step(cfg, w, bounded=True)
+        out, kind = run_cpu_step(cfg, w, bounded=True)
         iters += out["iterations"]
     dt = time.perf_counter() - t0
     val = iters / dt
@@ -212,14 +276,13 @@ def reference_arm(args, cfg):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "iterations/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded numpy, BASELINE.json formula)",
-        "config": {"workload": cfg["desc"], "step": "one full solve, reference stopping rule",
-                   "status": out["status"], "iterations_per_step": out["iterations"]},
-        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} solves capped at {cfg['cpu_max_iters']} "
-                                   f"iterations (oracle/port.py, numpy+OpenBLAS {cores} threads; "
-                                   "same calls as the reference)"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy, BASELINE.json formula; SURVEY.md Appendix A)",
+        "config": config_dict(cfg),
+        "solve": {"status": out["status"], "iterations_per_step": out["iterations"]},
+        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": kind,
+                         "sample": cpu_sample_text(cfg, out, kind, cores, args.steps),
+                         "host": host_info()},
         "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -228,6 +291,21 @@ def reference_arm(args, cfg):
 
 
 # ------------------------------------------------------------------- ours ---
+def make_operand(ts, w, part, dev, a_local=None, stream=None):
+    """The solve operand: a DeviceMatrix (N = 1) or this rank's shard built from
+    its pre-sliced block (`a_local` overrides the block with a pinned copy)."""
+    if part is None:
+        return ts.DeviceMatrix(w.a if a_local is None else a_local, device=dev, stream=stream)
+    from paper_2304_12168_b200 import shard as S
+
+    kind, blk = part
+    if kind == "rows":
+        rows, cols, hw = blk if a_local is None else a_local
+        return S.RowShardedMatrix(w.a, device=dev, blocks=(rows, cols, hw))
+    return S.ShardedMatrix(blk if a_local is None else a_local, device=dev, local=True,
+                           n_global=w.a.shape[1])
+
+
 def solve_once(ts, cfg, dm, b, bn):
     if cfg["solver"] == "cta":
         return ts.centering_solve(dm, b, ts.CenteringOptions(epsilon=cfg["eps"],
@@ -253,20 +331,22 @@ def ours_arm(args, cfg):
 
     w = make_workload(cfg)
     bn = float(np.linalg.norm(w.b))
-    if world > 1 and cfg["gen"] == "c4":
-        # row-block sharded solve (square banded C4): each rank owns rows and
-        # columns [r0, r1); a halo exchange with each neighbour before every pass
-        from paper_2304_12168_b200.shard import RowShardedMatrix
+    part = None
+    if world > 1:
+        # this rank's block, sliced once (the timed loops only upload it)
+        from paper_2304_12168_b200 import shard as S
 
-        dm = RowShardedMatrix(w.a, device=dev)
-    elif world > 1:
-        # column-sharded solve: each rank holds A[:, c0:c1]; A v is one fused
-        # fixed-rank-order all-reduce over NVLink peer memory per pass
-        from paper_2304_12168_b200.shard import ShardedMatrix
-
-        dm = ShardedMatrix(w.a, device=dev)
-    else:
-        dm = ts.DeviceMatrix(w.a, device=dev)
+        if cfg["gen"] == "c4":
+            # row-block sharded solve (square banded C4): each rank owns rows and
+            # columns [r0, r1); a halo exchange with each neighbour before every pass
+            rr = S.column_range(w.a.shape[0], world, rank)
+            part = ("rows", S.row_blocks(w.a, *rr))
+        else:
+            # column-sharded solve: each rank holds A[:, c0:c1]; A v is one fused
+            # fixed-rank-order all-reduce over NVLink peer memory per pass
+            cr = S.column_range(w.a.shape[1], world, rank)
+            part = ("columns", S.local_block(w.a, *cr))
+    dm = make_operand(ts, w, part, dev)
     b_dev = torch.from_numpy(w.b).to(f"cuda:{dev}")
 
     def barrier():
@@ -342,19 +422,17 @@ def ours_arm(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy, BASELINE.json formula; SURVEY.md Appendix A)",
-        "config": {"workload": cfg["desc"], "step": "one full solve, reference stopping rule",
-                   "status": results[-1].status, "iterations_per_step": results[-1].iterations,
-                   "time_to_tolerance_ms": float(np.median([r.device_ms for r in results])),
-                   "final_rel_residual": results[-1].residual_norm / bn,
-                   "l2": "no flush: matrix larger than L2" if cfg["gen"] in ("c2", "c4", "c5")
-                         else "L2-resident matrix (latency-bound config)",
-                   "parallelism": "single GPU" if world == 1 else
-                   (f"row-block sharded x{world} (halo exchange + scalar all-reduce over NVLink)"
-                    if cfg["gen"] == "c4" else
-                    f"column-sharded x{world} (fused fixed-order all-reduce over NVLink)")},
+        "config": config_dict(cfg),
+        "solve": {"status": results[-1].status, "iterations_per_step": results[-1].iterations,
+                  "time_to_tolerance_ms": float(np.median([r.device_ms for r in results])),
+                  "final_rel_residual": results[-1].residual_norm / bn},
+        "parallelism": "single GPU" if world == 1 else
+        (f"row-block sharded x{world} (halo exchange + scalar all-reduce over NVLink)"
+         if cfg["gen"] == "c4" else
+         f"column-sharded x{world} (fused fixed-order all-reduce over NVLink)"),
         "roofline": roofline,
         "kernel_breakdown": breakdown,
         "gpu_launches": int(launches),
@@ -362,7 +440,7 @@ def ours_arm(args, cfg):
     }
 
     if not args.no_e2e:
-        line["e2e"] = e2e_measure(ts, cfg, w, bn, args, dev, world)
+        line["e2e"] = e2e_measure(ts, cfg, w, bn, args, dev, world, part)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, w)
     if rank == 0:
@@ -372,7 +450,7 @@ def ours_arm(args, cfg):
     return 0
 
 
-def e2e_measure(ts, cfg, w, bn, args, dev, world):
+def e2e_measure(ts, cfg, w, bn, args, dev, world, part=None):
     """Same metric through the public API with pinned HOST buffers: every
     step uploads A and b and reads x (+ trace) back."""
     import scipy.sparse as sp
@@ -385,43 +463,46 @@ def e2e_measure(ts, cfg, w, bn, args, dev, world):
         out[...] = arr
         return out, t
 
-    keep = []
-    if sp.issparse(w.a):
-        csr = w.a
+    def pinned_csr(csr):
         data, t1 = pinned_copy(csr.data)
         ind, t2 = pinned_copy(csr.indices.astype(np.int32))
         ptr, t3 = pinned_copy(csr.indptr.astype(np.int32))
-        keep += [t1, t2, t3]
-        a_host = sp.csr_array((data, ind, ptr), shape=csr.shape)
-        a_host.indices = ind
-        a_host.indptr = ptr
-        h2d = data.nbytes + ind.nbytes + ptr.nbytes
+        keep.extend([t1, t2, t3])
+        out = sp.csr_array((data, ind, ptr), shape=csr.shape)
+        out.indices = ind
+        out.indptr = ptr
+        return out, data.nbytes + ind.nbytes + ptr.nbytes
+
+    def pinned_any(a):
+        if sp.issparse(a):
+            return pinned_csr(a)
+        arr, t = pinned_copy(np.ascontiguousarray(a))
+        keep.append(t)
+        return arr, arr.nbytes
+
+    keep = []
+    if part is None:
+        a_host, h2d = pinned_any(w.a)
+    elif part[0] == "rows":  # this rank's rows and columns (as rows of A^T), with the halo width
+        rows, cols, hw = part[1]
+        (r_h, nb1), (c_h, nb2) = pinned_csr(rows), pinned_csr(cols)
+        a_host, h2d = (r_h, c_h, hw), nb1 + nb2
     else:
-        a_host, t1 = pinned_copy(w.a)
-        keep.append(t1)
-        h2d = a_host.nbytes
+        a_host, h2d = pinned_any(part[1])
     b_host, t4 = pinned_copy(w.b)
     keep.append(t4)
-    h2d += b_host.nbytes
+    h2d += b_host.nbytes  # per rank; the line reports the job total below
     steps = max(1, min(args.steps, 10))
-
     if world > 1:
-        from paper_2304_12168_b200.shard import ShardedMatrix, column_range, local_block
-
-        c0, c1 = column_range(w.a.shape[1], world, torch.distributed.get_rank())
-        a_host = local_block(a_host, c0, c1)
-        h2d = h2d  # job total: the shards together upload A once per step
+        hb = torch.tensor([h2d], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(hb)
+        h2d = int(hb.item())
 
     copy_stream = torch.cuda.Stream(device=dev)  # non-blocking: uploads overlap solves
 
     def upload():
-        if world > 1 and cfg["gen"] == "c4":
-            from paper_2304_12168_b200.shard import RowShardedMatrix
-
-            return RowShardedMatrix(w.a, device=dev)
-        if world > 1:
-            return ShardedMatrix(a_host, device=dev, local=True, n_global=w.a.shape[1])
-        return ts.DeviceMatrix(a_host, device=dev, stream=copy_stream)
+        return make_operand(ts, w, part, dev, a_local=a_host,
+                            stream=copy_stream if world == 1 else None)
 
     def run(n_steps, pipelined):
         """n_steps x (upload A and b, solve, read x and the trace back); with
@@ -477,14 +558,14 @@ def e2e_measure(ts, cfg, w, bn, args, dev, world):
 
 
 def cpu_baseline(cfg, w):
+    run_cpu_step(cfg, w, bounded=True)  # warm-up (imports, page-in)
     t0 = time.perf_counter()
-    out = run_oracle_step(cfg, w, bounded=True)
+    out, kind = run_cpu_step(cfg, w, bounded=True)
     dt = time.perf_counter() - t0
     cores = blas_threads()
     return {"value": out["iterations"] / dt, "unit": "iterations/s", "cores": cores,
-            "kind": "port",
-            "sample": f"1 full solve ({out['iterations']} iterations, {out['status']}) with "
-                      f"oracle/port.py (numpy/OpenBLAS, {cores} threads; the reference's calls)"}
+            "kind": kind, "sample": cpu_sample_text(cfg, out, kind, cores, 1),
+            "host": host_info()}
 
 
 def main():

@@ -287,11 +287,14 @@ class RowShardedMatrix(_Shard):
 
     layout = "rows"
 
-    def __init__(self, a, group=None, device: int | None = None):
+    def __init__(self, a, group=None, device: int | None = None, blocks=None):
+        """``blocks``: this rank's ``row_blocks(a, r0, r1)`` already sliced
+        (rows, columns as rows of A^T, halo width) — a caller building shards
+        repeatedly slices once."""
         ctx = _DistCtx(group, device)
         n = int(a.shape[0])
         rr = column_range(n, ctx.world, ctx.rank)
-        rows, cols, hw = row_blocks(a, *rr)
+        rows, cols, hw = blocks if blocks is not None else row_blocks(a, *rr)
         hw, neg_min_block = ctx.max_int([hw, -(rr[1] - rr[0])])
         _check_halo(hw, -neg_min_block)
         dm = _pair_matrix(rows, cols, rr, hw, ctx.device)
