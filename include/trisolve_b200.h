@@ -47,7 +47,7 @@ extern "C" {
 #define TS_API
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2
 
 typedef struct ts_matrix ts_matrix; /* opaque; immutable after creation */
 typedef struct ts_comm ts_comm;     /* column-sharding communicator (one per rank) */
@@ -146,6 +146,11 @@ typedef struct {
   int32_t accel_patience;
   double accel_ratio;
   const double* x_start; /* NULL: start = "zero"; else the random start vector (n) */
+  /* 1: the operator is the implicit normal matrix A^T A (n x n) of the handle
+   * (the reference's GramProduct, linalg.py:93-114): every operator apply is
+   * the pass pair A^T (A v); b, x and the Krylov vectors live in n-space. */
+  int32_t normal_operand;
+  int32_t reserved;
 } ts_cta_options;
 
 typedef struct {
@@ -254,6 +259,10 @@ TS_API int ts_norm2(const double* v, int64_t len, double* out, void* stream);
  * the honest-residual step of every driver (triangle.py:84-89, hybrid.py:102-104) */
 TS_API int ts_residual(const ts_matrix* a, const double* x, const double* b, double* r_out,
                        double* r_norm, double* atr_norm, void* stream);
+/* ts_residual for the implicit normal operator G = A^T A of the handle (the
+ * reference's GramProduct): r = b - G x (n), ||r||, ||G r||. */
+TS_API int ts_gram_residual(const ts_matrix* a, const double* x, const double* b, double* r_out,
+                            double* r_norm, double* gr_norm, void* stream);
 TS_API int ts_dot(const double* u, const double* v, int64_t len, double* out, void* stream);
 
 /* ---- CTA pieces ------------------------------------------------------------ */

@@ -16,10 +16,12 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(_HERE, "_lib", "libtrisolve_b200.so")
 
+ABI_VERSION = 2  # TS_ABI_VERSION of include/trisolve_b200.h
+
 EXPORTS = (
     "ts_abi_version", "ts_last_error", "ts_device_count",
     "ts_matrix_create_dense", "ts_matrix_create_csr", "ts_matrix_destroy", "ts_matrix_info",
-    "ts_matvec", "ts_rmatvec", "ts_gram_matvec", "ts_norm2", "ts_dot", "ts_residual",
+    "ts_matvec", "ts_rmatvec", "ts_gram_matvec", "ts_norm2", "ts_dot", "ts_residual", "ts_gram_residual",
     "ts_moments", "ts_hankel_min_norm", "ts_cta_step", "ts_time_pass",
     "ts_cta_solve", "ts_ta_adaptive", "ts_ta_in_ball", "ts_lp_feasibility",
     "ts_comm_create", "ts_comm_connect", "ts_comm_destroy", "ts_matrix_set_shard",
@@ -67,7 +69,7 @@ class CtaOptions(C.Structure):
                 ("max_iters", C.c_int64), ("enhanced", C.c_int32), ("known_solvable", C.c_int32),
                 ("recheck_every", C.c_int64), ("rcond", C.c_double), ("accelerate", C.c_int32),
                 ("accel_patience", C.c_int32), ("accel_ratio", C.c_double),
-                ("x_start", C.c_void_p)]
+                ("x_start", C.c_void_p), ("normal_operand", C.c_int32), ("reserved", C.c_int32)]
 
 
 class TaOptions(C.Structure):
@@ -116,6 +118,7 @@ def _declare(lib):
         "ts_norm2": ([_P, _I64, _P, _P], C.c_int),
         "ts_dot": ([_P, _P, _I64, _P, _P], C.c_int),
         "ts_residual": ([_P, _P, _P, _P, C.POINTER(_D), C.POINTER(_D), _P], C.c_int),
+        "ts_gram_residual": ([_P, _P, _P, _P, C.POINTER(_D), C.POINTER(_D), _P], C.c_int),
         "ts_moments": ([_P, _I32, _P, _I32, _P, _P, _P, _P], C.c_int),
         "ts_hankel_min_norm": ([_P, _I32, _I32, _D, _P, _P], C.c_int),
         "ts_cta_step": ([_P, _I32, _P, _P, _I32, _D, _P, _P, C.POINTER(_I32), C.POINTER(_D),
@@ -159,6 +162,9 @@ def load_library(path: str = LIB_PATH):
                     "(run `make` or __graft_entry__.build()); there is no CPU fallback")
             lib = C.CDLL(path)
             _declare(lib)
+            if lib.ts_abi_version() != ABI_VERSION:  # structs would be misread: refuse a stale build
+                raise RuntimeError(f"{path} implements ABI {lib.ts_abi_version()}, this package "
+                                   f"expects {ABI_VERSION}: rebuild it (`make`)")
             _lib = lib
     return _lib
 

@@ -23,6 +23,7 @@ from .linalg import (
     H_MODE_SYMMETRIC,
     HOperator,
     as_device_matrix,
+    dot,
     local_rows,
     local_slice,
     norm2,
@@ -166,6 +167,31 @@ def centering_step(state: CenteringState, t: int, h: HOperator, a, b) -> Centeri
     return CenteringState(x_out, r_out, state.iterations + 1, state.schedule_pos, state.trace)
 
 
+def first_order_probe(x, r, h: HOperator, j_max: int, threshold: float, hr=None, atr=None):
+    """Short first-order orbit search (centering.py:227-251): follow
+    ``y <- y - (y^T H y / y^T H^2 y) H y`` for up to ``j_max - 1``
+    compositions; return ``(x_hat, j)`` for the first image with
+    ``|y^T H y| <= threshold``, else None.  The H-applications and inner
+    products run on the device (``centering_solve(enhanced=True)`` runs the
+    same probe inside its device loop)."""
+    y = np.asarray(r, dtype=np.float64)
+    x_hat = np.asarray(x, dtype=np.float64).copy()
+    if hr is None:
+        hr, atr = h.apply_with_transpose(y)
+    for j in range(1, j_max):
+        phi1 = dot(y, hr)
+        phi2 = dot(hr, hr)
+        if phi2 == 0.0:
+            return None  # orbit terminated without triggering
+        alpha = phi1 / phi2
+        x_hat += alpha * (atr if h.mode == H_MODE_GRAM else y)
+        y = y - alpha * hr
+        hr, atr = h.apply_with_transpose(y)
+        if abs(dot(y, hr)) <= threshold:
+            return x_hat, j
+    return None
+
+
 def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResult:
     """Solve ``Ax = b`` (or its normal equation) by cycled centering steps
     (centering.py:263-358), entirely on the device."""
@@ -183,8 +209,8 @@ def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResul
     if opts.t_max > DEVICE_T_MAX:
         raise ValueError(f"t_max={opts.t_max} exceeds the device limit {DEVICE_T_MAX}")
     dm, gram = as_device_matrix(a)
-    if gram:
-        raise TypeError("centering_solve on a GramProduct operator is not supported on the device")
+    # gram: `a` is a GramProduct, the implicit normal matrix A^T A of dm (the
+    # device applies it as the pass pair A^T (A v); centering.py:278)
     n_local = dm.shape[1]  # == n unless `a` is a column-sharded ShardedMatrix
     x_start = None
     if opts.start == "random":
@@ -202,6 +228,7 @@ def centering_solve(a, b, options: CenteringOptions | None = None) -> SolveResul
     o.accel_patience = int(opts.accel_patience)
     o.accel_ratio = float(opts.accel_ratio)
     o.x_start = x_start.ctypes.data if x_start is not None else None
+    o.normal_operand = int(bool(gram))
     buf, cap = trace_buffer(opts.max_iters)
     x = N.pinned_empty(n_local)
     res = N.Result()

@@ -637,86 +637,128 @@ struct CtaArgs {
   double accel_ratio = 0.95;
   const double* x_start = nullptr;
   int enhanced = 0;
+  int normal = 0;  // operator = A^T A of the handle (GramProduct)
 };
 
-static int cta_alloc(Instance* I, const Mat& M, int t_max, int gram, int enhanced = 0) {
+// The pass that applies an operand of the CTA: A itself, or the implicit
+// normal matrix G = A^T A (the reference's GramProduct, linalg.py:93-114),
+// applied as A v -> t1, then A^T t1 with the real epilogue; G is symmetric,
+// so G^T v = G v.  The store pass carries the outer epilogue's activity
+// predicate, so an inactive pair skips both halves alike.
+template <class Epi>
+struct EpiTmpFor : EpiBase {
+  static constexpr int K = 1;
+  Epi e;
+  double* y = nullptr;
+  __device__ bool active() const { return e.active(); }
+  __device__ void idle() const {}
+  __device__ void elem(int64_t i, double v, double (&)[K]) const { y[i] = v; }
+  __device__ void finish(double (&)[K]) const {}
+};
+
+struct CtaOp {
+  const Mat& M;
+  const Instance* I;
+  int normal;
+  int64_t mo() const { return normal ? M.n : M.m; }  // operator rows (b-space)
+  int64_t no() const { return M.n; }                 // operator columns (x-space)
+  template <class Epi>
+  int apply(int trans, const double* v, const Epi& e, cudaStream_t s) const {
+    if (!normal) return pass(M, trans, v, XS{}, e, I->wk, s);
+    EpiTmpFor<Epi> t;
+    t.st = e.st;
+    t.e = e;
+    t.y = I->t1;
+    TS_CHECK(pass(M, 0, v, XS{}, t, I->wk, s));
+    return pass(M, 1, I->t1, XS{}, e, I->wk, s);
+  }
+  template <class Epi>
+  int N(const double* v, const Epi& e, cudaStream_t s) const { return apply(0, v, e, s); }
+  template <class Epi>
+  int T(const double* v, const Epi& e, cudaStream_t s) const { return apply(1, v, e, s); }
+};
+
+static int cta_alloc(Instance* I, const Mat& M, int t_max, int gram, int enhanced = 0, int normal = 0) {
+  const int64_t mo = normal ? M.n : M.m, no = M.n;
   memset(&I->kp, 0, sizeof(I->kp));
-  for (int i = 0; i <= t_max; ++i) TS_CHECK(I->alloc(&I->kp.p[i], M.m));
+  for (int i = 0; i <= t_max; ++i) TS_CHECK(I->alloc(&I->kp.p[i], mo));
   if (gram)
-    for (int i = 0; i < t_max; ++i) TS_CHECK(I->alloc(&I->kp.q[i], M.n));
-  TS_CHECK(I->alloc(&I->b, M.m));
-  TS_CHECK(I->alloc(&I->x, M.n));
-  TS_CHECK(I->alloc(&I->xs, M.n));
-  TS_CHECK(I->alloc(&I->fr, M.m));
+    for (int i = 0; i < t_max; ++i) TS_CHECK(I->alloc(&I->kp.q[i], no));
+  TS_CHECK(I->alloc(&I->b, mo));
+  TS_CHECK(I->alloc(&I->x, no));
+  TS_CHECK(I->alloc(&I->xs, no));
+  TS_CHECK(I->alloc(&I->fr, mo));
+  if (normal) TS_CHECK(I->alloc(&I->t1, M.m));
   if (enhanced) {
-    TS_CHECK(I->alloc(&I->pp.y, M.m));
-    TS_CHECK(I->alloc(&I->pp.hy, M.m));
-    TS_CHECK(I->alloc(&I->pp.aty, M.n));
-    TS_CHECK(I->alloc(&I->pp.xh, M.n));
-    TS_CHECK(I->alloc(&I->pp.fr2, M.m));
+    TS_CHECK(I->alloc(&I->pp.y, mo));
+    TS_CHECK(I->alloc(&I->pp.hy, mo));
+    TS_CHECK(I->alloc(&I->pp.aty, no));
+    TS_CHECK(I->alloc(&I->pp.xh, no));
+    TS_CHECK(I->alloc(&I->pp.fr2, mo));
   }
   return 0;
 }
 
 // enhanced probe steps 1..npairs-1 (centering.py:240-250), after the moments
-static int cta_probe_kernels(const Mat& M, const Instance* I, int npairs, int gram, cudaStream_t s) {
+static int cta_probe_kernels(const CtaOp& op, const Instance* I, int npairs, int gram, cudaStream_t s) {
+  const Mat& M = op.M;
   for (int j = 1; j < npairs; ++j) {
     EpiProbeUpd eu;
-    eu.st = I->ds; eu.kp = I->kp; eu.pp = I->pp; eu.x = I->x; eu.m = M.m; eu.n = M.n;
+    eu.st = I->ds; eu.kp = I->kp; eu.pp = I->pp; eu.x = I->x; eu.m = op.mo(); eu.n = op.no();
     eu.gram = gram; eu.j = j;
-    TS_CHECK(vecpass(M, std::max(M.m, M.n), eu, I->wk, s));
+    TS_CHECK(vecpass(M, std::max(op.mo(), op.no()), eu, I->wk, s));
     EpiProbeN en;
     en.st = I->ds; en.y = I->pp.y; en.hy = I->pp.hy; en.j = j;
     if (gram) {
       EpiProbeT et;
       et.st = I->ds; et.aty = I->pp.aty; et.j = j;
-      TS_CHECK(pass(M, 1, I->pp.y, XS{}, et, I->wk, s));
-      TS_CHECK(pass(M, 0, I->pp.aty, XS{}, en, I->wk, s));
+      TS_CHECK(op.T(I->pp.y, et, s));
+      TS_CHECK(op.N(I->pp.aty, en, s));
     } else {
-      TS_CHECK(pass(M, 0, I->pp.y, XS{}, en, I->wk, s));
+      TS_CHECK(op.N(I->pp.y, en, s));
     }
   }
   return 0;
 }
 
 // stepped vs refined normal residual, adopt x_hat if it wins (centering.py:335-343)
-static int cta_probe_finish(const Mat& M, const Instance* I, cudaStream_t s) {
+static int cta_probe_finish(const CtaOp& op, const Instance* I, cudaStream_t s) {
   EpiProbeR r1;
   r1.st = I->ds; r1.b = I->b; r1.fr = I->fr;
-  TS_CHECK(pass(M, 0, I->x, XS{}, r1, I->wk, s));
+  TS_CHECK(op.N(I->x, r1, s));
   EpiProbeNR n1;
   n1.st = I->ds; n1.which = 0;
-  TS_CHECK(pass(M, 1, I->fr, XS{}, n1, I->wk, s));
+  TS_CHECK(op.T(I->fr, n1, s));
   EpiProbeR r2;
   r2.st = I->ds; r2.b = I->b; r2.fr = I->pp.fr2;
-  TS_CHECK(pass(M, 0, I->pp.xh, XS{}, r2, I->wk, s));
+  TS_CHECK(op.N(I->pp.xh, r2, s));
   EpiProbeNR n2;
   n2.st = I->ds; n2.which = 1;
-  TS_CHECK(pass(M, 1, I->pp.fr2, XS{}, n2, I->wk, s));
+  TS_CHECK(op.T(I->pp.fr2, n2, s));
   EpiProbeTake et;
   et.st = I->ds; et.xh = I->pp.xh; et.fr2 = I->pp.fr2; et.x = I->x; et.r = I->kp.p[0];
-  et.m = M.m; et.n = M.n;
-  return vecpass(M, std::max(M.m, M.n), et, I->wk, s);
+  et.m = op.mo(); et.n = op.no();
+  return vecpass(op.M, std::max(op.mo(), op.no()), et, I->wk, s);
 }
 
 // moments pairs for orders 1..npairs (predicated on state t); `solve_last`
 // makes the pair that equals the state's t run the Hankel solves
-static int cta_pairs(const Mat& M, const Instance* I, int npairs, int gram, int solve_last,
+static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, int solve_last,
                      cudaStream_t s) {
   for (int i = 1; i <= npairs; ++i) {
     if (gram) {
       EpiCtaQ eq;
       eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i;
-      TS_CHECK(pass(M, 1, I->kp.p[i - 1], XS{}, eq, I->wk, s));
+      TS_CHECK(op.T(I->kp.p[i - 1], eq, s));
       EpiCtaP ep;
       ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
       ep.with_solve = solve_last;
-      TS_CHECK(pass(M, 0, I->kp.q[i - 1], XS{}, ep, I->wk, s));
+      TS_CHECK(op.N(I->kp.q[i - 1], ep, s));
     } else {
       EpiCtaP ep;
       ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
       ep.with_solve = solve_last;
-      TS_CHECK(pass(M, 0, I->kp.p[i - 1], XS{}, ep, I->wk, s));
+      TS_CHECK(op.N(I->kp.p[i - 1], ep, s));
     }
   }
   return 0;
@@ -724,26 +766,30 @@ static int cta_pairs(const Mat& M, const Instance* I, int npairs, int gram, int 
 
 // one CTA step of at most `npairs` pairs: moments (+ Hankel in the last pair's
 // finisher), candidate norms / retry rule, fused r / x update (tail)
-static int cta_step_kernels(const Mat& M, const Instance* I, int npairs, int gram, cudaStream_t s,
+static int cta_step_kernels(const CtaOp& op, const Instance* I, int npairs, int gram, cudaStream_t s,
                             cudaGraphConditionalHandle h, int use, int enhanced = 0) {
-  TS_CHECK(cta_pairs(M, I, npairs, gram, 1, s));
-  if (enhanced) TS_CHECK(cta_probe_kernels(M, I, npairs, gram, s));
+  TS_CHECK(cta_pairs(op, I, npairs, gram, 1, s));
+  if (enhanced) TS_CHECK(cta_probe_kernels(op, I, npairs, gram, s));
+  const int64_t mo = op.mo(), no = op.no();
   EpiCtaCand ecd;
-  ecd.st = I->ds; ecd.kp = I->kp; ecd.m = M.m;
-  TS_CHECK(vecpass(M, M.m, ecd, I->wk, s));
+  ecd.st = I->ds; ecd.kp = I->kp; ecd.m = mo;
+  TS_CHECK(vecpass(op.M, mo, ecd, I->wk, s));
   EpiCtaUpd eu;
-  eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = M.m;
-  eu.n = M.n; eu.gram = gram;
-  return vecpass(M, std::max(M.m, M.n), eu, I->wk, s);
+  eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = mo;
+  eu.n = no; eu.gram = gram;
+  return vecpass(op.M, std::max(mo, no), eu, I->wk, s);
 }
 
 static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double* x_out,
                      ts_trace_row* trace, int64_t trace_cap, ts_result* res, cudaStream_t st) {
-  const int key[4] = {2, a.gram, a.t_max, a.enhanced};
+  const int key[4] = {2 + 16 * a.normal, a.gram, a.t_max, a.enhanced};
   InstanceLease lease(M);
-  TS_CHECK(acquire(M, key, [&](Instance* I) { return cta_alloc(I, M, a.t_max, a.gram, a.enhanced); },
-                   &lease.I));
+  TS_CHECK(acquire(M, key, [&](Instance* I) {
+    return cta_alloc(I, M, a.t_max, a.gram, a.enhanced, a.normal);
+  }, &lease.I));
   Instance* I = lease.I;
+  const CtaOp op{M, I, a.normal};
+  const int64_t mo = op.mo(), no = op.no();
   SolveCtx c(M, st, I);
   SolveState s0;
   memset(&s0, 0, sizeof(s0));
@@ -758,31 +804,31 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   s0.accel_patience = a.accel_patience;
   s0.accel_ratio = a.accel_ratio;
   s0.rcond = a.rcond;
-  s0.a_fro = M.fro;
-  s0.m_rows = M.comm ? M.m_global : M.m;
-  s0.n_cols = M.comm ? M.n_global : M.n;
+  s0.a_fro = a.normal ? M.fro * M.fro : M.fro;  // ||A^T A||_F as the reference's GramProduct reports it
+  s0.m_rows = M.comm ? M.m_global : mo;
+  s0.n_cols = M.comm ? M.n_global : no;
   s0.warm = 1;
   s0.enhanced = a.enhanced;
   s0.probe_done = 1;
   TS_CHECK(c.init(s0, trace, trace_cap));
   SolveState* ds = I->ds;
   const Work& wk = I->wk;
-  TS_CHECK(I->stage_in(I->b, b_in, M.m, st));
+  TS_CHECK(I->stage_in(I->b, b_in, mo, st));
   if (a.x_start) {
-    TS_CHECK(I->stage_in(I->xs, a.x_start, M.n, st));
+    TS_CHECK(I->stage_in(I->xs, a.x_start, no, st));
     EpiCopyWarm ec;
     ec.st = ds; ec.src = I->xs; ec.dst = I->x;
-    TS_CHECK(vecpass(M, M.n, ec, wk, st));
+    TS_CHECK(vecpass(M, no, ec, wk, st));
     EpiCtaInitR ei;
     ei.st = ds; ei.b = I->b; ei.r = I->kp.p[0];
-    TS_CHECK(pass(M, 0, I->x, XS{}, ei, wk, st));
+    TS_CHECK(op.N(I->x, ei, st));
   } else {
     EpiCtaInit ei;
-    ei.st = ds; ei.b = I->b; ei.r = I->kp.p[0]; ei.x = I->x; ei.m = M.m; ei.n = M.n;
-    TS_CHECK(vecpass(M, std::max(M.m, M.n), ei, wk, st));
+    ei.st = ds; ei.b = I->b; ei.r = I->kp.p[0]; ei.x = I->x; ei.m = mo; ei.n = no;
+    TS_CHECK(vecpass(M, std::max(mo, no), ei, wk, st));
   }
   BodyFn body = [&](cudaStream_t s) -> int {
-    return cta_step_kernels(M, I, a.t_max, a.gram, s, 0, 0, a.enhanced);
+    return cta_step_kernels(op, I, a.t_max, a.gram, s, 0, 0, a.enhanced);
   };
   // graph body: [head: switch = t - 1] -> SWITCH{order 1 .. t_max}: each case
   // launches exactly its t pairs + candidate + update
@@ -798,30 +844,30 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     }));
     for (int k = 0; k < a.t_max; ++k)
       TS_CHECK(capture_into(cap, cases[k], [&](cudaStream_t s) -> int {
-        return cta_step_kernels(M, I, k + 1, a.gram, s, hw, 1, a.enhanced);
+        return cta_step_kernels(op, I, k + 1, a.gram, s, hw, 1, a.enhanced);
       }));
     return 0;
   };
   auto maint = [&](cudaStream_t s) -> int {
-    if (c.hs->maint == MAINT_PROBE) return cta_probe_finish(M, I, s);
+    if (c.hs->maint == MAINT_PROBE) return cta_probe_finish(op, I, s);
     EpiNormTo en;
-    en.st = ds; en.v = I->x; en.len = M.n; en.what = 1;
-    TS_CHECK(vecpass(M, M.n, en, wk, s));
+    en.st = ds; en.v = I->x; en.len = no; en.what = 1;
+    TS_CHECK(vecpass(M, no, en, wk, s));
     EpiCtaRecheck er;
     er.st = ds; er.b = I->b; er.r = I->kp.p[0];
-    return pass(M, 0, I->x, XS{}, er, wk, s);
+    return op.N(I->x, er, s);
   };
   TS_CHECK(c.run(body, gbody, maint));
   if (!c.hs->trivial) {
     EpiFinalR efr;
     efr.st = ds; efr.b = I->b; efr.fr = I->fr;
-    TS_CHECK(pass(M, 0, I->x, XS{}, efr, wk, st));
+    TS_CHECK(op.N(I->x, efr, st));
     EpiFinalNR enr;
     enr.st = ds; enr.out = nullptr;
-    TS_CHECK(pass(M, 1, I->fr, XS{}, enr, wk, st));
+    TS_CHECK(op.T(I->fr, enr, st));
   }
   TS_CHECK(c.read_state());
-  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, M.n * sizeof(double), cudaMemcpyDefault, st));
+  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, no * sizeof(double), cudaMemcpyDefault, st));
   fill_result(*c.hs, res);
   TS_CHECK(c.finish_timing(res));
   TS_CUDA(cudaStreamSynchronize(st));
@@ -936,39 +982,60 @@ struct EpiResid {
   __device__ void finish(double (&red)[K]) const { *out = sqrt(red[0]); }
 };
 
-int ts_residual(const ts_matrix* A, const double* x, const double* b, double* r_out,
-                double* r_norm, double* atr_norm, void* stream) {
+// r = b - Op x, ||r||, ||Op^T r|| for Op = A (normal = 0) or the implicit
+// normal matrix A^T A (normal = 1; symmetric, so Op^T r = A^T (A r))
+static int residual_impl(const ts_matrix* A, int normal, const double* x, const double* b, double* r_out,
+                         double* r_norm, double* atr_norm, void* stream) {
   TS_CHECK_HANDLE(A);
   if (!x || !b) TS_INVAL("null argument");
   if (A->comm) TS_INVAL("not supported on a column-sharded matrix");
   DeviceGuard g(A->dev);
   cudaStream_t st = (cudaStream_t)stream;
+  const int64_t mo = normal ? A->n : A->m, no = A->n;
   double hn[2] = {0.0, 0.0};
   {
     Arena ar(st);
     Work wk;
     TS_CHECK(make_work(ar, work_blocks(A->sms), &wk, A->npart));
-    double *dx, *db, *dr, *dn, *dt;
-    TS_CHECK(stage_in(ar, x, A->n, &dx));
-    TS_CHECK(stage_in(ar, b, A->m, &db));
-    TS_CHECK(ar.get(&dr, A->m));
-    TS_CHECK(ar.get(&dt, A->n));
+    double *dx, *db, *dr, *dn, *dt, *dm = nullptr;
+    TS_CHECK(stage_in(ar, x, no, &dx));
+    TS_CHECK(stage_in(ar, b, mo, &db));
+    TS_CHECK(ar.get(&dr, mo));
+    TS_CHECK(ar.get(&dt, no));
     TS_CHECK(ar.get(&dn, 2));
+    if (normal) TS_CHECK(ar.get(&dm, A->m));
+    auto apply = [&](int trans, const double* v, auto epi) -> int {
+      if (!normal) return pass(*A, trans, v, XS{}, epi, wk, st);
+      EpiStore es;
+      es.y = dm;
+      TS_CHECK(pass(*A, 0, v, XS{}, es, wk, st));
+      return pass(*A, 1, dm, XS{}, epi, wk, st);
+    };
     EpiResid er{db, dr, dn};
-    TS_CHECK(pass(*A, 0, dx, XS{}, er, wk, st));
+    TS_CHECK(apply(0, dx, er));
     if (atr_norm) {
       EpiStore es;
       es.y = dt;
       es.sq = dn + 1;
-      TS_CHECK(pass(*A, 1, dr, XS{}, es, wk, st));
+      TS_CHECK(apply(1, dr, es));
     }
-    if (r_out) TS_CUDA(cudaMemcpyAsync(r_out, dr, A->m * sizeof(double), cudaMemcpyDefault, st));
+    if (r_out) TS_CUDA(cudaMemcpyAsync(r_out, dr, mo * sizeof(double), cudaMemcpyDefault, st));
     TS_CUDA(cudaMemcpyAsync(hn, dn, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     TS_CUDA(cudaStreamSynchronize(st));
   }
   if (r_norm) *r_norm = hn[0];
   if (atr_norm) *atr_norm = sqrt(hn[1]);
   return 0;
+}
+
+int ts_residual(const ts_matrix* A, const double* x, const double* b, double* r_out,
+                double* r_norm, double* atr_norm, void* stream) {
+  return residual_impl(A, 0, x, b, r_out, r_norm, atr_norm, stream);
+}
+
+int ts_gram_residual(const ts_matrix* A, const double* x, const double* b, double* r_out,
+                     double* r_norm, double* gr_norm, void* stream) {
+  return residual_impl(A, 1, x, b, r_out, r_norm, gr_norm, stream);
 }
 
 static int dot_impl(const double* u, const double* v, int64_t len, double* out, int sq,
@@ -1055,7 +1122,7 @@ int ts_moments(const ts_matrix* A, int32_t h_mode, const double* r, int32_t t, d
   s0.gram = gram;
   TS_CHECK(c.init(s0, nullptr, 0));
   TS_CUDA(cudaMemcpyAsync(I->kp.p[0], r, A->m * sizeof(double), cudaMemcpyDefault, st));
-  TS_CHECK(cta_pairs(*A, I, t, gram, 0, st));
+  TS_CHECK(cta_pairs(CtaOp{*A, I, 0}, I, t, gram, 0, st));
   TS_CHECK(c.read_state());
   memcpy(phi, c.hs->phi, 2 * t * sizeof(double));
   if (krylov)
@@ -1101,7 +1168,7 @@ int ts_cta_step(const ts_matrix* A, int32_t h_mode, const double* x, const doubl
   TS_CUDA(cudaMemcpyAsync(I->x, x, A->n * sizeof(double), cudaMemcpyDefault, st));
   EpiDot e{I->kp.p[0], I->kp.p[0], &I->ds->r_norm, 1};  // ||r|| for the monotone test
   TS_CHECK(vecpass(*A, A->m, e, I->wk, st));
-  TS_CHECK(cta_step_kernels(*A, I, t, gram, st, 0, 0));
+  TS_CHECK(cta_step_kernels(CtaOp{*A, I, 0}, I, t, gram, st, 0, 0));
   TS_CHECK(c.read_state());
   if (c.hs->status == TS_NUMERICAL_FAILURE) {
     set_error("moment solve failed: SVD did not converge in Linear Least Squares");
@@ -1372,8 +1439,12 @@ int ts_cta_solve(const ts_matrix* A, const double* b, const ts_cta_options* o, d
   if (o->h_mode != 0 && o->h_mode != 1) TS_INVAL("unknown h_mode");
   int t_max = (int)std::min<int64_t>(o->t_max, A->m);
   if (t_max > kTMax) TS_INVAL("t_max=%d exceeds the device limit %d", t_max, kTMax);
-  if (o->h_mode == 1 && A->m != A->n) TS_INVAL("symmetric mode requires a square matrix");
+  if (o->h_mode == 1 && A->m != A->n && !o->normal_operand)
+    TS_INVAL("symmetric mode requires a square matrix");
   if (o->h_mode == 1 && A->comm) TS_INVAL("symmetric mode is not supported on a column-sharded matrix");
+  if (o->normal_operand && A->comm) TS_INVAL("the normal operand A^T A is not supported on a sharded matrix");
+  if (o->normal_operand) t_max = (int)std::min<int64_t>(o->t_max, A->n);
+  if (t_max > kTMax) TS_INVAL("t_max=%d exceeds the device limit %d", t_max, kTMax);
   memset(res, 0, sizeof(*res));
   DeviceGuard g(A->dev);
   CtaArgs a;
@@ -1389,6 +1460,7 @@ int ts_cta_solve(const ts_matrix* A, const double* b, const ts_cta_options* o, d
   a.accel_ratio = o->accel_ratio;
   a.x_start = o->x_start;
   a.enhanced = (o->enhanced && !o->known_solvable) ? 1 : 0;  // centering.py:306
+  a.normal = o->normal_operand ? 1 : 0;
   return cta_solve(*A, b, a, x_out, trace, trace_cap, res, (cudaStream_t)stream);
 }
 

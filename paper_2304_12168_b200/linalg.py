@@ -233,15 +233,16 @@ def residual(a, x, b, want_normal: bool = True, want_vector: bool = False):
     with ``want_vector``) — the honest-residual step of the drivers
     (triangle.py:84-89, hybrid.py:102-104)."""
     dm, gram = as_device_matrix(a)
-    if gram:
-        raise TypeError("residual() expects a matrix, not a GramProduct")
     m, n = dm.shape
+    if gram:  # `a` is a GramProduct: r = b - A^T A x in n-space
+        m = n
     x = _as_vec(x, n, "x has length {got}, expected {want}")
     b = _as_vec(b, m, "b has length {got}, expected {want}")
     rn, an = C.c_double(), C.c_double()
     r = np.empty(m) if want_vector else None
-    N.check(N.lib().ts_residual(dm.handle, N.ptr(x), N.ptr(b), r.ctypes.data if r is not None else None,
-                                C.byref(rn), C.byref(an) if want_normal else None, None))
+    fn = N.lib().ts_gram_residual if gram else N.lib().ts_residual
+    N.check(fn(dm.handle, N.ptr(x), N.ptr(b), r.ctypes.data if r is not None else None,
+               C.byref(rn), C.byref(an) if want_normal else None, None))
     out = (float(rn.value), float(an.value) if want_normal else None)
     return out + (r,) if want_vector else out
 
@@ -318,6 +319,16 @@ class HOperator:
 
     def quadratic_form(self, r, hr) -> float:
         return dot(r, hr)
+
+
+def nnz_of(a) -> int:
+    """Stored nonzeros of a sparse matrix, else the nonzero count
+    (linalg.py:72-76)."""
+    if isinstance(a, DeviceMatrix):
+        return int(a.nnz)
+    if sparse.issparse(a):
+        return int(a.nnz)
+    return int(np.count_nonzero(np.asarray(a)))
 
 
 def validate_symmetric(a, rel_tol: float = 1e-12) -> bool:

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _native as N
 from ._solve import build_result, host_vec, rows_to_trace, trace_buffer
-from .linalg import (as_device_matrix, dot, local_rows, local_slice, matvec, matvec_transpose, norm2,
+from .linalg import (GramProduct, as_device_matrix, dot, local_rows, local_slice, matvec, matvec_transpose, norm2,
                      residual, shape_of)
 from .results import (
     APPROX_SOLUTION,
@@ -151,14 +151,15 @@ def min_norm_solve(a, b, eps, x_eps, inner_cap=250_000, max_iters=4_000_000) -> 
     if norm2(b) == 0.0:
         raise ValueError("b must be nonzero")
     dm, gram = as_device_matrix(a)
-    if gram:
-        raise TypeError("min_norm_solve expects a matrix, not a GramProduct")
+    # the operand of the inner solves and residuals: A, or the implicit A^T A
+    # (a GramProduct: every apply is the device pass pair A^T (A v))
+    op = GramProduct(dm) if gram else dm
     x_eps = host_vec(local_slice(a, x_eps, dm.shape[1]), dm.shape[1], "x_eps has wrong shape")
-    start_gap, _ = residual(dm, x_eps, b, want_normal=False)
+    start_gap, _ = residual(op, x_eps, b, want_normal=False)
     if start_gap > eps * (1.0 + 1e-9):
         raise ValueError(
             f"x_eps is not an eps-approximate solution: ||Ax-b|| = {start_gap:.3e} > {eps:.3e}")
-    zero_floor = 1e-14 * dm.frobenius_norm() * norm2(b)  # floating floor for "||c|| > 0"
+    zero_floor = 1e-14 * op.frobenius_norm() * norm2(b)  # floating floor for "||c|| > 0"
 
     rho_hi = norm2(x_eps)
     rho_lo = 0.0
@@ -173,7 +174,7 @@ def min_norm_solve(a, b, eps, x_eps, inner_cap=250_000, max_iters=4_000_000) -> 
     launches = 0
 
     def finish(st, x, **extra):
-        rn, an = residual(dm, x, b)
+        rn, an = residual(op, x, b)
         out = SolveResult(st, x, rn, an, iterations, trace, **extra)
         out.device_ms = device_ms
         out.kernel_launches = launches
@@ -186,7 +187,7 @@ def min_norm_solve(a, b, eps, x_eps, inner_cap=250_000, max_iters=4_000_000) -> 
         rho = 0.5 * (rho_hi + rho_lo)
         if rho <= 0.0:
             break
-        inner = solve_in_ball(dm, b, rho, 0.25 * eps, eps_prime=zero_floor,
+        inner = solve_in_ball(op, b, rho, 0.25 * eps, eps_prime=zero_floor,
                               max_iters=min(inner_cap, max_iters - iterations), x0=warm)
         device_ms += inner.device_ms or 0.0
         launches += inner.kernel_launches or 0

@@ -64,6 +64,17 @@ def _c(w):
     return (w.a, w.b)
 
 
+def _gram_operand(seed, m, n, mn=False):
+    """A (m x n) and b = (A^T A) x* in n-space, for solves on the implicit
+    normal matrix GramProduct(A) (the reference's operator plug-in); with `mn`
+    also x* (an exact solution, the min-norm bisection's start)."""
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    xs = rng.standard_normal(n)
+    b = a.T @ (a @ xs)
+    return (a, b, xs) if mn else (a, b)
+
+
 CASES = [
     # --- CTA (centering_solve) ------------------------------------------------
     ("cta_c1_window", lambda: _c(W.dense_gaussian(64, 64, seed=1)), "cta",
@@ -94,6 +105,11 @@ CASES = [
     ("cta_sparse_rect", lambda: (sparse.csr_array(sparse.random_array(
         (40, 90), density=0.1, rng=np.random.default_rng(5))), np.random.default_rng(6).standard_normal(40)),
      "cta", dict(epsilon=1e-9, max_iters=2000)),
+    # CTA on the implicit normal matrix (centering.py:278 over linalg.py:93-114)
+    ("cta_gram_operand", lambda: _gram_operand(21, 30, 12), "cta_gramop",
+     dict(epsilon=1e-8, max_iters=40)),
+    ("cta_gram_operand_sym", lambda: _gram_operand(22, 25, 9), "cta_gramop",
+     dict(epsilon=1e-10, h_mode="a", max_iters=60)),
     # --- TA (solve_adaptive) --------------------------------------------------
     ("ta_c1_window", lambda: _c(W.dense_gaussian(64, 64, seed=1)), "ta",
      dict(eps_rel=1e-8, max_iters=50)),
@@ -140,6 +156,7 @@ CASES = [
      dict(eps=1e-7)),
     ("mn_ne_branch", lambda: (np.array([[1.0, 0.0], [0.0, 0.0]]), np.array([1.0, 0.5]),
                               np.array([1.0, 0.0])), "mn", dict(eps=0.6)),
+    ("mn_gram_operand", lambda: _gram_operand(23, 6, 10, mn=True), "mn_gramop", dict(eps=1e-6)),
     # --- hybrid CTA -> TA (hybrid_solve) --------------------------------------
     ("hy_min_norm", lambda: (lambda r: (lambda a: (a, a @ r.standard_normal(5)))(
         r.standard_normal((2, 5))))(np.random.default_rng(0)), "hybrid",
@@ -151,6 +168,8 @@ CASES = [
      dict(eps_cta=1e-6, eps_ta=1e-12)),
     ("hy_c2_lowrank", lambda: _c(W.dense_lowrank(60, 200, 20, seed=9)), "hybrid",
      dict(eps_cta=1e-8, eps_ta=1e-10)),
+    ("hy_gram_operand", lambda: _gram_operand(24, 20, 8), "hybrid_gramop",
+     dict(eps_cta=1e-6, eps_ta=1e-12, max_iters_stage2=40)),
 ]
 
 

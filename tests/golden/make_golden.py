@@ -72,14 +72,19 @@ def _call(solver, a, b, kw):
         return trisolve.nonnegative_feasibility(a, b, **kw), kw
     if solver == "hybrid":
         return trisolve.hybrid_solve(a, b, trisolve.HybridOptions(**kw)), kw
+    if solver == "cta_gramop":
+        return trisolve.centering_solve(trisolve.GramProduct(a), b, trisolve.CenteringOptions(**kw)), kw
+    if solver == "hybrid_gramop":
+        return trisolve.hybrid_solve(trisolve.GramProduct(a), b, trisolve.HybridOptions(**kw)), kw
     raise KeyError(solver)
 
 
 def record_case(name, builder, solver, kw):
     built = builder()
     a, b = built[0], built[1]
-    if solver == "mn":
-        res = trisolve.min_norm_solve(a, b, x_eps=built[2], **kw)
+    if solver in ("mn", "mn_gramop"):
+        op = trisolve.GramProduct(a) if solver == "mn_gramop" else a
+        res = trisolve.min_norm_solve(op, b, x_eps=built[2], **kw)
         resolved = dict(kw)
     else:
         res, resolved = _call(solver, a, b, kw)
@@ -179,8 +184,12 @@ def record_kats():
 
 
 def main():
-    record_kats()
+    only = set(sys.argv[1:])  # record just these cases (default: everything)
+    if not only:
+        record_kats()
     for name, builder, solver, kw in CASES:
+        if only and name not in only:
+            continue
         res = record_case(name, builder, solver, kw)
         print(f"{name:24s} {res.status:20s} iters={res.iterations:6d} "
               f"res={res.residual_norm:.3e} nres={res.normal_residual_norm:.3e}")

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_symbols():
         assert hasattr(lib, name), name
     assert set(declared_symbols()) == set(_native.EXPORTS)
-    assert lib.ts_abi_version() == 1
+    assert lib.ts_abi_version() == _native.ABI_VERSION == 2
 
 
 def test_struct_layouts_match_header(tmp_path):

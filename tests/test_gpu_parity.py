@@ -5,19 +5,23 @@ drop-in entry points (C ABI -> CUDA kernels) on the recorded inputs and
 compared with the reference's recorded result:
 
 * WINDOW cases (default): identical status, detail, iteration count and
-  trace event sequence; iterates and trace norms within 1e-9 relative
-  (BASELINE.json north_star: "iterates within 1e-9 relative l2").
+  trace event sequence; iterates and trace norms within
+  max(1e-9, 10 x_noise) relative, where x_noise is the REFERENCE'S OWN
+  spread on that case (tests/golden/self_noise.json, recorded by
+  make_noise.py: 1e-15 perturbations of b and 1 vs 8 OpenBLAS threads).
+  That is north_star's 1e-9 on every case but two whose reference spread is
+  itself above 1e-10 (ta_c1_window 1.0e-9, ta_gram 4.8e-10, cta_enhanced_probe31
+  1.3e-10, ball_random_inside 1.2e-10).
 * CHAOTIC cases: ill-conditioned runs far past the parity window, where
   the reference disagrees with itself once only BLAS reduction order
   changes (1e-3..1e-2 after a few hundred iterations).
   Their outcome moves with the last bits of every step, so it is checked
-  against the REFERENCE'S OWN band, recorded from the real reference by
-  tests/golden/make_bands.py under 1e-15 input perturbations and
-  equivalent moment-system solvers (gelsd / SVD / eigh / Cholesky / LU):
+  against the REFERENCE'S OWN perturbation band (tests/golden/make_bands.py:
+  200 runs with b * (1 + 1e-15 N(0,1)), the reference's code unchanged):
   status among the band's statuses, final residual within a factor of 2
-  (north_star) of the band, iteration count within the band +-1 %
-  (cta_c4_convdiff: 173 .. 268 iterations, approx or normal-equation stop;
-  cta_c3_clement at its cap: residual 2.8e-5 .. 1.2e-3).
+  (north_star) of the band, iteration count within the band +-1 %, and x no
+  farther from the recorded x than 10 x the band's x spread.  Where the
+  device lands is printed (``LANDING`` lines, ``pytest -s``).
 """
 
 from __future__ import annotations
@@ -32,8 +36,11 @@ from conftest import EVENTS, Golden, golden_names, rel_l2, trace_rows_numeric
 
 pytestmark = pytest.mark.gpu
 
-with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "chaotic_bands.json")) as _fh:
-    CHAOTIC_BANDS = json.load(_fh)
+_GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+with open(os.path.join(_GOLDEN, "chaotic_bands.json")) as _fh:
+    CHAOTIC_BANDS = {k: v["perturbation"] for k, v in json.load(_fh).items()}
+with open(os.path.join(_GOLDEN, "self_noise.json")) as _fh:
+    SELF_NOISE = json.load(_fh)["cases"]
 CHAOTIC = {"cta_c1_cap", "ta_c1_500", "ta_c1_revalidate", "cta_c3_clement", "ta_sparse_c3",
            "cta_c4_convdiff"}
 # Warm-started bisections / staged solves whose iteration count is not stable
@@ -42,12 +49,20 @@ CHAOTIC = {"cta_c1_cap", "ta_c1_500", "ta_c1_revalidate", "cta_c3_clement", "ta_
 # 192..234 (hy_c2_lowrank), 70..1266 (hy_min_norm).  Parity there is the
 # outcome: status (and stage statuses), the certified bracket, ||x|| and the
 # residual against the tolerance the solve certifies.
-OUTCOME = {"mn_underdetermined", "mn_bisection", "hy_min_norm", "hy_c2_lowrank"}
-# cases whose tolerances are looser than the window but still tight
-LOOSE_X = {"cta_sym_diag": 1e-7, "ta_diag": 1e-7, "ta_restart": 1e-6, "ta_gram": 1e-6,
-           "ball_random_inside": 1e-7, "lp_random_feasible": 1e-6, "lp_sparse_feasible": 1e-6,
-           "cta_known_solvable": 1e-7, "cta_sparse_rect": 1e-7, "cta_c2_lowrank": 1e-8,
-           "ta_c5_lp_matrix": 1e-8, "cta_accelerate": 1e-8, "cta_random_start": 1e-8}
+OUTCOME = {"mn_underdetermined", "mn_bisection", "hy_min_norm", "hy_c2_lowrank", "mn_gram_operand"}
+
+
+def x_tolerance(name: str) -> float:
+    """max(1e-9, 10 x the reference's own x spread on the case)."""
+    return max(1e-9, 10.0 * SELF_NOISE[name]["x_noise"]) if name in SELF_NOISE else 1e-9
+
+
+def trace_tolerance(name: str) -> float:
+    """max(1e-9, 10 x the reference's own trace spread on the case): trace
+    norms near convergence sit at the cancellation floor of the recursively
+    updated residual, where the reference's own rows move by more than x."""
+    return max(x_tolerance(name), 10.0 * SELF_NOISE[name].get("trace_noise", 0.0)) \
+        if name in SELF_NOISE else 1e-9
 
 
 def run_device(g: Golden):
@@ -68,6 +83,12 @@ def run_device(g: Golden):
         return ts.min_norm_solve(g.a, g.b, x_eps=g.x_eps, **kw)
     if g.solver == "hybrid":
         return ts.hybrid_solve(g.a, g.b, ts.HybridOptions(**kw))
+    if g.solver == "cta_gramop":
+        return ts.centering_solve(ts.GramProduct(g.a), g.b, ts.CenteringOptions(**kw))
+    if g.solver == "mn_gramop":
+        return ts.min_norm_solve(ts.GramProduct(g.a), g.b, x_eps=g.x_eps, **kw)
+    if g.solver == "hybrid_gramop":
+        return ts.hybrid_solve(ts.GramProduct(g.a), g.b, ts.HybridOptions(**kw))
     raise KeyError(g.solver)
 
 
@@ -109,11 +130,17 @@ def test_golden_parity(name):
         assert hi - lo <= g.kwargs.get("eps", 1e-6) * (1 + 1e-9) or g.solver == "hybrid"
     if name in CHAOTIC:
         bd = CHAOTIC_BANDS[name]
+        xd = rel_l2(res.x, g.x)
+        print(f"LANDING {name}: status {res.status} iterations {res.iterations} "
+              f"(band {bd['iterations_lo']}..{bd['iterations_hi']}, reference {g.iterations}), "
+              f"residual {res.residual_norm:.3e} (band {bd['residual_lo']:.3e}..{bd['residual_hi']:.3e}), "
+              f"x {xd:.2e} from the reference's (band spread {bd['x_spread']:.2e})")
         assert 0.5 * bd["residual_lo"] - floor <= res.residual_norm <= 2.0 * bd["residual_hi"] + floor, (
             res.residual_norm, bd)
-        lo = int(np.floor(0.99 * bd["iterations_lo"])) - 2
-        hi = int(np.ceil(1.01 * bd["iterations_hi"])) + 2
+        lo = int(np.floor(0.99 * bd["iterations_lo"]))
+        hi = int(np.ceil(1.01 * bd["iterations_hi"]))
         assert lo <= res.iterations <= hi, (res.iterations, bd)
+        assert xd <= 10.0 * bd["x_spread"], (xd, bd["x_spread"])
         return
     assert res.iterations == g.iterations
     tr = trace_rows_numeric(res.trace.rows, res.trace.columns)
@@ -122,11 +149,12 @@ def test_golden_parity(name):
         ev = g.trace_columns.index("event")
         assert np.array_equal(tr[:, ev], g.trace[:, ev])
     assert res.detail == g.detail
-    tol = LOOSE_X.get(name, 1e-9)
+    tol = x_tolerance(name)
     assert rel_l2(res.x, g.x) <= tol, rel_l2(res.x, g.x)
     if g.trace.size:
         colmax = np.abs(g.trace).max(axis=0)
-        assert np.all(np.abs(tr - g.trace) <= tol * np.maximum(np.abs(g.trace), colmax))
+        ttol = trace_tolerance(name)
+        assert np.all(np.abs(tr - g.trace) <= ttol * np.maximum(np.abs(g.trace), colmax))
     for key, val in g.extras.items():
         got = getattr(res, key)
         if isinstance(val, np.ndarray):

@@ -31,6 +31,12 @@ def run_oracle(g):
         return port.min_norm_solve(g.a, g.b, x_eps=g.x_eps, **kw)
     if g.solver == "hybrid":
         return port.hybrid_solve(g.a, g.b, **kw)
+    if g.solver == "cta_gramop":
+        return port.cta_solve(port.Gram(g.a), g.b, **kw)
+    if g.solver == "mn_gramop":
+        return port.min_norm_solve(port.Gram(g.a), g.b, x_eps=g.x_eps, **kw)
+    if g.solver == "hybrid_gramop":
+        return port.hybrid_solve(port.Gram(g.a), g.b, **kw)
     raise KeyError(g.solver)
 
 
@@ -44,7 +50,7 @@ def test_oracle_matches_reference(golden):
     # last-ulp allowance only for BLAS kernel selection differences
     assert rel_l2(out["x"], g.x) <= 1e-14
     assert out["residual_norm"] == pytest.approx(g.residual_norm, rel=1e-12, abs=1e-300)
-    if g.solver == "hybrid":  # merged trace is host bookkeeping; check the stages instead
+    if g.solver.startswith("hybrid"):  # merged trace is host bookkeeping; check the stages instead
         assert list(out["stage_status"]) == g.stage_status
         assert list(out["stage_iterations"]) == g.stage_iterations
         return
@@ -100,7 +106,7 @@ def test_chaotic_bands_cover_the_recorded_and_oracle_runs():
     from conftest import Golden
 
     with open(os.path.join(GOLDEN, "chaotic_bands.json")) as fh:
-        bands = json.load(fh)
+        bands = {k: v["perturbation"] for k, v in json.load(fh).items()}
     assert set(bands) == {"cta_c1_cap", "ta_c1_500", "ta_c1_revalidate", "cta_c3_clement",
                           "ta_sparse_c3", "cta_c4_convdiff"}
     for name, bd in bands.items():
@@ -111,3 +117,23 @@ def test_chaotic_bands_cover_the_recorded_and_oracle_runs():
             continue  # dense: the oracle's BLAS order is the recorded one (checked above)
         out = run_oracle(g)
         assert 0.5 * bd["residual_lo"] <= out["residual_norm"] <= 2.0 * bd["residual_hi"]
+        assert np.linalg.norm(out["x"] - g.x) <= 10 * bd["x_spread"] * np.linalg.norm(g.x)
+
+
+def test_self_noise_table_covers_the_window_cases():
+    """tests/golden/self_noise.json (make_noise.py) holds the reference's own
+    x spread for every non-OUTCOME golden case, and the recorded run sits
+    inside its recorded spread of statuses / iterations."""
+    import json
+
+    from conftest import Golden, golden_names
+
+    with open(os.path.join(GOLDEN, "self_noise.json")) as fh:
+        noise = json.load(fh)["cases"]
+    outcome = {"mn_underdetermined", "mn_bisection", "hy_min_norm", "hy_c2_lowrank", "mn_gram_operand"}
+    assert set(noise) == set(golden_names()) - outcome
+    for name, nd in noise.items():
+        g = Golden(name)
+        assert g.status in nd["statuses"]
+        assert nd["iterations_lo"] <= g.iterations <= nd["iterations_hi"]
+        assert 0.0 <= nd["x_noise"] < 1e-2
