@@ -323,14 +323,17 @@ TS_API int ts_matrix_set_row_shard(ts_matrix* a, ts_comm* comm, int64_t n_global
  * A^T r of every solver for this layout. */
 TS_API int ts_matrix_set_tall_shard(ts_matrix* a, ts_comm* comm, int64_t m_global, int64_t row_offset,
                                     double frobenius_global);
-/* Emulated world: `world` communicators of ONE process on one device (out
- * receives `world` handles, rank order), for running the sharded device code
- * at world > 1 on a single GPU.  Each rank's solves run on their own host
+/* In-process world: `world` communicators of ONE process (out receives
+ * `world` handles, rank order), rank r on devices[r] (devices NULL: every rank
+ * on `device`, an emulated world that runs the sharded device code at world
+ * > 1 on a single GPU).  Ranks on different GPUs read each other's slots over
+ * NVLink (peer access is enabled).  Each rank's solves run on their own host
  * thread; every exchange is ordered on the host between the producer and the
- * consumer kernels instead of spinning on device flags (kernels that wait on
- * one another must not share a GPU).  Results are bit-identical to a world of
- * the same size across GPUs. */
-TS_API int ts_comm_create_local(int device, int world, int64_t vec_capacity, ts_comm** out);
+ * consumer kernels (events) instead of spinning on device flags, so ranks may
+ * share a GPU.  Results are bit-identical to a world of the same size with one
+ * process per GPU. */
+TS_API int ts_comm_create_local(int device, int world, int64_t vec_capacity, const int32_t* devices,
+                                ts_comm** out);
 
 /* ---- solvers --------------------------------------------------------------- */
 TS_API int ts_cta_solve(const ts_matrix* a, const double* b, const ts_cta_options* opts, double* x_out,

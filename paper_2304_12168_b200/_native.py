@@ -130,7 +130,7 @@ def _declare(lib):
         "ts_matrix_set_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
         "ts_matrix_set_row_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
         "ts_matrix_set_tall_shard": ([_P, _P, _I64, _I64, _D], C.c_int),
-        "ts_comm_create_local": ([C.c_int, C.c_int, _I64, _P], C.c_int),
+        "ts_comm_create_local": ([C.c_int, C.c_int, _I64, _P, _P], C.c_int),
         "ts_matrix_gen_stencil5": ([_I64, _D, _D, _D, _D, _D, _I32, C.c_int, _P, C.POINTER(_P)],
                                    C.c_int),
         "ts_matrix_gen_clement": ([_I64, C.c_int, _P, C.POINTER(_P)], C.c_int),

@@ -1231,10 +1231,26 @@ int ts_comm_create(int device, int rank, int world, int64_t vec_capacity, ts_com
 // its own symmetric slots, flags and epoch; peers are plain device pointers
 // and every exchange is ordered on the host (LocalGroup, csrc/ts_comm.cuh).
 // Each rank's solves must run on their own host thread.
-int ts_comm_create_local(int device, int world, int64_t vec_capacity, ts_comm** out) {
+int ts_comm_create_local(int device, int world, int64_t vec_capacity, const int32_t* devices,
+                         ts_comm** out) {
   if (!out) TS_INVAL("null argument");
   if (world < 1 || world > kMaxRanks) TS_INVAL("world %d outside 1..%d", world, kMaxRanks);
   if (vec_capacity < 1) TS_INVAL("vector capacity must be positive");
+  std::vector<int> dev(world, device);
+  if (devices)
+    for (int r = 0; r < world; ++r) dev[r] = devices[r];
+  // ranks on different GPUs read each other's slots over NVLink: peer access
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) {
+      if (dev[r] == dev[q]) continue;
+      int ok = 0;
+      TS_CUDA(cudaDeviceCanAccessPeer(&ok, dev[r], dev[q]));
+      if (!ok) TS_INVAL("device %d cannot access device %d (no peer path)", dev[r], dev[q]);
+      DeviceGuard pg(dev[r]);
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(dev[q], 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) TS_CUDA(pe);
+      cudaGetLastError();
+    }
   DeviceGuard g(device);
   auto grp = std::make_shared<LocalGroup>(world);
   std::vector<Comm*> cs;
@@ -1250,9 +1266,10 @@ int ts_comm_create_local(int device, int world, int64_t vec_capacity, ts_comm** 
   const size_t slot = (size_t)vec_capacity + kArScalars;
   cudaError_t e;
   for (int r = 0; r < world; ++r) {
+    DeviceGuard rg(dev[r]);
     Comm* c = new Comm();
     cs.push_back(c);
-    c->dev = device;
+    c->dev = dev[r];
     c->rank = r;
     c->world = world;
     c->vec_cap = (size_t)vec_capacity;
@@ -1273,13 +1290,17 @@ int ts_comm_create_local(int device, int world, int64_t vec_capacity, ts_comm** 
     pflags[r] = cs[r]->flags;
   }
   for (Comm* c : cs) {
+    DeviceGuard rg(c->dev);
     if ((e = cudaMalloc(&c->psym_d, world * sizeof(double*))) != cudaSuccess) return fail("cudaMalloc", e);
     if ((e = cudaMalloc(&c->pflags_d, world * sizeof(unsigned long long*))) != cudaSuccess)
       return fail("cudaMalloc", e);
     cudaMemcpy(c->psym_d, psym.data(), world * sizeof(double*), cudaMemcpyHostToDevice);
     cudaMemcpy(c->pflags_d, pflags.data(), world * sizeof(unsigned long long*), cudaMemcpyHostToDevice);
   }
-  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("comm init", e);
+  for (Comm* c : cs) {
+    DeviceGuard rg(c->dev);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("comm init", e);
+  }
   for (int r = 0; r < world; ++r) out[r] = reinterpret_cast<ts_comm*>(cs[r]);
   return 0;
 }

@@ -132,8 +132,11 @@ static cudaError_t dev_malloc(T** p, size_t bytes, int dev) {
 }
 
 static void free_plan(RowPlan& p) {
-  for (void* q : {(void*)p.wrow, (void*)p.sell_sp, (void*)p.sell_ci, (void*)p.sell_val})
-    if (q) cudaFree(q);
+  if (p.wrow) cudaFree(p.wrow);
+  if (!p.sell_borrowed)
+    for (void* q : {(void*)p.sell_sp, (void*)p.sell_ci, (void*)p.sell_val})
+      if (q) cudaFree(q);
+  p.sell_borrowed = 0;
   p.wrow = nullptr;
   p.sell_sp = nullptr;
   p.sell_ci = nullptr;
@@ -170,7 +173,7 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
     if (nw.wrow)
       cudaMemcpyAsync(old.wrow, nw.wrow, (size_t)nw.P * kWarps * sizeof(int),
                       cudaMemcpyDeviceToDevice, st);
-    if (nw.sell_sp) {
+    if (nw.sell_sp && !nw.sell_borrowed) {
       cudaMemcpyAsync(old.sell_sp, nw.sell_sp, (size_t)((rows + 31) / 32 + 1) * sizeof(int),
                       cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.sell_ci, nw.sell_ci, (size_t)nw.sell_slots * sizeof(int), cudaMemcpyDeviceToDevice, st);
@@ -180,6 +183,12 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
     cudaStreamSynchronize(st);
     free_plan(nw);
   } else {
+    if (nw.sell_borrowed) {  // nw refilled old's tables: they change owner, not freed
+      old.sell_sp = nullptr;
+      old.sell_ci = nullptr;
+      old.sell_val = nullptr;
+      nw.sell_borrowed = 0;
+    }
     free_plan(old);
     old = nw;
   }
@@ -471,7 +480,7 @@ static int grid_for(int64_t n) {
 // scanned on the host in 64 bits (a padded size past the int32 slot range
 // falls back to the thread-per-row kernel), then the fill on the device.
 static int build_sell(RowPlan& p, const int* rp, const int* ci, const double* val, int64_t rows, int sms, int dev,
-                      cudaStream_t st) {
+                      cudaStream_t st, RowPlan* reuse = nullptr) {
   if (p.kind != PLAN_SELL) return 0;
   const int64_t nsl = (rows + 31) / 32;
   std::vector<int> w((size_t)nsl + 1);
@@ -495,9 +504,17 @@ static int build_sell(RowPlan& p, const int* rp, const int* ci, const double* va
     return 0;
   }
   const size_t slots = (size_t)std::max<int64_t>(total, 1);
-  if (dev_malloc(&p.sell_sp, ((size_t)nsl + 1) * sizeof(int), dev) != cudaSuccess ||
-      dev_malloc(&p.sell_ci, slots * sizeof(int), dev) != cudaSuccess ||
-      dev_malloc(&p.sell_val, slots * sizeof(double), dev) != cudaSuccess) {
+  if (reuse && reuse->kind == PLAN_SELL && reuse->sell_slots == total && reuse->sell_sp) {
+    // a recycled handle of the same shape and padded size: refill its tables
+    // in place (no cudaMalloc / cudaFree: both synchronise the device and
+    // would stall solves running on other streams)
+    p.sell_sp = reuse->sell_sp;
+    p.sell_ci = reuse->sell_ci;
+    p.sell_val = reuse->sell_val;
+    p.sell_borrowed = 1;
+  } else if (dev_malloc(&p.sell_sp, ((size_t)nsl + 1) * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.sell_ci, slots * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.sell_val, slots * sizeof(double), dev) != cudaSuccess) {
     set_error("cudaMalloc for the sliced-ELL copy (%lld slots) failed", (long long)total);
     return TS_ENOMEM;
   }
@@ -854,8 +871,8 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
         free_plan(pN);
         return fail(rc);
       }
-      if ((rc = build_sell(pN, A->rp, A->ci, A->val, m, A->sms, device, st)) ||
-          (rc = build_sell(pT, A->rpT, A->ciT, A->valT, n, A->sms, device, st))) {
+      if ((rc = build_sell(pN, A->rp, A->ci, A->val, m, A->sms, device, st, reuse ? &A->planN : nullptr)) ||
+          (rc = build_sell(pT, A->rpT, A->ciT, A->valT, n, A->sms, device, st, reuse ? &A->planT : nullptr))) {
         free_plan(pN);
         free_plan(pT);
         return fail(rc);

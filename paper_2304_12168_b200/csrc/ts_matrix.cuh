@@ -48,6 +48,7 @@ struct RowPlan {
   int* sell_sp = nullptr;  // device [ceil(rows / 32) + 1]
   int* sell_ci = nullptr;  // device [sell_slots]
   double* sell_val = nullptr;
+  int sell_borrowed = 0;   // tables refilled in place in a recycled handle's plan (not owned)
 };
 
 struct Instance;  // cached solver instance (ts_drivers.cuh)

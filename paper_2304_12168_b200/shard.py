@@ -416,11 +416,16 @@ class LocalWorld:
     for the sharded device code, not a performance one.
     """
 
-    def __init__(self, world: int, device: int = 0):
+    def __init__(self, world: int, device: int = 0, devices=None):
+        """``devices``: the GPU of every rank (default: all on ``device``, an
+        emulated world; distinct GPUs read each other's slots over NVLink)."""
         if world < 1:
             raise ValueError("world must be positive")
         self.world = int(world)
         self.device = int(device)
+        self.devices = [int(d) for d in devices] if devices is not None else [self.device] * self.world
+        if len(self.devices) != self.world:
+            raise ValueError("one device per rank expected")
         self._comms: list[list[Communicator]] = []
 
     def comms(self, capacity: int) -> list[Communicator]:
@@ -428,8 +433,9 @@ class LocalWorld:
             if cs[0].capacity >= capacity:
                 return cs
         arr = (C.c_void_p * self.world)()
-        N.check(N.lib().ts_comm_create_local(self.device, self.world, int(capacity), arr))
-        cs = [Communicator(C.c_void_p(arr[r]), r, self.world, self.device, int(capacity), local=True)
+        devs = (C.c_int32 * self.world)(*self.devices)
+        N.check(N.lib().ts_comm_create_local(self.device, self.world, int(capacity), devs, arr))
+        cs = [Communicator(C.c_void_p(arr[r]), r, self.world, self.devices[r], int(capacity), local=True)
               for r in range(self.world)]
         self._comms.append(cs)
         return cs
@@ -437,7 +443,7 @@ class LocalWorld:
     def columns(self, a) -> list[ShardedMatrix]:
         m, n = (int(s) for s in a.shape)
         crs = [column_range(n, self.world, r) for r in range(self.world)]
-        dms = [DeviceMatrix(local_block(a, *cr), device=self.device) for cr in crs]
+        dms = [DeviceMatrix(local_block(a, *cr), device=d) for cr, d in zip(crs, self.devices)]
         fro = math.sqrt(sum(dm.frobenius_norm() ** 2 for dm in dms))
         cs = self.comms(m)
         out = []
@@ -453,7 +459,7 @@ class LocalWorld:
         blocks = [row_blocks(a, *rr) for rr in rrs]
         hw = max(b[2] for b in blocks)
         _check_halo(hw, min(rr[1] - rr[0] for rr in rrs))
-        dms = [_pair_matrix(b[0], b[1], rr, hw, self.device) for b, rr in zip(blocks, rrs)]
+        dms = [_pair_matrix(b[0], b[1], rr, hw, d) for b, rr, d in zip(blocks, rrs, self.devices)]
         fro = math.sqrt(sum(dm.frobenius_norm() ** 2 for dm in dms))
         cs = self.comms(max(2 * hw, 1))
         out = []
@@ -466,7 +472,7 @@ class LocalWorld:
     def tall(self, a) -> list[TallShardedMatrix]:
         m, n = (int(s) for s in a.shape)
         rrs = [column_range(m, self.world, r) for r in range(self.world)]
-        dms = [DeviceMatrix(row_block(a, *rr), device=self.device) for rr in rrs]
+        dms = [DeviceMatrix(row_block(a, *rr), device=d) for rr, d in zip(rrs, self.devices)]
         fro = math.sqrt(sum(dm.frobenius_norm() ** 2 for dm in dms))
         cs = self.comms(n)
         out = []
@@ -475,6 +481,18 @@ class LocalWorld:
             s._setup(dms[r], cs[r], (m, n), rrs[r], fro)
             out.append(s)
         return out
+
+    def shard(self, a) -> list:
+        """Every rank's shard in the north_star layout for `a` (see
+        shard_matrix): square banded sparse -> row blocks with halos, tall ->
+        row blocks, else column blocks."""
+        m, n = a.shape
+        if m == n and sparse.issparse(a):
+            try:
+                return self.rows(a)
+            except ValueError:  # band wider than a row block: column blocks
+                pass
+        return self.tall(a) if m > n else self.columns(a)
 
     def run(self, fn, shards, *args, **kw) -> list:
         """``fn(shard, *args, **kw)`` for every rank at once (one host thread

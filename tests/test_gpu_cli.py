@@ -36,11 +36,44 @@ def test_solve_generated_and_file(tmp_path, capsys):
     capsys.readouterr()
 
 
-def test_bench_rows(capsys):
+def test_bench_rows(capsys, monkeypatch):
+    """The reference's CSV columns, then device_ms and matvec_gbs; rows on a
+    TRISOLVE_WORKERS thread pool spread over --gpus devices give the same
+    rows as the serial run."""
     from paper_2304_12168_b200.cli import main
 
-    assert main(["bench", "--gen", "clement:101", "--gen", "convdiff:20", "--algo", "cta",
-                 "--algo", "ta", "--trials", "1", "--max-iters", "200"]) == 0
+    argv = ["bench", "--gen", "clement:101", "--gen", "convdiff:20", "--algo", "cta",
+            "--algo", "ta", "--trials", "1", "--max-iters", "200"]
+    assert main(argv) == 0
     lines = capsys.readouterr().out.strip().splitlines()
-    assert lines[0] == "family,n,algo,iterations,wall_ms,residual,normal_residual,outcome"
+    assert lines[0] == ("family,n,algo,iterations,wall_ms,residual,normal_residual,outcome,"
+                        "device_ms,matvec_gbs")
     assert len(lines) == 5 and not any("error" in ln for ln in lines[1:])
+    for ln in lines[1:]:
+        cols = ln.split(",")
+        assert float(cols[8]) > 0 and float(cols[9]) > 0  # device time and pair GB/s
+    monkeypatch.setenv("TRISOLVE_WORKERS", "3")
+    assert main(argv + ["--gpus", "2"]) == 0
+    pooled = capsys.readouterr().out.strip().splitlines()
+    key = lambda ln: [c for i, c in enumerate(ln.split(",")) if i not in (4, 8, 9)]  # noqa: E731
+    assert [key(ln) for ln in pooled] == [key(ln) for ln in lines]
+
+
+@pytest.mark.parametrize("spec,algo", [("poisson-d:40", "cta"), ("clement:301", "ta"),
+                                       ("diag-pd:200", "lpfeas")])
+def test_solve_on_two_gpus_matches_one(spec, algo, tmp_path, capsys):
+    """solve --gpus 2 (one sharded solve, two ranks; on a one-GPU box both
+    ranks share it) reaches the outcome and iteration count of --gpus 1, and
+    inside the 40-iteration parity window the same residual."""
+    from paper_2304_12168_b200.cli import main
+
+    outs = []
+    for gpus in ("1", "2"):
+        summ = tmp_path / f"s{gpus}.json"
+        rc = main(["solve", "--gen", spec, "--algo", algo, "--eps", "1e-8", "--max-iters", "40",
+                   "--gpus", gpus, "--summary", str(summ), "--dump-x", str(tmp_path / f"x{gpus}.mtx")])
+        capsys.readouterr()
+        outs.append((rc, json.loads(summ.read_text())))
+    (rc1, s1), (rc2, s2) = outs
+    assert rc1 == rc2 and s1["outcome"] == s2["outcome"] and s1["iterations"] == s2["iterations"]
+    assert s2["final_residual_norm"] == pytest.approx(s1["final_residual_norm"], rel=1e-6, abs=1e-12)
