@@ -200,6 +200,10 @@ TS_API int ts_matrix_destroy(ts_matrix* a);
 /* kind: 0 dense, 1 csr.  frobenius: ||A||_F computed once at creation. */
 TS_API int ts_matrix_info(const ts_matrix* a, int64_t* m, int64_t* n, int64_t* nnz, int32_t* kind,
                    double* frobenius);
+/* The launch plans chosen for the handle's two passes (diagnostics / tests):
+ * 0 flat split, 1 thread per row, 2 dense tiles, 7 warp per row, 9 dense
+ * transposed copy, 10 sliced ELL, 11 column slabs. */
+TS_API int ts_matrix_plans(const ts_matrix* a, int32_t* plan_av, int32_t* plan_atv);
 
 /* ---- storage pools --------------------------------------------------------
  * ts_matrix_destroy retires an unsharded handle (device storage, launch plans,

@@ -21,6 +21,7 @@ ABI_VERSION = 2  # TS_ABI_VERSION of include/trisolve_b200.h
 EXPORTS = (
     "ts_abi_version", "ts_last_error", "ts_device_count",
     "ts_matrix_create_dense", "ts_matrix_create_csr", "ts_matrix_destroy", "ts_matrix_info",
+    "ts_matrix_plans",
     "ts_matvec", "ts_rmatvec", "ts_gram_matvec", "ts_norm2", "ts_dot", "ts_residual", "ts_gram_residual",
     "ts_moments", "ts_hankel_min_norm", "ts_cta_step", "ts_time_pass",
     "ts_cta_solve", "ts_ta_adaptive", "ts_ta_in_ball", "ts_lp_feasibility",
@@ -112,6 +113,7 @@ def _declare(lib):
         "ts_host_free": ([_P], C.c_int),
         "ts_matrix_info": ([_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64),
                             C.POINTER(_I32), C.POINTER(_D)], C.c_int),
+        "ts_matrix_plans": ([_P, C.POINTER(_I32), C.POINTER(_I32)], C.c_int),
         "ts_matvec": ([_P, _P, _P, _P], C.c_int),
         "ts_rmatvec": ([_P, _P, _P, _P], C.c_int),
         "ts_gram_matvec": ([_P, _P, _P, _P], C.c_int),

@@ -8,6 +8,7 @@
 // ring (seg_cap rows) needs flushing.  The host synchronises only at those
 // points, never inside an iteration.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -136,7 +137,15 @@ static void free_plan(RowPlan& p) {
   if (!p.sell_borrowed)
     for (void* q : {(void*)p.sell_sp, (void*)p.sell_ci, (void*)p.sell_val})
       if (q) cudaFree(q);
+  if (!p.slab_borrowed)
+    for (void* q : {(void*)p.slab_cb, (void*)p.slab_sp, (void*)p.slab_wr, (void*)p.slab_perm,
+                    (void*)p.slab_col, (void*)p.slab_val})
+      if (q) cudaFree(q);
   p.sell_borrowed = 0;
+  p.slab_borrowed = 0;
+  p.slab_cb = p.slab_sp = p.slab_wr = p.slab_perm = nullptr;
+  p.slab_col = nullptr;
+  p.slab_val = nullptr;
   p.wrow = nullptr;
   p.sell_sp = nullptr;
   p.sell_ci = nullptr;
@@ -168,7 +177,9 @@ static cudaError_t upload_rows(double* dst, int64_t dld, const double* src, int6
 // graphs bake the grid and the plan-table pointer); false: geometry changed
 static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st) {
   const bool same = old.kind == nw.kind && old.P == nw.P && (old.wrow != nullptr) == (nw.wrow != nullptr) &&
-                    old.sell_slots == nw.sell_slots && (old.sell_sp != nullptr) == (nw.sell_sp != nullptr);
+                    old.sell_slots == nw.sell_slots && (old.sell_sp != nullptr) == (nw.sell_sp != nullptr) &&
+                    old.slab_slots == nw.slab_slots && old.slab_nsl == nw.slab_nsl &&
+                    old.slab_maxw == nw.slab_maxw;
   if (same) {
     if (nw.wrow)
       cudaMemcpyAsync(old.wrow, nw.wrow, (size_t)nw.P * kWarps * sizeof(int),
@@ -180,6 +191,15 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
       cudaMemcpyAsync(old.sell_val, nw.sell_val, (size_t)nw.sell_slots * sizeof(double),
                       cudaMemcpyDeviceToDevice, st);
     }
+    if (nw.slab_sp && !nw.slab_borrowed) {
+      const size_t nsp = (size_t)nw.P * nw.slab_nsl + 1, np32 = (size_t)nw.P * nw.slab_nsl * 32;
+      cudaMemcpyAsync(old.slab_cb, nw.slab_cb, (nw.P + 1) * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.slab_sp, nw.slab_sp, nsp * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.slab_wr, nw.slab_wr, (size_t)nw.P * 33 * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.slab_perm, nw.slab_perm, np32 * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.slab_col, nw.slab_col, nw.slab_slots * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.slab_val, nw.slab_val, nw.slab_slots * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    }
     cudaStreamSynchronize(st);
     free_plan(nw);
   } else {
@@ -188,6 +208,12 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
       old.sell_ci = nullptr;
       old.sell_val = nullptr;
       nw.sell_borrowed = 0;
+    }
+    if (nw.slab_borrowed) {
+      old.slab_cb = old.slab_sp = old.slab_wr = old.slab_perm = nullptr;
+      old.slab_col = nullptr;
+      old.slab_val = nullptr;
+      nw.slab_borrowed = 0;
     }
     free_plan(old);
     old = nw;
@@ -470,6 +496,57 @@ __global__ void k_sell_fill(const int* rp, const int* ci, const double* val, int
   }
 }
 
+// column-slab copy (k_slab_av): per (slab, row) the row's run of entries
+// inside the slab (CSR rows sorted by column: contiguous); flags unsorted rows
+__global__ void k_slab_runs(const int* rp, const int* ci, int64_t m, const int* cb, int P, int* cnt, int* start,
+                            int* unsorted) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    int e = rp[r];
+    const int e1 = rp[r + 1];
+    for (int k = e + 1; k < e1; ++k)
+      if (ci[k] < ci[k - 1]) *unsorted = 1;
+    for (int s = 0; s < P; ++s) {
+      const int st = e, lim = cb[s + 1];
+      while (e < e1 && ci[e] < lim) ++e;
+      cnt[(int64_t)s * m + r] = e - st;
+      start[(int64_t)s * m + r] = st;
+    }
+  }
+}
+__global__ void k_slab_iota(int64_t m, int P, int* rows, int* offs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)P * m; i += (int64_t)gridDim.x * blockDim.x)
+    rows[i] = (int)(i % m);
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= P; s += (int64_t)gridDim.x * blockDim.x)
+    offs[s] = (int)(s * m);
+}
+// slice widths (the first, longest row of each sorted slice), permutation
+// table (row of (slice, lane)) and inverse position of every row
+__global__ void k_slab_tables(const int* slen, const int* srow, int64_t m, int P, int nsl, int* width, int* perm,
+                              int* pos) {
+  const int64_t tot = (int64_t)P * nsl * 32;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = t / ((int64_t)nsl * 32), i = t - s * nsl * 32;  // i = q * 32 + lane
+    const int row = i < m ? srow[s * m + i] : -1;
+    perm[t] = row;
+    if (row >= 0) pos[s * m + row] = (int)i;
+    if ((i & 31) == 0) width[s * nsl + (i >> 5)] = i < m ? slen[s * m + i] : 0;
+  }
+}
+__global__ void k_slab_fill(const int* ci, const double* val, int64_t m, int P, int nsl, const int* cb,
+                            const int* cnt, const int* start, const int* pos, const int* sp, uint16_t* scol,
+                            double* sval) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)P * m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = t / m;
+    const int i = pos[t];
+    const int64_t base = (int64_t)sp[s * nsl + (i >> 5)] + (i & 31);
+    const int k0 = start[t], c0 = cb[s];
+    for (int k = 0; k < cnt[t]; ++k) {
+      scol[base + 32 * k] = (uint16_t)(ci[k0 + k] - c0);
+      sval[base + 32 * k] = val[k0 + k];
+    }
+  }
+}
+
 static int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4096));
@@ -523,6 +600,127 @@ static int build_sell(RowPlan& p, const int* rp, const int* ci, const double* va
   k_sell_fill<<<grid_for(nsl * 32), 256, 0, st>>>(rp, ci, val, rows, nsl, p.sell_sp, p.sell_ci, p.sell_val);
   TS_CUDA(cudaGetLastError());
   TS_CUDA(cudaStreamSynchronize(st));  // the host offsets leave scope
+  return 0;
+}
+
+// The column-slab tables of a long-row CSR A v over a wide matrix (PLAN_SLAB,
+// k_slab_av): P = #SM slabs of equal nnz (column boundaries from the CSC
+// column pointers).  Kept only when it pays and fits: n >= 65536 (x beyond
+// any L1), every slab <= kSlabMaxW columns, the per-(slab, row) partials at
+// most a quarter of the matrix bytes, sorted row indices.  Otherwise `p`
+// stays the row kernel's plan.
+static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* val, int64_t m, int64_t n,
+                      int64_t nnz, const std::vector<int>& colptr, int sms, int dev, cudaStream_t st,
+                      RowPlan* reuse = nullptr) {
+  if (!(p.kind == PLAN_WROW || p.kind == PLAN_FLAT) || n < 65536 || m > (int64_t)INT32_MAX / 64) return 0;
+  const int P = sms;
+  if ((double)m * P * 16.0 > 0.25 * 12.0 * (double)nnz) return 0;
+  std::vector<int> cb(P + 1);
+  int maxw = 0;
+  for (int s = 0; s <= P; ++s) {
+    const int64_t target = nnz * s / P;
+    cb[s] = s == 0 ? 0 : s == P ? (int)n
+                   : (int)(std::lower_bound(colptr.begin(), colptr.end(), (int)target) - colptr.begin());
+    if (s > 0) {
+      cb[s] = std::max(cb[s], cb[s - 1]);
+      maxw = std::max(maxw, cb[s] - cb[s - 1]);
+    }
+  }
+  if (maxw > kSlabMaxW || maxw < 1) return 0;
+  const int nsl = (int)((m + 31) / 32);
+  const int64_t Pm = (int64_t)P * m, Pn32 = (int64_t)P * nsl * 32;
+  Arena ar(st);
+  int *dcb, *cnt, *start, *unsorted, *rows_in, *offs, *slen, *srow, *width, *pos;
+  TS_CHECK(ar.get(&dcb, P + 1));
+  TS_CHECK(ar.get(&cnt, Pm));
+  TS_CHECK(ar.get(&start, Pm));
+  TS_CHECK(ar.get(&unsorted, 1));
+  TS_CHECK(ar.get(&rows_in, Pm));
+  TS_CHECK(ar.get(&offs, P + 1));
+  TS_CHECK(ar.get(&slen, Pm));
+  TS_CHECK(ar.get(&srow, Pm));
+  TS_CHECK(ar.get(&width, (size_t)P * nsl));
+  TS_CHECK(ar.get(&pos, Pm));
+  TS_CUDA(cudaMemcpyAsync(dcb, cb.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
+  k_slab_runs<<<grid_for(m), 256, 0, st>>>(rp, ci, m, dcb, P, cnt, start, unsorted);
+  k_slab_iota<<<grid_for(Pm), 256, 0, st>>>(m, P, rows_in, offs);
+  // rows of every slab by in-slab length, descending, stable
+  int end_bit = 1;
+  while (end_bit < 31 && (1ll << end_bit) <= (int64_t)nnz) ++end_bit;
+  size_t tb = 0;
+  cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, cnt, slen, rows_in, srow, (int)Pm, P, offs,
+                                                     offs + 1, 0, end_bit, st);
+  char* tmp;
+  TS_CHECK(ar.get(&tmp, std::max<size_t>(tb, 16)));
+  if (cub::DeviceSegmentedRadixSort::SortPairsDescending(tmp, tb, cnt, slen, rows_in, srow, (int)Pm, P, offs,
+                                                         offs + 1, 0, end_bit, st) != cudaSuccess) {
+    set_error("segmented sort for the column-slab copy failed");
+    return TS_ECUDA;
+  }
+  int* dperm_tmp;
+  TS_CHECK(ar.get(&dperm_tmp, Pn32));
+  k_slab_tables<<<grid_for(Pn32), 256, 0, st>>>(slen, srow, m, P, nsl, width, dperm_tmp, pos);
+  TS_CUDA(cudaGetLastError());
+  std::vector<int> w((size_t)P * nsl);
+  int hun = 0;
+  TS_CUDA(d2h_pinned(w.data(), width, w.size() * sizeof(int), st));
+  TS_CUDA(d2h_pinned(&hun, unsorted, sizeof(int), st));
+  if (hun) return 0;  // unsorted column indices: keep the row kernel
+  // slice offsets (64-bit scan) and the warp runs of every slab (equal slots)
+  std::vector<int> sp((size_t)P * nsl + 1), wr((size_t)P * 33);
+  int64_t tot = 0;
+  for (int s = 0; s < P; ++s) {
+    const int64_t s0 = tot;
+    for (int q = 0; q < nsl; ++q) {
+      sp[(size_t)s * nsl + q] = (int)std::min<int64_t>(tot, INT32_MAX);
+      tot += 32ll * w[(size_t)s * nsl + q];
+    }
+    const int64_t stot = tot - s0;
+    int64_t acc = 0;
+    int q = 0;
+    for (int ww = 0; ww <= 32; ++ww) {
+      const int64_t target = stot * ww / 32;
+      while (q < nsl && acc + 16ll * w[(size_t)s * nsl + q] < target) acc += 32ll * w[(size_t)s * nsl + q++];
+      wr[(size_t)s * 33 + ww] = ww == 32 ? nsl : std::max(q, ww ? wr[(size_t)s * 33 + ww - 1] : 0);
+    }
+  }
+  if (tot >= (int64_t)INT32_MAX) return 0;
+  sp[(size_t)P * nsl] = (int)tot;
+  const size_t slots = (size_t)std::max<int64_t>(tot, 1);
+  if (reuse && reuse->kind == PLAN_SLAB && reuse->slab_slots == tot && reuse->P == P && reuse->slab_nsl == nsl) {
+    // a recycled handle of the same shape and size: refill its tables in place
+    p.slab_cb = reuse->slab_cb;
+    p.slab_sp = reuse->slab_sp;
+    p.slab_wr = reuse->slab_wr;
+    p.slab_perm = reuse->slab_perm;
+    p.slab_col = reuse->slab_col;
+    p.slab_val = reuse->slab_val;
+    p.slab_borrowed = 1;
+  } else if (dev_malloc(&p.slab_cb, (P + 1) * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.slab_sp, sp.size() * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.slab_wr, wr.size() * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.slab_perm, Pn32 * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.slab_col, slots * sizeof(uint16_t), dev) != cudaSuccess ||
+             dev_malloc(&p.slab_val, slots * sizeof(double), dev) != cudaSuccess) {
+    set_error("cudaMalloc for the column-slab copy (%lld slots) failed", (long long)tot);
+    return TS_ENOMEM;
+  }
+  TS_CUDA(cudaMemcpyAsync(p.slab_cb, cb.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaMemcpyAsync(p.slab_sp, sp.data(), sp.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaMemcpyAsync(p.slab_wr, wr.data(), wr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaMemcpyAsync(p.slab_perm, dperm_tmp, Pn32 * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  TS_CUDA(cudaMemsetAsync(p.slab_col, 0xFF, slots * sizeof(uint16_t), st));  // padding: kSlabPad
+  TS_CUDA(cudaMemsetAsync(p.slab_val, 0, slots * sizeof(double), st));
+  k_slab_fill<<<grid_for(Pm), 256, 0, st>>>(ci, val, m, P, nsl, p.slab_cb, cnt, start, pos, p.slab_sp,
+                                            p.slab_col, p.slab_val);
+  TS_CUDA(cudaGetLastError());
+  TS_CUDA(cudaStreamSynchronize(st));  // the host tables leave scope
+  p.kind = PLAN_SLAB;
+  p.P = P;
+  p.slab_nsl = nsl;
+  p.slab_maxw = maxw;
+  p.slab_slots = tot;
   return 0;
 }
 }  // namespace ts
@@ -635,6 +833,13 @@ int ts_host_free(void* ptr) {
     }
   }
   cudaFreeHost(base);
+  return 0;
+}
+
+int ts_matrix_plans(const ts_matrix* A, int32_t* plan_av, int32_t* plan_atv) {
+  if (!A) TS_INVAL("null matrix handle");
+  if (plan_av) *plan_av = A->planN.kind;
+  if (plan_atv) *plan_atv = A->planT.kind;
   return 0;
 }
 
@@ -872,13 +1077,16 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
         return fail(rc);
       }
       if ((rc = build_sell(pN, A->rp, A->ci, A->val, m, A->sms, device, st, reuse ? &A->planN : nullptr)) ||
-          (rc = build_sell(pT, A->rpT, A->ciT, A->valT, n, A->sms, device, st, reuse ? &A->planT : nullptr))) {
+          (rc = build_sell(pT, A->rpT, A->ciT, A->valT, n, A->sms, device, st, reuse ? &A->planT : nullptr)) ||
+          (rc = build_slab(pN, A->rp, A->ci, A->val, m, n, nnz, rpT_h, A->sms, device, st,
+                           reuse ? &A->planN : nullptr))) {
         free_plan(pN);
         free_plan(pT);
         return fail(rc);
       }
       const bool keepN = adopt_plan(A->planN, pN, m, st);
       const bool keepT = adopt_plan(A->planT, pT, n, st);
+      A->npart = A->planN.kind == PLAN_SLAB ? (int64_t)A->planN.P * m : 0;  // the slab partials
       // a recycled handle's instances bake the old launch geometry
       if (reuse && !(keepN && keepT)) destroy_instances(A);
     }

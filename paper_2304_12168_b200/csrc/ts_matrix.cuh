@@ -28,8 +28,9 @@ namespace ts {
 // PLAN_WROW   long CSR rows of near-uniform length (k_rows_wrow)
 // PLAN_TRANS  small dense A^T v over a transposed copy (k_rows_tile_fused)
 // PLAN_SELL   short CSR rows, HBM-sized: sliced-ELL copy (k_rows_sell)
+// PLAN_SLAB   long CSR rows of a wide matrix: column slabs (k_slab_av + k_slab_combine)
 enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WROW = 7, PLAN_TRANS = 9,
-                      PLAN_SELL = 10 };
+                      PLAN_SELL = 10, PLAN_SLAB = 11 };
 
 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans):
@@ -49,6 +50,13 @@ struct RowPlan {
   int* sell_ci = nullptr;  // device [sell_slots]
   double* sell_val = nullptr;
   int sell_borrowed = 0;   // tables refilled in place in a recycled handle's plan (not owned)
+  // PLAN_SLAB: the column-slab copy (see k_slab_av); P = slabs
+  int slab_nsl = 0, slab_maxw = 0;
+  int64_t slab_slots = 0;
+  int *slab_cb = nullptr, *slab_sp = nullptr, *slab_wr = nullptr, *slab_perm = nullptr;
+  uint16_t* slab_col = nullptr;
+  double* slab_val = nullptr;
+  int slab_borrowed = 0;
 };
 
 struct Instance;  // cached solver instance (ts_drivers.cuh)
@@ -182,7 +190,20 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
   } else {
     const RowPlan& pl = trans ? M.planT : M.planN;
     const CsrRows acc = trans ? M.csrT() : M.csr();
-    if (pl.kind == PLAN_SELL)
+    if (pl.kind == PLAN_SLAB) {
+      static bool attr_done[64] = {false};  // per device: the attribute is per function and device
+      if (M.dev >= 0 && M.dev < 64 && !attr_done[M.dev]) {
+        TS_CUDA(cudaFuncSetAttribute(k_slab_av<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSlabMaxW * (int)sizeof(double)));
+        attr_done[M.dev] = true;
+      }
+      const SlabRows sr{(int)acc.m, pl.P, pl.slab_nsl, pl.slab_cb, pl.slab_sp, pl.slab_wr, pl.slab_perm,
+                        pl.slab_col, pl.slab_val};
+      k_slab_av<Epi><<<pl.P, kSlabT, pl.slab_maxw * sizeof(double), st>>>(sr, x, xs, epi, wk.npart);
+      const int ng = (int)((acc.m + 31) / 32);
+      k_slab_combine<Epi><<<std::max(1, std::min(ng, wk.pmax)), kNT, 0, st>>>((int)acc.m, pl.P, wk.npart, epi,
+                                                                             wk);
+    } else if (pl.kind == PLAN_SELL)
       k_rows_sell<Epi><<<pl.P, kNT, 0, st>>>(SellRows{pl.sell_sp, pl.sell_ci, pl.sell_val, acc.m}, x, xs,
                                              epi, wk);
     else if (pl.kind == PLAN_FLAT)

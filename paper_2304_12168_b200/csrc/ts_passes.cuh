@@ -8,8 +8,10 @@
 //                     any row-length distribution; rows cut by a warp boundary
 //                     are merged inside the block, rows cut by a block boundary
 //                     by the last block to arrive on that row.
-//   k_rows_wrow       long CSR rows of near-uniform length (C5's A v): warp per
-//                     row with the next chunks' loads in flight.
+//   k_rows_wrow       long CSR rows of near-uniform length: warp per row with
+//                     the next chunks' loads in flight.
+//   k_slab_av         long CSR rows of a wide matrix (C5's A v): column slabs
+//   + k_slab_combine  with x staged in shared memory, SELL-32-sigma inside.
 //   k_rows_short      one thread per row, sequential left-to-right sum without
 //                     FMA: bitwise scipy csr_matvec; L2-resident matrices (C3).
 //   k_rows_sell       one thread per row over a sliced-ELL copy, bitwise
@@ -535,6 +537,166 @@ __global__ void __launch_bounds__(kNT, kWrowBlocks) k_rows_wrow(CsrRows A, const
     }
     const double sum = warp_reduce((a[0] + a[1]) + (a[2] + a[3]), RED_SUM);
     if (lane == 0) epi.elem(r, sum, acc);
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+  }
+  finish_last(epi, wk, nullptr, (int)gridDim.x, sm, &sflag);
+}
+
+// ------------------------------------------------------------- k_slab_av ----
+// Long-row CSR A v over a WIDE matrix (C5: 10^4 rows x 10^6 columns, ~1000
+// entries per row, x = 8 MB): the warp-per-row kernel is bound by its random
+// 8-byte gathers of x, each one 32-byte L2 sector.  Here the columns are cut
+// into P slabs of equal nnz (P = #SMs, one 1024-thread block per slab), each
+// block stages its slab of x — transformed once by `xs` — in shared memory,
+// so every gather is a shared-memory read.  Inside a slab the rows are sorted
+// by their in-slab length (descending, stable) and cut into slices of 32
+// whose entries are interleaved (SELL-32-sigma: entry k of lane l at sp + 32 k
+// + l; fp64 values, in-slab column offsets as u16, padding 0xFFFF).  Each warp
+// streams a contiguous run of slices as one coalesced stream (kSlabU loads in
+// flight per lane, slice ends from registers) and writes every row's slab sum
+// (FMA chain in the row's column order) to part[s][row].  k_slab_combine then
+// adds the P partials of a row in slab order and runs the pass epilogue.
+// tools/microbench/spmv_slab.cu on C5 (warm): 34.7 us for both kernels vs
+// 53.3 us for k_rows_wrow.
+constexpr int kSlabT = 1024;       // threads of a slab block
+constexpr int kSlabU = 8;          // loads in flight per lane
+constexpr int kSlabMaxW = 24576;   // columns per slab: the x slab in <= 192 KB of smem
+constexpr unsigned kSlabPad = 0xFFFFu;
+
+struct SlabRows {
+  int m, P, nsl;          // rows, slabs, slices per slab
+  const int* cb;          // [P + 1] slab column boundaries
+  const int* sp;          // [P * nsl + 1] slot offset of every slice
+  const int* wr;          // [P * 33] first in-slab slice of each warp's run
+  const int* perm;        // [P * nsl * 32] row of (slice, lane), -1 past m
+  const uint16_t* col;    // in-slab column, kSlabPad on padding
+  const double* val;
+};
+
+__device__ __forceinline__ unsigned ld_stream_u16(const uint16_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(kSlabT, 1) k_slab_av(SlabRows S, const double* __restrict__ x, XS xs, Epi epi,
+                                                       double* __restrict__ part) {
+  extern __shared__ double xsl[];
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) return;  // k_slab_combine owns idle()
+  xs.load();
+  ktimer_begin(epi.timer());
+  constexpr int U = kSlabU;
+  const int s = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cb0 = __ldg(S.cb + s), cw = __ldg(S.cb + s + 1) - cb0;
+  const int q0 = __ldg(S.wr + s * 33 + w), q1 = __ldg(S.wr + s * 33 + w + 1);
+  // the first chunk's slice ends and first rows are in flight with the x loads
+  const int g0 = s * S.nsl;
+  int nq = min(q1 - q0, 31);
+  int bnd = (lane <= nq && q0 < q1) ? __ldg(S.sp + g0 + q0 + lane) : 0;
+  int prow = (q0 < q1) ? __ldg(S.perm + (size_t)(g0 + q0) * 32 + lane) : -1;
+  for (int i = threadIdx.x; i < cw; i += kSlabT) xsl[i] = xs(__ldg(x + cb0 + i));
+  __syncthreads();
+  double* out = part + (size_t)s * S.m;
+  for (int qc = q0; qc < q1;) {
+    nq = min(q1 - qc, 31);
+    const int gq = g0 + qc;
+    const int e0 = __shfl_sync(0xffffffffu, bnd, 0);
+    const int K = (__shfl_sync(0xffffffffu, bnd, nq) - e0) >> 5;
+    int j = 0;
+    int kend = (__shfl_sync(0xffffffffu, bnd, 1) - e0) >> 5;
+    int row = prow;
+    prow = (nq > 1) ? __ldg(S.perm + (size_t)(gq + 1) * 32 + lane) : -1;
+    double acc = 0.0;
+    auto emit = [&]() {  // the slice's rows are complete: store, move to the next slice
+      if (row >= 0) out[row] = acc;
+      acc = 0.0;
+      ++j;
+      row = prow;
+      if (j + 1 < nq) prow = __ldg(S.perm + (size_t)(gq + j + 1) * 32 + lane);
+      kend = (__shfl_sync(0xffffffffu, bnd, min(j + 1, nq)) - e0) >> 5;
+    };
+    const double* vp = S.val + e0 + lane;
+    const uint16_t* cp = S.col + e0 + lane;
+    for (int k0 = 0; k0 < K; k0 += U) {
+      double v[U];
+      unsigned c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = k0 + u < K;
+        v[u] = ok ? ld_stream(vp + 32 * (k0 + u)) : 0.0;
+        c[u] = ok ? ld_stream_u16(cp + 32 * (k0 + u)) : kSlabPad;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u;
+        if (k >= K) break;
+        while (k == kend && j < nq) emit();
+        if (c[u] != kSlabPad) acc = fma(v[u], xsl[c[u]], acc);
+      }
+    }
+    while (j < nq) emit();
+    qc += nq;
+    if (qc < q1) {  // the next chunk's slice ends and first rows
+      const int nn = min(q1 - qc, 31);
+      bnd = (lane <= nn) ? __ldg(S.sp + g0 + qc + lane) : 0;
+      prow = __ldg(S.perm + (size_t)(g0 + qc) * 32 + lane);
+    }
+  }
+}
+
+// y_r = sum over slabs of part[s][r], slabs in order: 32 rows per block, warp
+// g adds the contiguous slab range [g P / 8, (g + 1) P / 8) with all its loads
+// in flight, the 8 warp sums are added in warp order; then the epilogue
+template <class Epi>
+__global__ void __launch_bounds__(kNT) k_slab_combine(int m, int P, const double* __restrict__ part, Epi epi,
+                                                      Work wk) {
+  constexpr int K = Epi::K;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ double red[kWarps][33];
+  __shared__ int sflag;
+  __shared__ double epi_smem[kEpiSmem];
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  epi.prepare(epi_smem);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int qa = P * g / kWarps, qb = P * (g + 1) / kWarps;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  const int ngroups = (m + 31) >> 5;
+  for (int rg = blockIdx.x; rg < ngroups; rg += gridDim.x) {
+    const int r = rg * 32 + lane;
+    double sum = 0.0;
+    if (r < m) {
+      int q = qa;
+      for (; q + 8 <= qb; q += 8) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = __ldcg(part + (size_t)(q + u) * m + r);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += t[u];
+      }
+      for (; q < qb; ++q) sum += __ldcg(part + (size_t)q * m + r);
+    }
+    red[g][lane] = sum;
+    __syncthreads();
+    if (g == 0 && r < m) {
+      double y = red[0][lane];
+#pragma unroll
+      for (int j = 1; j < kWarps; ++j) y += red[j][lane];
+      epi.elem(r, y, acc);
+    }
+    __syncthreads();
   }
   block_reduce<K>(acc, sm, epi);
   if (threadIdx.x == 0) {

@@ -143,6 +143,15 @@ class DeviceMatrix:
         N.check(N.lib().ts_gram_matvec(self._handle, N.ptr(v), out.ctypes.data, None))
         return out
 
+    PLAN_NAMES = {0: "flat", 1: "thread_rows", 2: "dense_tiles", 7: "warp_rows", 9: "dense_transposed",
+                  10: "sliced_ell", 11: "column_slabs"}
+
+    def plans(self) -> tuple[str, str]:
+        """The kernels chosen for A v and A^T v."""
+        pn, pt = C.c_int32(), C.c_int32()
+        N.check(N.lib().ts_matrix_plans(self.handle, C.byref(pn), C.byref(pt)))
+        return self.PLAN_NAMES.get(pn.value, str(pn.value)), self.PLAN_NAMES.get(pt.value, str(pt.value))
+
     def __repr__(self):
         return f"DeviceMatrix({self.kind}, shape={self.shape}, nnz={self.nnz}, device={self.device})"
 

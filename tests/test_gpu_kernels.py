@@ -233,3 +233,39 @@ def test_dense_av_and_transposed_atv_alternate():
     r1, r2 = ts.centering_solve(dm, b, opts), ts.centering_solve(ts.DeviceMatrix(a), b, opts)
     assert r1.iterations == r2.iterations
     assert np.array_equal(r1.x, r2.x)
+
+
+def test_column_slab_plan_wide_long_rows():
+    """Long rows of a wide matrix (the C5 shape, scaled) take the column-slab
+    plan (k_slab_av + k_slab_combine): A v within 1e-14 of scipy (FMA chains
+    per slab, slabs added in order), the LP pivot's c+ transform applied when
+    the x slab is staged, identical bits run to run; a CSR whose rows hold
+    unsorted column indices keeps the warp-per-row kernel."""
+    import paper_2304_12168_b200 as ts
+    from paper_2304_12168_b200 import workloads as W
+
+    w = W.lp_columns(2000, 200_000, 10, seed=41)
+    dm = ts.DeviceMatrix(w.a)
+    assert dm.plans()[0] == "column_slabs"
+    rng = np.random.default_rng(4)
+    v = rng.standard_normal(w.a.shape[1])
+    y = dm.matvec(v)
+    ref = w.a @ v
+    assert np.all(np.abs(y - ref) <= 1e-14 * (abs(w.a) @ np.abs(v)))
+    assert np.array_equal(dm.matvec(v), y)
+    bn = float(np.linalg.norm(w.b))
+    r = ts.nonnegative_feasibility(dm, w.b, eps=1e-6 * bn)
+    r2 = ts.nonnegative_feasibility(ts.DeviceMatrix(w.a, ), w.b, eps=1e-6 * bn)
+    assert (r.status, r.iterations) == (r2.status, r2.iterations) and np.array_equal(r.x, r2.x)
+    # every row's entries in descending column order (a valid, unsorted CSR):
+    # no slab plan (its runs need sorted rows), the same product
+    a = w.a
+    idx, dat = a.indices.copy(), a.data.copy()
+    for r in range(a.shape[0]):
+        lo, hi = a.indptr[r], a.indptr[r + 1]
+        idx[lo:hi] = idx[lo:hi][::-1]
+        dat[lo:hi] = dat[lo:hi][::-1]
+    uns = sparse.csr_array((dat, idx, a.indptr.copy()), shape=a.shape)
+    du = ts.DeviceMatrix(uns)
+    assert du.plans()[0] == "warp_rows"
+    assert np.all(np.abs(du.matvec(v) - ref) <= 1e-14 * (abs(w.a) @ np.abs(v)))
