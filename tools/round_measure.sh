@@ -33,7 +33,7 @@ timeout 900 ncu --set full --clock-control none -k regex:"k_rows" -s 2 -c 2 \
   -o /tmp/c4_passes python tools/prof_pass.py c4 2 > $O/ncu_c4.log 2>&1
 python tools/ncu_summary.py full /tmp/c4_passes.ncu-rep > $O/c4_full_sparse_passes.json 2>&1
 python tools/ncu_summary.py traffic /tmp/c4_passes.ncu-rep > $O/c4_traffic.json 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:"k_rows" -s 2 -c 2 \
+timeout 900 ncu --set full --clock-control none -k regex:"k_rows|k_slab" -s 3 -c 3 \
   -o /tmp/c5_passes python tools/prof_pass.py c5 2 > $O/ncu_c5.log 2>&1
 python tools/ncu_summary.py full /tmp/c5_passes.ncu-rep > $O/c5_full_sparse_passes.json 2>&1
 python tools/ncu_summary.py traffic /tmp/c5_passes.ncu-rep > $O/c5_traffic.json 2>&1
