@@ -2,7 +2,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
-           --expt-relaxed-constexpr -cudart static
+           --expt-relaxed-constexpr -cudart static --split-compile=0
 LIBDIR := paper_2304_12168_b200/_lib
 SRC := $(wildcard paper_2304_12168_b200/csrc/*.cu paper_2304_12168_b200/csrc/*.cuh) include/trisolve_b200.h
 

@@ -350,14 +350,16 @@ struct EpiCtaP : EpiBase {
   int with_solve = 1;
 };
 
-// WHILE-body head: select the order-t case of the SWITCH node (t - 1), or
-// no case when the state is not running (defensive: the tail of the previous
-// trip already cleared the loop condition then).
-__global__ void k_cta_head(SolveState* s, cudaGraphConditionalHandle sw, int ncases) {
+// Graph head (once per launch, before the WHILE node): select the order-t case
+// of the first trip's SWITCH node (t - 1); later trips are selected by the
+// update's finisher.  Not running: no case and no trip.
+__global__ void k_cta_head(SolveState* s, cudaGraphConditionalHandle sw, cudaGraphConditionalHandle hw,
+                           int nocase) {
   if (threadIdx.x == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&s->launches), 1ull);
     const bool run = s->status == TS_RUNNING && s->maint == MAINT_NONE;
-    cudaGraphSetConditional(sw, run ? (unsigned)(s->t - 1) : (unsigned)ncases);
+    cudaGraphSetConditional(sw, run ? (unsigned)(s->t - 1) : (unsigned)nocase);
+    if (!run) cudaGraphSetConditional(hw, 0u);  // nothing to do: skip the loop
   }
 }
 
@@ -607,7 +609,14 @@ struct EpiCtaUpd : EpiBase {
       cta_head(s);
     }
     tail();
+    // the next trip's SWITCH case (graph mode): the order cta_head just took,
+    // the recheck case (index ncases) when it is due, none (ncases + 1) otherwise
+    if (use_sw)
+      cudaGraphSetConditional(sw, running(s) ? (unsigned)(s->t - 1)
+                                  : (s->status == TS_RUNNING && s->maint == MAINT_RECHECK) ? (unsigned)ncases
+                                                                                           : (unsigned)(ncases + 1));
   }
+  int ncases = 0;
 };
 
 // ---- enhanced probe (first_order_probe, centering.py:227-251) ------------
@@ -741,11 +750,19 @@ struct EpiCtaRecheck : EpiBase {
     if (drift > 1e-10 * scale) {
       s->status = TS_NUMERICAL_FAILURE;
       s->detail = TS_DETAIL_DRIFT;
+      graph_tail();
       return;
     }
     s->r_norm = sqrt(red[1]);
     cta_head(s);
+    graph_tail();
   }
+  // in-graph recheck (the SWITCH case after the orders): loop condition and the next case
+  __device__ void graph_tail() const {
+    tail();
+    if (use_sw) cudaGraphSetConditional(sw, running(st) ? (unsigned)(st->t - 1) : (unsigned)nocase);
+  }
+  int nocase = 0;
 };
 
 }  // namespace ts

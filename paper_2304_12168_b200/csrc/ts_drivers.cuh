@@ -185,6 +185,7 @@ struct Instance {
   ProbePtrs pp = {nullptr, nullptr, nullptr, nullptr, nullptr};
   // graph
   cudaGraph_t graph = nullptr;
+  cudaGraphNode_t wnode = nullptr;  // the WHILE node of `graph`
   cudaGraphExec_t exec = nullptr;
   cudaStream_t cap = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -274,8 +275,7 @@ struct Instance {
     np.conditional.handle = h;
     np.conditional.type = cudaGraphCondTypeWhile;
     np.conditional.size = 1;
-    cudaGraphNode_t node;
-    TS_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+    TS_CUDA(cudaGraphAddNode(&wnode, graph, nullptr, 0, &np));
     cudaGraph_t bodyg = np.conditional.phGraph_out[0];
     TS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     TS_CHECK(gbody(bodyg, h, cap));
@@ -411,6 +411,10 @@ struct SolveCtx {
     const bool direct = no_graph || (M.comm && M.comm->local);
     while (hs->status == TS_RUNNING) {
       if (hs->maint != MAINT_NONE) {
+        // graph mode services revalidation / recheck inside the loop; the host
+        // path runs in direct mode, for the probe, and after a trace-ring flush
+        static const bool dbg = getenv("TS_DEBUG_MAINT") != nullptr;
+        if (dbg) fprintf(stderr, "[trisolve] host maintenance %d at iteration %lld\n", hs->maint, hs->iterations);
         TS_CHECK(maint(st));
       } else if (!direct) {
         if (!I->exec) TS_CHECK(I->build(gbody));
@@ -511,16 +515,25 @@ struct TaKernels {
     eu.m = mo; eu.n = no; eu.relu = relu;
     return vecpass(M, mx, eu, I->wk, s);
   }
-  // graph body: [c pass] -> SWITCH{0: pivot}  (expand / stop select no case)
+  // b' = A x, gap = b - b' (every 512 pivots, triangle.py:239-242)
+  int revalidate(cudaStream_t s, cudaGraphConditionalHandle hw, int use) const {
+    EpiTaBp eb;
+    eb.st = I->ds; eb.b = I->b; eb.bp = I->bp; eb.gap = I->gap; eb.kind = 1;
+    eb.cond = hw; eb.use_cond = use;
+    return op_apply(s, I->x, XS{}, eb, 0);
+  }
+  // graph body: [c pass] -> SWITCH{0: pivot, 1: revalidate}  (expand / stop
+  // select no case; a due revalidation idles the c pass, which selects case 1)
   int graph(cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) const {
     cudaGraphConditionalHandle hsw;
     TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
     cudaGraph_t* cases = nullptr;
     TS_CHECK(capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
       TS_CHECK(c_pass(s, hw, hsw, 1));
-      return capture_switch(s, hsw, 1, &cases);
+      return capture_switch(s, hsw, 2, &cases);
     }));
-    return capture_into(cap, cases[0], [&](cudaStream_t s) -> int { return pivot(s, hw, 1); });
+    TS_CHECK(capture_into(cap, cases[0], [&](cudaStream_t s) -> int { return pivot(s, hw, 1); }));
+    return capture_into(cap, cases[1], [&](cudaStream_t s) -> int { return revalidate(s, hw, 1); });
   }
 };
 
@@ -591,11 +604,7 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
   GraphFn gbody = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
     return K.graph(bodyg, hw, cap);
   };
-  auto maint = [&](cudaStream_t s) -> int {
-    EpiTaBp eb;
-    eb.st = ds; eb.b = I->b; eb.bp = I->bp; eb.gap = I->gap; eb.kind = 1;
-    return K.op_apply(s, I->x, XS{}, eb, 0);
-  };
+  auto maint = [&](cudaStream_t s) -> int { return K.revalidate(s, 0, 0); };
   TS_CHECK(c.run(body, gbody, maint));
   if (c.hs->error == TS_EDEGENERATE) {
     set_error("degenerate pivot: v coincides with the iterate");
@@ -767,7 +776,8 @@ static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, i
 // one CTA step of at most `npairs` pairs: moments (+ Hankel in the last pair's
 // finisher), candidate norms / retry rule, fused r / x update (tail)
 static int cta_step_kernels(const CtaOp& op, const Instance* I, int npairs, int gram, cudaStream_t s,
-                            cudaGraphConditionalHandle h, int use, int enhanced = 0) {
+                            cudaGraphConditionalHandle h, int use, int enhanced = 0,
+                            cudaGraphConditionalHandle hsw = 0, int ncases = 0) {
   TS_CHECK(cta_pairs(op, I, npairs, gram, 1, s));
   if (enhanced) TS_CHECK(cta_probe_kernels(op, I, npairs, gram, s));
   const int64_t mo = op.mo(), no = op.no();
@@ -777,6 +787,7 @@ static int cta_step_kernels(const CtaOp& op, const Instance* I, int npairs, int 
   EpiCtaUpd eu;
   eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = mo;
   eu.n = no; eu.gram = gram;
+  eu.sw = hsw; eu.use_sw = ncases > 0; eu.ncases = ncases;
   return vecpass(op.M, std::max(mo, no), eu, I->wk, s);
 }
 
@@ -830,32 +841,57 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   BodyFn body = [&](cudaStream_t s) -> int {
     return cta_step_kernels(op, I, a.t_max, a.gram, s, 0, 0, a.enhanced);
   };
-  // graph body: [head: switch = t - 1] -> SWITCH{order 1 .. t_max}: each case
-  // launches exactly its t pairs + candidate + update
-  GraphFn gbody = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
-    cudaGraphConditionalHandle hsw;
-    TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
-    cudaGraph_t* cases = nullptr;
-    TS_CHECK(capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
-      ++g_launches;
-      k_cta_head<<<1, 32, 0, s>>>(ds, hsw, a.t_max);
-      TS_CUDA(cudaGetLastError());
-      return capture_switch(s, hsw, a.t_max, &cases);
-    }));
-    for (int k = 0; k < a.t_max; ++k)
-      TS_CHECK(capture_into(cap, cases[k], [&](cudaStream_t s) -> int {
-        return cta_step_kernels(op, I, k + 1, a.gram, s, hw, 1, a.enhanced);
-      }));
-    return 0;
-  };
-  auto maint = [&](cudaStream_t s) -> int {
-    if (c.hs->maint == MAINT_PROBE) return cta_probe_finish(op, I, s);
+  // ||x||, then r = b - A x against the maintained residual
+  auto recheck = [&](cudaStream_t s, cudaGraphConditionalHandle hw, int use, cudaGraphConditionalHandle hsw,
+                     int nocase) -> int {
     EpiNormTo en;
     en.st = ds; en.v = I->x; en.len = no; en.what = 1;
     TS_CHECK(vecpass(M, no, en, wk, s));
     EpiCtaRecheck er;
     er.st = ds; er.b = I->b; er.r = I->kp.p[0];
+    er.cond = hw; er.use_cond = use; er.sw = hsw; er.use_sw = use; er.nocase = nocase;
     return op.N(I->x, er, s);
+  };
+  // graph: [head: switch = t - 1] -> WHILE{ SWITCH{order 1 .. t_max} }: each case
+  // launches exactly its t pairs + candidate + update, and the update's
+  // finisher — which takes the next order from the schedule — selects the
+  // next trip's case itself, so the head runs once per graph launch, not once
+  // per iteration (tools/microbench/cond_handle.cu: a case kernel may set the
+  // value the next trip's SWITCH reads; the first value may come from a
+  // kernel node in the outer graph)
+  GraphFn gbody = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
+    cudaGraphConditionalHandle hsw;
+    TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
+    {
+      cudaGraphNodeParams kp = {};
+      kp.type = cudaGraphNodeTypeKernel;
+      SolveState* dsp = ds;
+      int nocase = a.t_max + 1;
+      void* args[4] = {&dsp, &hsw, &hw, &nocase};
+      kp.kernel.func = (void*)k_cta_head;
+      kp.kernel.gridDim = dim3(1);
+      kp.kernel.blockDim = dim3(32);
+      kp.kernel.kernelParams = args;
+      cudaGraphNode_t first;
+      TS_CUDA(cudaGraphAddNode(&first, I->graph, nullptr, 0, &kp));
+      TS_CUDA(cudaGraphAddDependencies(I->graph, &first, &I->wnode, 1));
+    }
+    cudaGraph_t* cases = nullptr;
+    TS_CHECK(capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
+      return capture_switch(s, hsw, a.t_max + 1, &cases);
+    }));
+    for (int k = 0; k < a.t_max; ++k)
+      TS_CHECK(capture_into(cap, cases[k], [&](cudaStream_t s) -> int {
+        return cta_step_kernels(op, I, k + 1, a.gram, s, hw, 1, a.enhanced, hsw, a.t_max);
+      }));
+    // case t_max: the residual recheck every `recheck_every` iterations (centering.py:345-352)
+    return capture_into(cap, cases[a.t_max], [&](cudaStream_t s) -> int {
+      return recheck(s, hw, 1, hsw, a.t_max + 1);
+    });
+  };
+  auto maint = [&](cudaStream_t s) -> int {
+    if (c.hs->maint == MAINT_PROBE) return cta_probe_finish(op, I, s);
+    return recheck(s, 0, 0, 0, 0);
   };
   TS_CHECK(c.run(body, gbody, maint));
   if (!c.hs->trivial) {

@@ -138,12 +138,12 @@ static void free_plan(RowPlan& p) {
     for (void* q : {(void*)p.sell_sp, (void*)p.sell_ci, (void*)p.sell_val})
       if (q) cudaFree(q);
   if (!p.slab_borrowed)
-    for (void* q : {(void*)p.slab_cb, (void*)p.slab_sp, (void*)p.slab_wr, (void*)p.slab_perm,
+    for (void* q : {(void*)p.slab_cb, (void*)p.slab_sp, (void*)p.slab_wr, (void*)p.slab_pos,
                     (void*)p.slab_col, (void*)p.slab_val})
       if (q) cudaFree(q);
   p.sell_borrowed = 0;
   p.slab_borrowed = 0;
-  p.slab_cb = p.slab_sp = p.slab_wr = p.slab_perm = nullptr;
+  p.slab_cb = p.slab_sp = p.slab_wr = p.slab_pos = nullptr;
   p.slab_col = nullptr;
   p.slab_val = nullptr;
   p.wrow = nullptr;
@@ -192,11 +192,11 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
                       cudaMemcpyDeviceToDevice, st);
     }
     if (nw.slab_sp && !nw.slab_borrowed) {
-      const size_t nsp = (size_t)nw.P * nw.slab_nsl + 1, np32 = (size_t)nw.P * nw.slab_nsl * 32;
+      const size_t nsp = (size_t)nw.P * nw.slab_nsl + 1, npos = (size_t)nw.P * nw.slab_rows;
       cudaMemcpyAsync(old.slab_cb, nw.slab_cb, (nw.P + 1) * sizeof(int), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_sp, nw.slab_sp, nsp * sizeof(int), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_wr, nw.slab_wr, (size_t)nw.P * 33 * sizeof(int), cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(old.slab_perm, nw.slab_perm, np32 * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.slab_pos, nw.slab_pos, npos * sizeof(int), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_col, nw.slab_col, nw.slab_slots * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_val, nw.slab_val, nw.slab_slots * sizeof(double), cudaMemcpyDeviceToDevice, st);
     }
@@ -210,7 +210,7 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
       nw.sell_borrowed = 0;
     }
     if (nw.slab_borrowed) {
-      old.slab_cb = old.slab_sp = old.slab_wr = old.slab_perm = nullptr;
+      old.slab_cb = old.slab_sp = old.slab_wr = old.slab_pos = nullptr;
       old.slab_col = nullptr;
       old.slab_val = nullptr;
       nw.slab_borrowed = 0;
@@ -519,15 +519,13 @@ __global__ void k_slab_iota(int64_t m, int P, int* rows, int* offs) {
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= P; s += (int64_t)gridDim.x * blockDim.x)
     offs[s] = (int)(s * m);
 }
-// slice widths (the first, longest row of each sorted slice), permutation
-// table (row of (slice, lane)) and inverse position of every row
-__global__ void k_slab_tables(const int* slen, const int* srow, int64_t m, int P, int nsl, int* width, int* perm,
-                              int* pos) {
+// slice widths (the first, longest row of each sorted slice) and the position
+// (slice * 32 + lane) of every row in its slab's order
+__global__ void k_slab_tables(const int* slen, const int* srow, int64_t m, int P, int nsl, int* width, int* pos) {
   const int64_t tot = (int64_t)P * nsl * 32;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t / ((int64_t)nsl * 32), i = t - s * nsl * 32;  // i = q * 32 + lane
     const int row = i < m ? srow[s * m + i] : -1;
-    perm[t] = row;
     if (row >= 0) pos[s * m + row] = (int)i;
     if ((i & 31) == 0) width[s * nsl + (i >> 5)] = i < m ? slen[s * m + i] : 0;
   }
@@ -626,8 +624,8 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
       maxw = std::max(maxw, cb[s] - cb[s - 1]);
     }
   }
-  if (maxw > kSlabMaxW || maxw < 1) return 0;
   const int nsl = (int)((m + 31) / 32);
+  if (maxw > kSlabMaxW || maxw < 1 || slab_smem(maxw, nsl) > (size_t)kSlabSmemMax) return 0;
   const int64_t Pm = (int64_t)P * m, Pn32 = (int64_t)P * nsl * 32;
   Arena ar(st);
   int *dcb, *cnt, *start, *unsorted, *rows_in, *offs, *slen, *srow, *width, *pos;
@@ -658,9 +656,7 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
     set_error("segmented sort for the column-slab copy failed");
     return TS_ECUDA;
   }
-  int* dperm_tmp;
-  TS_CHECK(ar.get(&dperm_tmp, Pn32));
-  k_slab_tables<<<grid_for(Pn32), 256, 0, st>>>(slen, srow, m, P, nsl, width, dperm_tmp, pos);
+  k_slab_tables<<<grid_for(Pn32), 256, 0, st>>>(slen, srow, m, P, nsl, width, pos);
   TS_CUDA(cudaGetLastError());
   std::vector<int> w((size_t)P * nsl);
   int hun = 0;
@@ -688,19 +684,20 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
   if (tot >= (int64_t)INT32_MAX) return 0;
   sp[(size_t)P * nsl] = (int)tot;
   const size_t slots = (size_t)std::max<int64_t>(tot, 1);
-  if (reuse && reuse->kind == PLAN_SLAB && reuse->slab_slots == tot && reuse->P == P && reuse->slab_nsl == nsl) {
+  if (reuse && reuse->kind == PLAN_SLAB && reuse->slab_slots == tot && reuse->P == P && reuse->slab_nsl == nsl &&
+      reuse->slab_rows == m) {
     // a recycled handle of the same shape and size: refill its tables in place
     p.slab_cb = reuse->slab_cb;
     p.slab_sp = reuse->slab_sp;
     p.slab_wr = reuse->slab_wr;
-    p.slab_perm = reuse->slab_perm;
+    p.slab_pos = reuse->slab_pos;
     p.slab_col = reuse->slab_col;
     p.slab_val = reuse->slab_val;
     p.slab_borrowed = 1;
   } else if (dev_malloc(&p.slab_cb, (P + 1) * sizeof(int), dev) != cudaSuccess ||
              dev_malloc(&p.slab_sp, sp.size() * sizeof(int), dev) != cudaSuccess ||
              dev_malloc(&p.slab_wr, wr.size() * sizeof(int), dev) != cudaSuccess ||
-             dev_malloc(&p.slab_perm, Pn32 * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.slab_pos, Pm * sizeof(int), dev) != cudaSuccess ||
              dev_malloc(&p.slab_col, slots * sizeof(uint16_t), dev) != cudaSuccess ||
              dev_malloc(&p.slab_val, slots * sizeof(double), dev) != cudaSuccess) {
     set_error("cudaMalloc for the column-slab copy (%lld slots) failed", (long long)tot);
@@ -709,7 +706,7 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
   TS_CUDA(cudaMemcpyAsync(p.slab_cb, cb.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
   TS_CUDA(cudaMemcpyAsync(p.slab_sp, sp.data(), sp.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   TS_CUDA(cudaMemcpyAsync(p.slab_wr, wr.data(), wr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  TS_CUDA(cudaMemcpyAsync(p.slab_perm, dperm_tmp, Pn32 * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  TS_CUDA(cudaMemcpyAsync(p.slab_pos, pos, Pm * sizeof(int), cudaMemcpyDeviceToDevice, st));
   TS_CUDA(cudaMemsetAsync(p.slab_col, 0xFF, slots * sizeof(uint16_t), st));  // padding: kSlabPad
   TS_CUDA(cudaMemsetAsync(p.slab_val, 0, slots * sizeof(double), st));
   k_slab_fill<<<grid_for(Pm), 256, 0, st>>>(ci, val, m, P, nsl, p.slab_cb, cnt, start, pos, p.slab_sp,
@@ -719,6 +716,7 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
   p.kind = PLAN_SLAB;
   p.P = P;
   p.slab_nsl = nsl;
+  p.slab_rows = m;
   p.slab_maxw = maxw;
   p.slab_slots = tot;
   return 0;

@@ -52,8 +52,8 @@ struct RowPlan {
   int sell_borrowed = 0;   // tables refilled in place in a recycled handle's plan (not owned)
   // PLAN_SLAB: the column-slab copy (see k_slab_av); P = slabs
   int slab_nsl = 0, slab_maxw = 0;
-  int64_t slab_slots = 0;
-  int *slab_cb = nullptr, *slab_sp = nullptr, *slab_wr = nullptr, *slab_perm = nullptr;
+  int64_t slab_slots = 0, slab_rows = 0;
+  int *slab_cb = nullptr, *slab_sp = nullptr, *slab_wr = nullptr, *slab_pos = nullptr;
   uint16_t* slab_col = nullptr;
   double* slab_val = nullptr;
   int slab_borrowed = 0;
@@ -193,13 +193,12 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
     if (pl.kind == PLAN_SLAB) {
       static bool attr_done[64] = {false};  // per device: the attribute is per function and device
       if (M.dev >= 0 && M.dev < 64 && !attr_done[M.dev]) {
-        TS_CUDA(cudaFuncSetAttribute(k_slab_av<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSlabMaxW * (int)sizeof(double)));
+        TS_CUDA(cudaFuncSetAttribute(k_slab_av<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmemMax));
         attr_done[M.dev] = true;
       }
-      const SlabRows sr{(int)acc.m, pl.P, pl.slab_nsl, pl.slab_cb, pl.slab_sp, pl.slab_wr, pl.slab_perm,
-                        pl.slab_col, pl.slab_val};
-      k_slab_av<Epi><<<pl.P, kSlabT, pl.slab_maxw * sizeof(double), st>>>(sr, x, xs, epi, wk.npart);
+      const SlabRows sr{(int)acc.m, pl.P, pl.slab_nsl, (pl.slab_maxw + 15) & ~15, pl.slab_cb, pl.slab_sp,
+                        pl.slab_wr, pl.slab_pos, pl.slab_col, pl.slab_val};
+      k_slab_av<Epi><<<pl.P, kSlabT, slab_smem(pl.slab_maxw, pl.slab_nsl), st>>>(sr, x, xs, epi, wk.npart);
       const int ng = (int)((acc.m + 31) / 32);
       k_slab_combine<Epi><<<std::max(1, std::min(ng, wk.pmax)), kNT, 0, st>>>((int)acc.m, pl.P, wk.npart, epi,
                                                                              wk);

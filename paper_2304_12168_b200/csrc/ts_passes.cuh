@@ -556,23 +556,37 @@ __global__ void __launch_bounds__(kNT, kWrowBlocks) k_rows_wrow(CsrRows A, const
 // by their in-slab length (descending, stable) and cut into slices of 32
 // whose entries are interleaved (SELL-32-sigma: entry k of lane l at sp + 32 k
 // + l; fp64 values, in-slab column offsets as u16, padding 0xFFFF).  Each warp
-// streams a contiguous run of slices as one coalesced stream (kSlabU loads in
-// flight per lane, slice ends from registers) and writes every row's slab sum
-// (FMA chain in the row's column order) to part[s][row].  k_slab_combine then
-// adds the P partials of a row in slab order and runs the pass epilogue.
-// tools/microbench/spmv_slab.cu on C5 (warm): 34.7 us for both kernels vs
-// 53.3 us for k_rows_wrow.
+// streams a contiguous run of slices as one coalesced stream, register
+// double-buffered: the next kSlabU k-steps are in flight while the current
+// ones are consumed (slice ends from the slab's offsets in shared memory).
+// A slice's row sums (FMA chain in the row's column order) go to shared
+// memory in SLICE order — no permutation load and no scattered store inside
+// the stream (1.5 M scattered 8-byte stores cost ~10 us of L2 sector traffic
+// on C5) — and the block writes part[s][0..m) coalesced at the end through
+// the inverse permutation `pos`.  k_slab_combine then adds the P partials of
+// a row in slab order and runs the pass epilogue.
+// tools/microbench/spmv_slab.cu on C5 (warm, in-kernel clocks): staged 2.1 us,
+// streamed by 18.8 us (100.5 MB in 16.7 us = 6.0 TB/s), flushed by 21.0 us.
 constexpr int kSlabT = 1024;       // threads of a slab block
-constexpr int kSlabU = 8;          // loads in flight per lane
-constexpr int kSlabMaxW = 24576;   // columns per slab: the x slab in <= 192 KB of smem
+constexpr int kSlabU = 4;          // k-steps per register buffer (two buffers in flight)
+constexpr int kSlabMaxW = 24576;   // columns per slab at most (u16 offsets, shared memory)
+constexpr int kSlabSmemMax = 220 * 1024;  // x slab + slice sums + slice offsets
 constexpr unsigned kSlabPad = 0xFFFFu;
+
+// dynamic shared memory of a slab block: x slab (padded to 16 doubles), one
+// sum per (slice, lane), the slab's slice offsets
+__host__ __device__ inline int slab_accn(int nsl) { return nsl * 32; }
+inline size_t slab_smem(int maxw, int nsl) {
+  return (size_t)((maxw + 15) & ~15) * 8 + (size_t)slab_accn(nsl) * 8 + ((size_t)nsl + 1) * 4 + 16;
+}
 
 struct SlabRows {
   int m, P, nsl;          // rows, slabs, slices per slab
+  int xcap;               // doubles reserved for the x slab
   const int* cb;          // [P + 1] slab column boundaries
   const int* sp;          // [P * nsl + 1] slot offset of every slice
   const int* wr;          // [P * 33] first in-slab slice of each warp's run
-  const int* perm;        // [P * nsl * 32] row of (slice, lane), -1 past m
+  const int* pos;         // [P * m] position (slice * 32 + lane) of every row in its slab's order
   const uint16_t* col;    // in-slab column, kSlabPad on padding
   const double* val;
 };
@@ -586,7 +600,10 @@ __device__ __forceinline__ unsigned ld_stream_u16(const uint16_t* p) {
 template <class Epi>
 __global__ void __launch_bounds__(kSlabT, 1) k_slab_av(SlabRows S, const double* __restrict__ x, XS xs, Epi epi,
                                                        double* __restrict__ part) {
-  extern __shared__ double xsl[];
+  extern __shared__ __align__(16) unsigned char slab_raw[];
+  double* xsl = reinterpret_cast<double*>(slab_raw);              // [xcap]
+  double* accs = xsl + S.xcap;                                    // [slab_accn(nsl)]
+  int* sps = reinterpret_cast<int*>(accs + slab_accn(S.nsl));     // [nsl + 1]
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
   if (!epi.active()) return;  // k_slab_combine owns idle()
   xs.load();
@@ -595,59 +612,54 @@ __global__ void __launch_bounds__(kSlabT, 1) k_slab_av(SlabRows S, const double*
   const int s = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int cb0 = __ldg(S.cb + s), cw = __ldg(S.cb + s + 1) - cb0;
   const int q0 = __ldg(S.wr + s * 33 + w), q1 = __ldg(S.wr + s * 33 + w + 1);
-  // the first chunk's slice ends and first rows are in flight with the x loads
   const int g0 = s * S.nsl;
-  int nq = min(q1 - q0, 31);
-  int bnd = (lane <= nq && q0 < q1) ? __ldg(S.sp + g0 + q0 + lane) : 0;
-  int prow = (q0 < q1) ? __ldg(S.perm + (size_t)(g0 + q0) * 32 + lane) : -1;
+  const int E0 = __ldg(S.sp + g0 + q0), E1 = __ldg(S.sp + g0 + q1);
+  const int KT = (E1 - E0) >> 5;  // k-steps (32 slots each) of this warp's run
+  const double* vp = S.val + E0 + lane;
+  const uint16_t* cp = S.col + E0 + lane;
+  double va[U], vb[U];
+  unsigned ca[U], cc[U];
+  auto load = [&](double (&v)[U], unsigned (&c)[U], int k0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = k0 + u < KT;
+      v[u] = ok ? ld_stream(vp + 32 * (k0 + u)) : 0.0;
+      c[u] = ok ? ld_stream_u16(cp + 32 * (k0 + u)) : kSlabPad;
+    }
+  };
+  load(va, ca, 0);  // in flight with the staging below
+  for (int i = threadIdx.x; i <= S.nsl; i += kSlabT) sps[i] = __ldg(S.sp + g0 + i);
   for (int i = threadIdx.x; i < cw; i += kSlabT) xsl[i] = xs(__ldg(x + cb0 + i));
   __syncthreads();
-  double* out = part + (size_t)s * S.m;
-  for (int qc = q0; qc < q1;) {
-    nq = min(q1 - qc, 31);
-    const int gq = g0 + qc;
-    const int e0 = __shfl_sync(0xffffffffu, bnd, 0);
-    const int K = (__shfl_sync(0xffffffffu, bnd, nq) - e0) >> 5;
-    int j = 0;
-    int kend = (__shfl_sync(0xffffffffu, bnd, 1) - e0) >> 5;
-    int row = prow;
-    prow = (nq > 1) ? __ldg(S.perm + (size_t)(gq + 1) * 32 + lane) : -1;
-    double acc = 0.0;
-    auto emit = [&]() {  // the slice's rows are complete: store, move to the next slice
-      if (row >= 0) out[row] = acc;
-      acc = 0.0;
-      ++j;
-      row = prow;
-      if (j + 1 < nq) prow = __ldg(S.perm + (size_t)(gq + j + 1) * 32 + lane);
-      kend = (__shfl_sync(0xffffffffu, bnd, min(j + 1, nq)) - e0) >> 5;
-    };
-    const double* vp = S.val + e0 + lane;
-    const uint16_t* cp = S.col + e0 + lane;
-    for (int k0 = 0; k0 < K; k0 += U) {
-      double v[U];
-      unsigned c[U];
+  int q = q0;
+  int kend = q0 < q1 ? (sps[q0 + 1] - E0) >> 5 : INT32_MAX;
+  double acc = 0.0;
+  auto emit = [&]() {  // the slice's rows are complete: park the sums, move to the next slice
+    accs[q * 32 + lane] = acc;
+    acc = 0.0;
+    ++q;
+    kend = q < q1 ? (sps[q + 1] - E0) >> 5 : INT32_MAX;
+  };
+  auto consume = [&](const double (&v)[U], const unsigned (&c)[U], int k0) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = k0 + u < K;
-        v[u] = ok ? ld_stream(vp + 32 * (k0 + u)) : 0.0;
-        c[u] = ok ? ld_stream_u16(cp + 32 * (k0 + u)) : kSlabPad;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = k0 + u;
-        if (k >= K) break;
-        while (k == kend && j < nq) emit();
-        if (c[u] != kSlabPad) acc = fma(v[u], xsl[c[u]], acc);
-      }
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u;
+      if (k >= KT) break;
+      while (k == kend) emit();
+      if (c[u] != kSlabPad) acc = fma(v[u], xsl[c[u]], acc);
     }
-    while (j < nq) emit();
-    qc += nq;
-    if (qc < q1) {  // the next chunk's slice ends and first rows
-      const int nn = min(q1 - qc, 31);
-      bnd = (lane <= nn) ? __ldg(S.sp + g0 + qc + lane) : 0;
-      prow = __ldg(S.perm + (size_t)(g0 + qc) * 32 + lane);
-    }
+  };
+  for (int k0 = 0; k0 < KT; k0 += 2 * U) {
+    load(vb, cc, k0 + U);
+    consume(va, ca, k0);
+    load(va, ca, k0 + 2 * U);
+    consume(vb, cc, k0 + U);
   }
+  while (q < q1) emit();
+  __syncthreads();
+  double* out = part + (size_t)s * S.m;
+  const int* pv = S.pos + (size_t)s * S.m;
+  for (int r = threadIdx.x; r < S.m; r += kSlabT) out[r] = accs[__ldg(pv + r)];
 }
 
 // y_r = sum over slabs of part[s][r], slabs in order: 32 rows per block, warp
@@ -677,16 +689,14 @@ __global__ void __launch_bounds__(kNT) k_slab_combine(int m, int P, const double
   for (int rg = blockIdx.x; rg < ngroups; rg += gridDim.x) {
     const int r = rg * 32 + lane;
     double sum = 0.0;
-    if (r < m) {
-      int q = qa;
-      for (; q + 8 <= qb; q += 8) {
-        double t[8];
+    if (r < m) {  // every load of a batch in flight (a serial tail costs a round trip per slab)
+      for (int q = qa; q < qb; q += 10) {
+        double t[10];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = __ldcg(part + (size_t)(q + u) * m + r);
+        for (int u = 0; u < 10; ++u) t[u] = q + u < qb ? __ldcg(part + (size_t)(q + u) * m + r) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) sum += t[u];
+        for (int u = 0; u < 10; ++u) sum += t[u];
       }
-      for (; q < qb; ++q) sum += __ldcg(part + (size_t)q * m + r);
     }
     red[g][lane] = sum;
     __syncthreads();

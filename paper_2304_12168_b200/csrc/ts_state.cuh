@@ -55,7 +55,9 @@ struct alignas(16) SolveState {
 
 __device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, int use, const SolveState* s) {
   if (!use) return;
-  const unsigned keep = (s->status == TS_RUNNING && s->maint == MAINT_NONE &&
+  // the b' = A x revalidation and the CTA residual recheck are cases of the
+  // graph's SWITCH node: the loop keeps running through them
+  const unsigned keep = (s->status == TS_RUNNING && s->maint != MAINT_PROBE &&
                          (s->trace_count - s->trace_flushed) < (long long)s->seg_cap)
                             ? 1u
                             : 0u;
@@ -335,9 +337,15 @@ struct EpiTaC : EpiBase {
     const double cp = (y >= 0.0 || y != y) ? y : 0.0;
     acc[1] = fma(cp, cp, acc[1]);
   }
+  // graph SWITCH cases: 0 pivot, 1 revalidate (b' = A x, every 512 pivots), 2 none
+  __device__ void idle() const {
+    if (use_sw)
+      cudaGraphSetConditional(sw, (st->status == TS_RUNNING && st->maint == MAINT_REVALIDATE) ? 1u : 2u);
+    EpiBase::idle();
+  }
   __device__ void finish(double (&r)[K]) const {
     ta_decide(st, r[0], r[1]);
-    if (use_sw) cudaGraphSetConditional(sw, st->event == EV_PIVOT ? 0u : 1u);
+    if (use_sw) cudaGraphSetConditional(sw, st->event == EV_PIVOT ? 0u : 2u);
     if (use_cond) {
       if (st->event != EV_PIVOT) st->body_runs += 1;
       set_cond(cond, 1, st);
@@ -539,6 +547,7 @@ __device__ inline void EpiTaBp::finish(double (&r)[K]) const {
     s->maint = MAINT_NONE;
   }
   ta_head(s);
+  tail();  // in-graph revalidation (SWITCH case 1): the loop condition
 }
 
 }  // namespace ts

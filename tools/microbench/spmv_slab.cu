@@ -126,6 +126,255 @@ __global__ void __launch_bounds__(kT, 1) k_slab(SlabStream S, const double* __re
   }
 }
 
+
+// ---------------------------------------------------------------- TMA ring --
+// The same slab layout streamed through per-warp shared-memory rings by bulk
+// copies (cp.async.bulk + mbarrier): each warp's run of slices is ONE
+// contiguous range of val[] and col[], so lane 0 keeps ST chunks of CH slots in
+// flight for its warp, independent of the register budget; the consumer reads
+// its operands from shared memory, lane-contiguous (conflict-free).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{ .reg .pred p; TS_WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; "
+      "@!p bra TS_WAIT_%=; }" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// MODE 0: full kernel; 1: no partial stores; 2: no x gather (constant)
+template <int NW, int ST, int CH, int MODE>
+__global__ void __launch_bounds__(NW * 32, 1) k_slab_tma(SlabStream S, const double* __restrict__ x,
+                                                         double* __restrict__ part, int xcap) {
+  constexpr int CK_ = CH / 32;  // k-steps per chunk
+  extern __shared__ __align__(128) unsigned char raw[];
+  double* xs = reinterpret_cast<double*>(raw);                           // [xcap]
+  double* rv = xs + xcap;                                                // [NW][ST][CH]
+  unsigned short* rc = reinterpret_cast<unsigned short*>(rv + (size_t)NW * ST * CH);  // [NW][ST][CH]
+  __shared__ __align__(8) unsigned long long full[NW * ST];
+  const int s = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int RUNS = 32 / NW;  // warp runs of the table per warp
+  const int cb0 = S.cb[s], cw = S.cb[s + 1] - cb0;
+  const int q0 = S.wr[s * 33 + w * RUNS], q1 = S.wr[s * 33 + (w + 1) * RUNS];
+  const int g0 = s * S.nsl;
+  const int E0 = __ldg(S.sp + g0 + q0), E1 = __ldg(S.sp + g0 + q1);
+  const int KT = (E1 - E0) >> 5;             // k-steps of this warp
+  const int NC = (KT + CK_ - 1) / CK_;       // chunks
+  double* mv = rv + (size_t)w * ST * CH;
+  unsigned short* mc = rc + (size_t)w * ST * CH;
+  unsigned long long* mb = full + w * ST;
+  auto issue = [&](int c) {  // lane 0
+    const int st = c % ST;
+    const int e = E0 + c * CH;
+    const int cnt = min(CH, E1 - e);
+    mbar_expect_tx(&mb[st], (unsigned)cnt * 10u);
+    bulk_g2s(mv + st * CH, S.val + e, (unsigned)cnt * 8u, &mb[st]);
+    bulk_g2s(mc + st * CH, S.col + e, (unsigned)cnt * 2u, &mb[st]);
+  };
+  if (lane == 0) {
+    for (int i = 0; i < ST; ++i) mbar_init(&mb[i], 1);
+    fence_mbar_init();
+    for (int c = 0; c < ST && c < NC; ++c) issue(c);
+  }
+  int nq = min(q1 - q0, 31);
+  int bnd = (lane <= nq && q0 < q1) ? __ldg(S.sp + g0 + q0 + lane) : 0;
+  int prow = (q0 < q1) ? __ldg(S.perm + (size_t)(g0 + q0) * 32 + lane) : -1;
+  for (int i = threadIdx.x; i < cw; i += NW * 32) xs[i] = __ldg(x + cb0 + i);
+  __syncthreads();
+  double* out = part + (size_t)s * S.m;
+  // slice bookkeeping: bounds of up to 31 slices live across the lanes of bnd
+  int qc = q0, j = 0;
+  int row = prow;
+  prow = (nq > 1) ? __ldg(S.perm + (size_t)(g0 + qc + 1) * 32 + lane) : -1;
+  int kend = (q0 < q1) ? (__shfl_sync(0xffffffffu, bnd, 1) - E0) >> 5 : 0;
+  double acc = 0.0;
+  auto emit = [&]() {  // the slice's rows are complete
+    if (MODE != 1) { if (row >= 0) out[row] = acc; }
+    acc = 0.0;
+    ++j;
+    if (j == nq) {  // next group of slice bounds
+      qc += nq;
+      j = 0;
+      nq = min(q1 - qc, 31);
+      if (nq > 0) {
+        bnd = (lane <= nq) ? __ldg(S.sp + g0 + qc + lane) : 0;
+        row = __ldg(S.perm + (size_t)(g0 + qc) * 32 + lane);
+        prow = (nq > 1) ? __ldg(S.perm + (size_t)(g0 + qc + 1) * 32 + lane) : -1;
+        kend = (__shfl_sync(0xffffffffu, bnd, 1) - E0) >> 5;
+      } else {
+        kend = 0x7fffffff;
+      }
+      return;
+    }
+    row = prow;
+    if (j + 1 < nq) prow = __ldg(S.perm + (size_t)(g0 + qc + j + 1) * 32 + lane);
+    kend = (__shfl_sync(0xffffffffu, bnd, j + 1) - E0) >> 5;
+  };
+  for (int c = 0; c < NC; ++c) {
+    const int st = c % ST;
+    mbar_wait(&mb[st], (unsigned)((c / ST) & 1));
+    const double* cv = mv + st * CH + lane;
+    const unsigned short* cc = mc + st * CH + lane;
+    const int kb = c * CK_;
+    const int kn = min(CK_, KT - kb);
+    constexpr int U = 8;
+    for (int k0 = 0; k0 < kn; k0 += U) {
+      double v[U];
+      unsigned ci_[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = k0 + u < kn;
+        v[u] = ok ? cv[32 * (k0 + u)] : 0.0;
+        ci_[u] = ok ? cc[32 * (k0 + u)] : 0xFFFFu;
+      }
+      double xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = (MODE == 2) ? 1.0 : (ci_[u] != 0xFFFFu ? xs[ci_[u]] : 0.0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = kb + k0 + u;
+        if (k0 + u >= kn) break;
+        while (k == kend) emit();
+        if (ci_[u] != 0xFFFFu) acc = fma(v[u], xv[u], acc);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && c + ST < NC) issue(c + ST);
+  }
+  while (qc < q1 && nq > 0) emit();
+}
+
+
+// ------------------------------------------------- smem-accumulated slab ----
+// Variant 2: (a) every slice's row sums go to shared memory in SLICE order
+// (conflict-free), no permutation load and no scattered global store inside
+// the stream; the block writes part[s][0..m) coalesced at the end through the
+// inverse permutation; (b) the slab's slice offsets live in shared memory;
+// (c) PIPE: register double buffering, the next batch of U k-steps is in
+// flight while the current one is consumed.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned map_peer(const void* p, unsigned rank) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double ld_dsmem(unsigned addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <int NW, int U, int PIPE, int CL = 1>
+__global__ void __launch_bounds__(NW * 32, 1) k_slab2(SlabStream S, const int* __restrict__ inv,
+                                                      const double* __restrict__ x, double* __restrict__ part,
+                                                      int xcap, unsigned long long* ts) {
+  extern __shared__ __align__(16) unsigned char raw2[];
+  double* xs = reinterpret_cast<double*>(raw2);   // [xcap]
+  double* accs = xs + xcap;                       // [nsl * 32]
+  int* sps = reinterpret_cast<int*>(accs + (size_t)S.nsl * 32);  // [nsl + 1]
+  __shared__ unsigned long long tl;
+  constexpr int NT_ = NW * 32;
+  constexpr int RUNS = 32 / NW;
+  const int s = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (ts && threadIdx.x == 0) { ts[s * 4 + 0] = gtimer(); tl = 0; }
+  const int cb0 = S.cb[s], cw = S.cb[s + 1] - cb0;
+  const int q0 = S.wr[s * 33 + w * RUNS], q1 = S.wr[s * 33 + (w + 1) * RUNS];
+  const int g0 = s * S.nsl;
+  const int E0 = __ldg(S.sp + g0 + q0), E1 = __ldg(S.sp + g0 + q1);
+  const int KT = (E1 - E0) >> 5;
+  const double* vp = S.val + E0 + lane;
+  const unsigned short* cp = S.col + E0 + lane;
+  double va[U], vb[U];
+  unsigned ca[U], cbf[U];
+  auto load = [&](double (&v)[U], unsigned (&c)[U], int k0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = k0 + u < KT;
+      v[u] = ok ? ld_stream(vp + 32 * (k0 + u)) : 0.0;
+      c[u] = ok ? ld_stream_u16(cp + 32 * (k0 + u)) : 0xFFFFu;
+    }
+  };
+  load(va, ca, 0);  // in flight with the staging below
+  for (int i = threadIdx.x; i <= S.nsl; i += NT_) sps[i] = __ldg(S.sp + g0 + i);
+  for (int i = threadIdx.x; i < cw; i += NT_) xs[i] = __ldg(x + cb0 + i);
+  __syncthreads();
+  if (ts && threadIdx.x == 0) ts[s * 4 + 1] = gtimer();
+  int q = q0;
+  int kend = q0 < q1 ? (sps[q0 + 1] - E0) >> 5 : 0x7fffffff;
+  double acc = 0.0;
+  auto emit = [&]() {
+    accs[q * 32 + lane] = acc;
+    acc = 0.0;
+    ++q;
+    kend = q < q1 ? (sps[q + 1] - E0) >> 5 : 0x7fffffff;
+  };
+  auto consume = [&](const double (&v)[U], const unsigned (&c)[U], int k0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u;
+      if (k >= KT) break;
+      while (k == kend) emit();
+      if (c[u] != 0xFFFFu) acc = fma(v[u], xs[c[u]], acc);
+    }
+  };
+  if (PIPE) {
+    for (int k0 = 0; k0 < KT; k0 += 2 * U) {
+      load(vb, cbf, k0 + U);
+      consume(va, ca, k0);
+      load(va, ca, k0 + 2 * U);
+      consume(vb, cbf, k0 + U);
+    }
+  } else {
+    for (int k0 = 0; k0 < KT; k0 += U) {
+      if (k0) load(va, ca, k0);
+      consume(va, ca, k0);
+    }
+  }
+  while (q < q1) emit();
+  if (ts && lane == 0) atomicMax(&tl, gtimer());
+  __syncthreads();
+  if (ts && threadIdx.x == 0) ts[s * 4 + 2] = tl;
+  if (CL == 1) {
+    double* out = part + (size_t)s * S.m;
+    const int* iv = inv + (size_t)s * S.m;
+    for (int r = threadIdx.x; r < S.m; r += NT_) out[r] = accs[__ldg(iv + r)];
+  } else {
+    // pair reduce over distributed shared memory: block `rank` of the pair owns
+    // rows [rank m/2, (rank+1) m/2): slab 2c's sum + slab 2c+1's sum, in that order
+    cluster_sync_all();
+    const int rank = s & 1, c = s >> 1;
+    const unsigned a0 = map_peer(accs, 0), a1 = map_peer(accs, 1);
+    const int* iv0 = inv + (size_t)(2 * c) * S.m;
+    const int* iv1 = iv0 + S.m;
+    double* out = part + (size_t)c * S.m;
+    const int rb = rank ? S.m / 2 : 0, re = rank ? S.m : S.m / 2;
+    for (int r = rb + threadIdx.x; r < re; r += NT_) {
+      const int i0 = __ldg(iv0 + r), i1 = __ldg(iv1 + r);
+      out[r] = ld_dsmem(a0 + 8u * i0) + ld_dsmem(a1 + 8u * i1);
+    }
+    cluster_sync_all();
+  }
+  if (ts) {
+    __syncthreads();
+    if (threadIdx.x == 0) ts[s * 4 + 3] = gtimer();
+  }
+}
+
 // 32 rows per block; warp g adds slabs g, g + 8, ... (4 loads in flight), the
 // 8 warp sums are combined in warp order: a fixed order
 __global__ void __launch_bounds__(256) k_sum(const double* __restrict__ part, int m, int P, double* y) {
@@ -172,6 +421,34 @@ __global__ void __launch_bounds__(NW * 32) k_sum32(const double* __restrict__ pa
       for (int u = 0; u < L; ++u) s += t[u];
     }
     for (; q < P; q += NW) s += __ldcg(part + (size_t)q * m + r);
+  }
+  red[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && r < m) {
+    double t = red[0][lane];
+    for (int j = 1; j < NW; ++j) t += red[j][lane];
+    y[r] = t;
+  }
+}
+
+// 32 rows per block; warp g adds the contiguous slab range [g P / NW, (g + 1) P / NW)
+// with up to L loads in flight, then the NW warp sums are added in warp order
+template <int NW, int L>
+__global__ void __launch_bounds__(NW * 32) k_sumA(const double* __restrict__ part, int m, int P, double* y) {
+  __shared__ double red[NW][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + lane;
+  const int qa = P * g / NW, qb = P * (g + 1) / NW;
+  double s = 0.0;
+  if (r < m) {
+    int q = qa;
+    for (; q < qb; q += L) {
+      double t[L];
+#pragma unroll
+      for (int u = 0; u < L; ++u) t[u] = q + u < qb ? __ldcg(part + (size_t)(q + u) * m + r) : 0.0;
+#pragma unroll
+      for (int u = 0; u < L; ++u) s += t[u];
+    }
   }
   red[g][lane] = s;
   __syncthreads();
@@ -371,6 +648,15 @@ int main() {
   sp[(size_t)P * nsl] = (int)slots;
   printf("C5 A v: %d slabs, widest %d columns (%.0f KB of x), %lld slots for %lld entries (%.2f %% padding)\n",
          P, maxw, maxw * 8.0 / 1024, slots, nnz, 100.0 * (slots - nnz) / nnz);
+  std::vector<int> hinv((size_t)P * m);
+  for (int s_ = 0; s_ < P; ++s_)
+    for (int i = 0; i < nsl * 32; ++i) {
+      const int r = perm[(size_t)s_ * nsl * 32 + i];
+      if (r >= 0) hinv[(size_t)s_ * m + r] = i;
+    }
+  int* dinv = up(hinv);
+  unsigned long long* dts;
+  CK(cudaMalloc(&dts, P * 4 * 8));
   SlabStream S{m, n, P, nsl, up(cb), up(sp), up(wr), up(perm), up(scol), up(sval)};
   double* x = up(hx);
   double *y, *part;
@@ -417,6 +703,91 @@ int main() {
       float t3 = timeit([&] { k_sum32<16><<<(m + 31) / 32, 512>>>(part, m, P, y); }, 20, fl);
       printf("      sum32x32 %.2f us, sum32x16 %.2f us\n", t2 * 1e3, t3 * 1e3);
     }
+
+#define SLABT(NW, ST, CH, MODE)                                                                          \
+    {                                                                                                    \
+      const int xcap = (maxw + 15) & ~15;                                                                \
+      const int sm_ = xcap * 8 + NW * ST * CH * 10;                                                      \
+      if (sm_ <= 232448 - 1024) {                                                                        \
+      CK(cudaFuncSetAttribute(k_slab_tma<NW, ST, CH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_)); \
+      float t = timeit([&] {                                                                             \
+        k_slab_tma<NW, ST, CH, MODE><<<P, NW * 32, sm_>>>(S, x, part, xcap);                             \
+        k_sum32<32><<<(m + 31) / 32, 1024>>>(part, m, P, y);                                             \
+      }, 20, fl);                                                                                        \
+      report("slab TMA NW" #NW " ST" #ST " CH" #CH " mode" #MODE " + sum32", t);                        \
+      float t1 = timeit([&] { k_slab_tma<NW, ST, CH, MODE><<<P, NW * 32, sm_>>>(S, x, part, xcap); }, 20, fl); \
+      printf("      slab kernel %.2f us (smem %d)\n", t1 * 1e3, sm_);                                    \
+      } else printf("slab TMA NW" #NW " ST" #ST " CH" #CH ": smem %d too large\n", sm_);                 \
+    }
+
+#define SLAB2(NW, U, PIPE)                                                                               \
+    {                                                                                                    \
+      const int xcap = (maxw + 15) & ~15;                                                                \
+      const int sm_ = xcap * 8 + nsl * 32 * 8 + (nsl + 1) * 4 + 16;                                      \
+      CK(cudaFuncSetAttribute(k_slab2<NW, U, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_));   \
+      float t = timeit([&] {                                                                             \
+        k_slab2<NW, U, PIPE><<<P, NW * 32, sm_>>>(S, dinv, x, part, xcap, nullptr);                       \
+        k_sum32<32><<<(m + 31) / 32, 1024>>>(part, m, P, y);                                             \
+      }, 20, fl);                                                                                        \
+      report("slab2 NW" #NW " U" #U " PIPE" #PIPE " + sum32", t);                                        \
+      float t1 = timeit([&] { k_slab2<NW, U, PIPE><<<P, NW * 32, sm_>>>(S, dinv, x, part, xcap, nullptr); }, 20, fl); \
+      if (fl) flush_l2();                                                                                \
+      k_slab2<NW, U, PIPE><<<P, NW * 32, sm_>>>(S, dinv, x, part, xcap, dts);                            \
+      CK(cudaDeviceSynchronize());                                                                       \
+      std::vector<unsigned long long> hts(P * 4);                                                        \
+      CK(cudaMemcpy(hts.data(), dts, P * 32, cudaMemcpyDeviceToHost));                                   \
+      unsigned long long T0 = ~0ull; double a0 = 0, a1 = 0, a2 = 0, a3 = 0, mx = 0;                       \
+      for (int b = 0; b < P; ++b) T0 = std::min(T0, hts[b * 4]);                                         \
+      for (int b = 0; b < P; ++b) { a0 += hts[b*4]-T0; a1 += hts[b*4+1]-T0; a2 += hts[b*4+2]-T0; a3 += hts[b*4+3]-T0; mx = std::max(mx, (double)(hts[b*4+3]-T0)); } \
+      printf("      slab kernel %.2f us; phases (mean over blocks, us from first start): start %.2f staged %.2f streamed %.2f flushed %.2f (max %.2f)\n", \
+             t1 * 1e3, a0 / P * 1e-3, a1 / P * 1e-3, a2 / P * 1e-3, a3 / P * 1e-3, mx * 1e-3);           \
+    }
+    SLAB2(32, 8, 0)
+    SLAB2(32, 4, 1)
+
+#define SLAB2C(NW, U, PIPE, SNW, SL)                                                                     \
+    {                                                                                                    \
+      const int xcap = (maxw + 15) & ~15;                                                                \
+      const int sm_ = xcap * 8 + nsl * 32 * 8 + (nsl + 1) * 4 + 16;                                      \
+      CK(cudaFuncSetAttribute(k_slab2<NW, U, PIPE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_)); \
+      cudaLaunchConfig_t cfg = {};                                                                       \
+      cfg.gridDim = dim3(P); cfg.blockDim = dim3(NW * 32); cfg.dynamicSmemBytes = sm_;                   \
+      cudaLaunchAttribute at[1];                                                                         \
+      at[0].id = cudaLaunchAttributeClusterDimension;                                                    \
+      at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;                \
+      cfg.attrs = at; cfg.numAttrs = 1;                                                                  \
+      unsigned long long* nots = nullptr;                                                                \
+      float t = timeit([&] {                                                                             \
+        CK(cudaLaunchKernelEx(&cfg, k_slab2<NW, U, PIPE, 2>, S, (const int*)dinv, (const double*)x, part, xcap, nots)); \
+        k_sumA<SNW, SL><<<(m + 31) / 32, SNW * 32>>>(part, m, P / 2, y);                                 \
+      }, 20, fl);                                                                                        \
+      report("slab2 pair NW" #NW " U" #U " PIPE" #PIPE " + sumA" #SNW "x" #SL, t);                       \
+      float t1 = timeit([&] { CK(cudaLaunchKernelEx(&cfg, k_slab2<NW, U, PIPE, 2>, S, (const int*)dinv, (const double*)x, part, xcap, nots)); }, 20, fl); \
+      float t2 = timeit([&] { k_sumA<SNW, SL><<<(m + 31) / 32, SNW * 32>>>(part, m, P / 2, y); }, 20, fl); \
+      if (fl) flush_l2();                                                                                \
+      CK(cudaLaunchKernelEx(&cfg, k_slab2<NW, U, PIPE, 2>, S, (const int*)dinv, (const double*)x, part, xcap, dts)); \
+      CK(cudaDeviceSynchronize());                                                                       \
+      std::vector<unsigned long long> hts(P * 4);                                                        \
+      CK(cudaMemcpy(hts.data(), dts, P * 32, cudaMemcpyDeviceToHost));                                   \
+      unsigned long long T0 = ~0ull; double a0 = 0, a1 = 0, a2 = 0, a3 = 0, mx = 0;                       \
+      for (int b = 0; b < P; ++b) T0 = std::min(T0, hts[b * 4]);                                         \
+      for (int b = 0; b < P; ++b) { a0 += hts[b*4]-T0; a1 += hts[b*4+1]-T0; a2 += hts[b*4+2]-T0; a3 += hts[b*4+3]-T0; mx = std::max(mx, (double)(hts[b*4+3]-T0)); } \
+      printf("      slab kernel %.2f us, sum %.2f us; phases: start %.2f staged %.2f streamed %.2f flushed %.2f (max %.2f)\n", \
+             t1 * 1e3, t2 * 1e3, a0 / P * 1e-3, a1 / P * 1e-3, a2 / P * 1e-3, a3 / P * 1e-3, mx * 1e-3); \
+    }
+    SLAB2C(32, 4, 1, 8, 10)
+    SLAB2C(32, 4, 1, 16, 5)
+    SLAB2C(32, 4, 1, 4, 10)
+    SLAB2C(32, 8, 0, 8, 10)
+    {
+      float a = timeit([&] { k_sumA<8, 10><<<(m + 31) / 32, 256>>>(part, m, P, y); }, 20, fl);
+      float b = timeit([&] { k_sumA<16, 10><<<(m + 31) / 32, 512>>>(part, m, P, y); }, 20, fl);
+      float c = timeit([&] { k_sumA<32, 5><<<(m + 31) / 32, 1024>>>(part, m, P, y); }, 20, fl);
+      float d = timeit([&] { k_sumA<8, 19><<<(m + 31) / 32, 256>>>(part, m, P, y); }, 20, fl);
+      float e = timeit([&] { k_sum32<32><<<1, 32>>>(part, 1, 1, y); }, 20, fl);
+      printf("      full-P sums: sumA8x10 %.2f sumA16x10 %.2f sumA32x5 %.2f sumA8x19 %.2f; empty kernel %.2f us\n", a * 1e3, b * 1e3, c * 1e3, d * 1e3, e * 1e3);
+    }
+    SLABT(32, 4, 128, 0)
   }
   return 0;
 }
