@@ -303,6 +303,58 @@ static void pass_T(Dev* D, const double* x, double xs, int use_xs, const Ops* op
   reduce_partials(D->bacc, D->facc, P, ops, red);
 }
 
+/* k_rows_wdense (small, L2-resident dense; ts_passes.cuh wdense_fits): one warp
+ * per row; lane l owns columns 64 k + 2 l, 64 k + 2 l + 1, chunk k feeds FMA
+ * chain k & 1, lanes are added by the xor butterfly; lane 0 of the warp runs
+ * the epilogue; rows of block b are [m b / P, m (b + 1) / P), warp w takes
+ * every 8th of them; block partials are reduced in block order. */
+static int wdense_fits(int64_t m, int64_t n) {
+  return n >= 128 && n <= 4096 && m >= 1 && 8 * m * n <= (32ll << 20);
+}
+static void rows_pass_warp(Dev* D, const double* a, int64_t lda, int64_t m, int64_t n, const double* x,
+                           double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx, double* red) {
+  const int K = ops->K;
+  Geo g = D->g;
+  g.m = m;
+  g.n = n;
+  int64_t P = (m + WARPS - 1) / WARPS;
+  if (P > resident(&g)) P = resident(&g);
+  if (P < 1) P = 1;
+  double* xv = (double*)malloc(sizeof(double) * (size_t)n);
+  for (int64_t c = 0; c < n; ++c) xv[c] = use_xs ? xs * x[c] : x[c];
+  for (int64_t b = 0; b < P; ++b) {
+    const int64_t r0 = m * b / P, r1 = m * (b + 1) / P;
+    double tv[KMAX][NT];
+    for (int k = 0; k < K; ++k)
+      for (int t = 0; t < NT; ++t) tv[k][t] = red_identity(ops->op[k]);
+    for (int w = 0; w < WARPS; ++w) {
+      double acc[KMAX];
+      for (int k = 0; k < K; ++k) acc[k] = red_identity(ops->op[k]);
+      for (int64_t r = r0 + w; r < r1; r += WARPS) {
+        const double* row = a + r * lda;
+        double lane[32];
+        for (int l = 0; l < 32; ++l) {
+          double a0 = 0.0, a1 = 0.0;
+          for (int64_t c0 = 0; c0 < n; c0 += 64 * 16)
+            for (int k = 0; k < 16; k += 2) {
+              const int64_t ca = c0 + 64 * k + 2 * l, cb = ca + 64;
+              if (ca < n) a0 = fma(row[ca], xv[ca], a0);
+              if (ca + 1 < n) a0 = fma(row[ca + 1], xv[ca + 1], a0);
+              if (cb < n) a1 = fma(row[cb], xv[cb], a1);
+              if (cb + 1 < n) a1 = fma(row[cb + 1], xv[cb + 1], a1);
+            }
+          lane[l] = a0 + a1;
+        }
+        elem(ctx, r, warp_reduce(lane, RED_SUM), acc);
+      }
+      for (int k = 0; k < K; ++k) tv[k][w * 32] = acc[k];
+    }
+    for (int k = 0; k < K; ++k) D->bacc[b * KMAX + k] = block_reduce1(tv[k], ops->op[k]);
+  }
+  free(xv);
+  reduce_partials(D->bacc, NULL, (int)P, ops, red);
+}
+
 /* k_rows_tile_fused: y = A x (x on the n side, optional scale).  The
  * (row, tile) partials do not depend on which block computes them; the
  * combine runs per 256-row group: one thread per row sums its tile partials
@@ -310,6 +362,10 @@ static void pass_T(Dev* D, const double* x, double xs, int use_xs, const Ops* op
  * reduced in group order. */
 static void rows_pass(Dev* D, const double* a, int64_t lda, int64_t m, int64_t n, const double* x,
                       double xs, int use_xs, const Ops* ops, ElemFn elem, void* ctx, double* red) {
+  if (wdense_fits(m, n)) {
+    rows_pass_warp(D, a, lda, m, n, x, xs, use_xs, ops, elem, ctx, red);
+    return;
+  }
   const int64_t nct = (n + TW - 1) / TW;
   for (int64_t ct = 0; ct < nct; ++ct) {
     const int64_t cb = ct * TW;

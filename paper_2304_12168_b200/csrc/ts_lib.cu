@@ -367,6 +367,12 @@ int plan_rows_dense(int64_t m, int64_t n, int sms, RowPlan* out, cudaStream_t) {
   } else {
     p.kind = PLAN_TILE;
     p.P = tile_grid(m, n, sms, kTileNBlocks);
+    // small and L2-resident: one warp per row (TS_DENSE_SMALL=tile keeps the tile kernel)
+    const char* e = getenv("TS_DENSE_SMALL");
+    if (wdense_fits(m, n) && !(e && !strcmp(e, "tile"))) {
+      p.wdense = 1;
+      p.P = wdense_grid(m, sms);
+    }
   }
   *out = p;
   return 0;
@@ -427,6 +433,17 @@ struct EpiIdxRange {
     out[1] = -r[1];
   }
 };
+
+// max |row - column| over the stored entries (the bandwidth of a square matrix)
+__global__ void k_csr_band(const int* rowid, const int* ci, int64_t nnz, int* out) {
+  int mx = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int d = rowid[k] - ci[k];
+    mx = max(mx, d < 0 ? -d : d);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0) atomicMax(out, mx);
+}
 
 __global__ void k_expand_rows(const int* rp, int64_t rows, int* rowid) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
@@ -951,6 +968,11 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
           if (A->ldaT != m) cudaMemsetAsync(A->aT, 0, (size_t)A->ldaT * n * sizeof(double), st);
           A->planT.kind = PLAN_TRANS;
           A->planT.P = tile_grid(n, m, A->sms, kTileNBlocks);
+          const char* se = getenv("TS_DENSE_SMALL");
+          if (wdense_fits(n, m) && !(se && !strcmp(se, "tile"))) {
+            A->planT.wdense = 1;
+            A->planT.P = wdense_grid(n, A->sms);
+          }
           A->npart = npart_elems(m, n) + npart_elems(n, m);  // disjoint A v / A^T v layouts
         }
       }
@@ -1017,6 +1039,7 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
       set_error("CSR upload failed");
       return fail(TS_ECUDA);
     }
+    int* dband = nullptr;
     if (nnz > 0) {
       // validate column indices on the device
       Work wk;
@@ -1040,6 +1063,9 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
           (rc = ar.get(&perm_out, nz)))
         return fail(rc);
       k_expand_rows<<<grid_for(m), 256, 0, st>>>(A->rp, m, rowid);
+      if ((rc = ar.get(&dband, 1))) return fail(rc);
+      cudaMemsetAsync(dband, 0, sizeof(int), st);
+      k_csr_band<<<grid_for(nnz), 256, 0, st>>>(rowid, A->ci, nnz, dband);
       k_iota<<<grid_for(nnz), 256, 0, st>>>(perm_in, nnz);
       int end_bit = 1;
       while (end_bit < 31 && ((int64_t)1 << end_bit) < n) ++end_bit;
@@ -1066,6 +1092,13 @@ int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const do
     if (d2h_pinned(rpT_h.data(), A->rpT, (n + 1) * sizeof(int), st) != cudaSuccess) {
       set_error("CSR transpose failed: %s", cudaGetErrorString(cudaGetLastError()));
       return fail(TS_ECUDA);
+    }
+    A->band = -1;
+    if (dband) {
+      int hb = 0;
+      if (d2h_pinned(&hb, dband, sizeof(int), st) == cudaSuccess) A->band = hb;
+    } else if (nnz == 0) {
+      A->band = 0;
     }
     {
       RowPlan pN, pT;

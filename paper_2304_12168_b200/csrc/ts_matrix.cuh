@@ -42,6 +42,7 @@ inline int64_t npart_elems(int64_t m, int64_t n) {
 
 struct RowPlan {
   int kind = PLAN_SHORT;
+  int wdense = 0;  // dense, small and L2-resident: one warp per row (k_rows_wdense)
   int P = 1;            // blocks
   int* wrow = nullptr;  // device [P * kWarps] (PLAN_FLAT)
   // PLAN_SELL: the sliced-ELL copy of this orientation (see k_rows_sell)
@@ -78,6 +79,7 @@ struct Mat {
   int *rp = nullptr, *ci = nullptr, *rpT = nullptr, *ciT = nullptr;
   double *val = nullptr, *valT = nullptr;
   double fro = 0.0;
+  int64_t band = -1;  // csr: max |row - column| over the stored entries (-1: unknown)
   RowPlan planN, planT;
   int Pmax = 0;  // largest grid any pass of this matrix uses
   // per-(tile,row) partials a solve's Work needs (dense tile A v)
@@ -169,12 +171,37 @@ inline int tile_grid(int64_t m, int64_t n, int sms, int per_sm = kMinBlocks, int
 
 // ------------------------------------------------------------ dispatch ----
 // y = M v (trans = 0) or y = M^T v (trans = 1) with a fused epilogue.
+// A square banded L2-resident CSR matrix runs a CTA moments pair as one kernel
+// (k_pair_band); TS_BAND_PAIR=0 keeps the two passes
+inline size_t band_pair_smem(const Mat& M) {
+  const int64_t P = M.planN.P > 0 ? M.planN.P : 1;
+  return (size_t)((M.m + P - 1) / P + 1 + 2 * M.band) * sizeof(double);
+}
+inline bool band_pair_ok(const Mat& M) {
+  static const bool off = [] {
+    const char* e = getenv("TS_BAND_PAIR");
+    return e && e[0] == '0';
+  }();
+  return !off && M.kind == 1 && !M.comm && M.m == M.n && M.band >= 0 && M.band <= 512 &&
+         M.planN.kind == PLAN_SHORT && M.planT.kind == PLAN_SHORT && M.planN.P == M.planT.P &&
+         M.band * 8 <= (M.m + M.planN.P - 1) / M.planN.P && band_pair_smem(M) <= 40 * 1024;
+}
+template <class EpiQ, class EpiP>
+int launch_pair_band(const Mat& M, const double* pprev, const EpiQ& eq, const EpiP& ep, const Work& wk,
+                     cudaStream_t st) {
+  k_pair_band<EpiQ, EpiP><<<M.planN.P, kNT, band_pair_smem(M), st>>>(M.csrT(), M.csr(), pprev, (int)M.band, eq, ep, wk);
+  TS_CUDA(cudaGetLastError());
+  return 0;
+}
+
 template <class Epi>
 int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi, const Work& wk,
                 cudaStream_t st) {
   if (M.kind == 0) {
     if (!trans) {
-      if (M.planN.kind == PLAN_TILE)
+      if (M.planN.wdense)
+        k_rows_wdense<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+      else if (M.planN.kind == PLAN_TILE)
         k_rows_tile_fused<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
       else
         k_rows_short<DenseRows, Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
@@ -183,7 +210,10 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
       // counters must stay zero between launches (self-resetting)
       Work wt = wk;
       wt.npart = wk.npart + npart_elems(M.m, M.n);
-      k_rows_tile_fused<Epi><<<M.planT.P, kNT, 0, st>>>(DenseRows{M.aT, M.ldaT, M.n, M.m}, x, xs, epi, wt);
+      if (M.planT.wdense)
+        k_rows_wdense<Epi><<<M.planT.P, kNT, 0, st>>>(DenseRows{M.aT, M.ldaT, M.n, M.m}, x, xs, epi, wt);
+      else
+        k_rows_tile_fused<Epi><<<M.planT.P, kNT, 0, st>>>(DenseRows{M.aT, M.ldaT, M.n, M.m}, x, xs, epi, wt);
     } else {
       k_cols_tile<Epi, 2><<<M.planT.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
     }

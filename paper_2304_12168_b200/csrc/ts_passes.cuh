@@ -391,6 +391,128 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_short(Acc A, const dou
   body_rows_short<Acc, Epi, false>(A, x, xs, epi, wk, blockIdx.x, gridDim.x, kb, ke);
 }
 
+// ------------------------------------------------------------ k_pair_band ----
+// One CTA moments pair in ONE kernel for a square banded CSR matrix that is
+// L2-resident (C3: tridiagonal, n = 100001): q = A^T p, then p' = A q.  A pass
+// over such a matrix is a chain of dependent latencies, and the pair needs a
+// grid-wide dependency only because p'_i reads q at the columns of row i —
+// with bandwidth bw those are [i - bw, i + bw].  So block b, owning rows [R0,
+// R1), computes q on [R0 - bw, R1 + bw) into shared memory (the halo rows
+// redundantly, from p which is complete), stores its own q rows and runs the
+// q epilogue on them, then computes p' on its rows from shared memory and
+// runs the p' epilogue; one reduction of both epilogues' sums, the last block
+// finishes both.  Every row keeps scipy's operation sequence (left to right,
+// no FMA) and the thread <-> row mapping of k_rows_short, so q, p' and their
+// block sums are the bits the two separate passes produce.
+struct OpsSum {
+  __device__ __forceinline__ int op(int) const { return RED_SUM; }
+};
+
+// scipy csr_matvec order over entries [k0, k1) with a generic gather pointer
+__device__ __forceinline__ double row_serial_any(const CsrRows& A, int k0, int k1, const double* xq) {
+  double s = 0.0;
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    double v[4], xv[4];
+    int j[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = ld_stream(A.val + k + u);
+      j[u] = ld_stream_i(A.ci + k + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = xq[j[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+  }
+  const int rem = k1 - k;
+  double v[3], xv[3];
+  int j[3];
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (u < rem) {
+      v[u] = ld_stream(A.val + k + u);
+      j[u] = ld_stream_i(A.ci + k + u);
+    }
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (u < rem) xv[u] = xq[j[u]];
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (u < rem) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+  return s;
+}
+
+template <class EpiQ, class EpiP>
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_pair_band(CsrRows AT, CsrRows A, const double* pprev, int bw,
+                                                             EpiQ eq, EpiP ep, Work wk) {
+  constexpr int KQ = EpiQ::K, KP = EpiP::K, K = KQ + KP;
+  extern __shared__ double qs[];  // q on [lo, hi)
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ep.count_launch();
+  const int64_t m = A.m, P = gridDim.x, b = blockIdx.x;
+  const int64_t R0 = m * b / P, R1 = m * (b + 1) / P;
+  const int64_t lo = R0 - bw > 0 ? R0 - bw : 0, hi = R1 + bw < m ? R1 + bw : m;
+  // the first row's bounds do not depend on the state word
+  int64_t j = R0 + threadIdx.x;
+  int kb = 0, ke = 0;
+  if (j < R1) {
+    kb = __ldg(AT.rp + j);
+    ke = __ldg(AT.rp + j + 1);
+  }
+  if (!ep.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ep.idle();
+    return;
+  }
+  ktimer_begin(ep.timer());
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  double (&aq)[KQ] = *reinterpret_cast<double (*)[KQ]>(&acc[0]);
+  double (&ap)[KP] = *reinterpret_cast<double (*)[KP]>(&acc[KQ]);
+  // q on the block's own rows (k_rows_short's thread <-> row mapping), then the halo rows
+  for (bool first = true; j < R1; j += kNT, first = false) {
+    if (!first) {
+      kb = __ldg(AT.rp + j);
+      ke = __ldg(AT.rp + j + 1);
+    }
+    const double qv = row_serial_any(AT, kb, ke, pprev);
+    qs[j - lo] = qv;
+    eq.elem(j, qv, aq);
+  }
+  for (int64_t h = lo + threadIdx.x; h < R0; h += kNT)
+    qs[h - lo] = row_serial_any(AT, __ldg(AT.rp + h), __ldg(AT.rp + h + 1), pprev);
+  for (int64_t h = R1 + threadIdx.x; h < hi; h += kNT)
+    qs[h - lo] = row_serial_any(AT, __ldg(AT.rp + h), __ldg(AT.rp + h + 1), pprev);
+  __syncthreads();
+  const double* xq = qs - lo;
+  for (int64_t r = R0 + threadIdx.x; r < R1; r += kNT)
+    ep.elem(r, row_serial_any(A, __ldg(A.rp + r), __ldg(A.rp + r + 1), xq), ap);
+  const OpsSum ops;
+  block_reduce<K>(acc, sm, ops);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, ops);
+    if (threadIdx.x == 0) {
+      ktimer_end(ep.timer());
+      double rq[KQ], rp2[KP];
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) rq[k] = red[k];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) rp2[k] = red[KQ + k];
+      eq.finish(rq);
+      ep.finish(rp2);
+    }
+    __syncthreads();
+    ep.finish_block();
+  }
+}
+
 // ----------------------------------------------------------- k_rows_sell ----
 // Short CSR rows, HBM-sized (C4 both ways, C5's A^T v): a sliced-ELL copy
 // (SELL-32) built once at matrix creation.  Slice s holds rows [32 s, 32 s +
@@ -862,6 +984,100 @@ __global__ void __launch_bounds__(kNT, kTileTBlocks) k_cols_tile(DenseRows A, co
     return;
   }
   body_cols_tile<Epi, VW, false, kTileTRows>(A, x, xs, epi, wk, blockIdx.x, gridDim.x);
+}
+
+// ---------------------------------------------------------- k_rows_wdense ----
+// Small dense A v (L2-resident, n <= kWdMaxN; C1 both ways, A^T v over the
+// transposed copy): the pass is a chain of dependent latencies, not a stream,
+// so the chain is kept as short as it gets — ONE warp per row, the whole x in
+// shared memory, the row's first 1024 columns in flight before x is staged,
+// the epilogue straight from the warp sum, one block reduction, the last
+// block finishes.  No (tile, row) partials, no group counters, no combine
+// stage (k_rows_tile_fused on C1: 7.2-8.2 us per pass).  Lane l owns columns
+// 64 k + 2 l, 64 k + 2 l + 1; chunk k feeds FMA chain k & 1; lanes are added
+// by the xor butterfly.
+constexpr int kWdMaxN = 4096;   // x in 32 KB of shared memory
+constexpr int kWdChunks = 16;   // 64-column chunks of a row in flight per lane
+
+__host__ __device__ inline bool wdense_fits(int64_t m, int64_t n) {
+  return n >= 128 && n <= kWdMaxN && m >= 1 && 8 * m * n <= (32ll << 20);
+}
+inline int wdense_grid(int64_t m, int sms) {
+  int64_t p = (m + kWarps - 1) / kWarps;
+  const int64_t pmax = (int64_t)sms * kMinBlocks;
+  if (p > pmax) p = pmax;
+  return (int)(p < 1 ? 1 : p);
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(kNT, 2) k_rows_wdense(DenseRows A, const double* __restrict__ x, XS xs, Epi epi,
+                                                       Work wk) {
+  constexpr int K = Epi::K;
+  constexpr int C = kWdChunks;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ __align__(16) double xsl[kWdMaxN + 64];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  const int64_t m = A.m, n = A.n, lda = A.lda, P = gridDim.x, b = blockIdx.x;
+  const int64_t r0 = m * b / P, r1 = m * (b + 1) / P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // the matrix does not depend on the solver state: the first row's leading
+  // chunks are in flight with the state word and the x slab
+  double2 v[C];
+  auto load = [&](int64_t r, int64_t c0) {
+    const double* row = A.a + r * lda + 2 * lane;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int64_t c = c0 + 64 * k + 2 * lane;
+      v[k] = c < lda ? ld_stream2(row + c0 + 64 * k) : make_double2(0.0, 0.0);
+    }
+  };
+  int64_t r = r0 + wid;
+  if (r < r1) load(r, 0);
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  xs.load();
+  ktimer_begin(epi.timer());
+  __shared__ double epi_smem[kEpiSmem];
+  epi.prepare(epi_smem);
+  const int npad = (int)((n + 63) & ~(int64_t)63);
+  for (int k = threadIdx.x; k < npad; k += kNT) xsl[k] = k < n ? xs(__ldg(x + k)) : 0.0;
+  __syncthreads();
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  bool first = true;
+  for (; r < r1; r += kWarps) {
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t c0 = 0; c0 < n; c0 += 64 * C) {
+      if (!(first && c0 == 0)) load(r, c0);
+#pragma unroll
+      for (int k = 0; k < C; k += 2) {
+        const int64_t ca = c0 + 64 * k + 2 * lane, cb = ca + 64;
+        if (ca < n) {
+          const double2 xa = *reinterpret_cast<const double2*>(xsl + ca);
+          a0 = fma(v[k].x, xa.x, a0);
+          if (ca + 1 < n) a0 = fma(v[k].y, xa.y, a0);
+        }
+        if (cb < n) {
+          const double2 xb = *reinterpret_cast<const double2*>(xsl + cb);
+          a1 = fma(v[k + 1].x, xb.x, a1);
+          if (cb + 1 < n) a1 = fma(v[k + 1].y, xb.y, a1);
+        }
+      }
+    }
+    first = false;
+    const double y = warp_reduce(a0 + a1, RED_SUM);
+    if (lane == 0) epi.elem(r, y, acc);
+  }
+  block_reduce<K>(acc, sm, epi);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[blockIdx.x * kKMax + k] = acc[k];
+  }
+  finish_last(epi, wk, nullptr, (int)gridDim.x, sm, &sflag);
 }
 
 // ------------------------------------------------------ k_rows_tile_fused ----
