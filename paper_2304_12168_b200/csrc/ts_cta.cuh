@@ -221,6 +221,7 @@ __device__ inline void cta_head(SolveState* s) {
     return;
   }
   s->t = sched_order(s->t_max, s->sched_pos);
+  s->slot = s->t_max == 1 ? 0 : s->sched_pos % (2 * s->t_max - 2);
   s->sched_pos += 1;
 }
 
@@ -283,7 +284,7 @@ struct EpiCtaQ : EpiBase {
   static constexpr int K = 1;
   double* q;
   int i;
-  __device__ bool active() const { return cta_pair_active(st, i); }
+  __device__ bool active() const { return cta_pair_active(st, i) && slot_ok(st, slot); }
   __device__ void elem(int64_t j, double y, double (&acc)[K]) const {
     q[j] = y;
     acc[0] = fma(y, y, acc[0]);
@@ -300,7 +301,7 @@ struct EpiCtaP : EpiBase {
   const double* pprev;
   double* p;
   int i;
-  __device__ bool active() const { return cta_pair_active(st, i); }
+  __device__ bool active() const { return cta_pair_active(st, i) && slot_ok(st, slot); }
   __device__ void elem(int64_t r, double y, double (&acc)[K]) const {
     p[r] = y;
     acc[0] = fma(pprev[r], y, acc[0]);
@@ -332,8 +333,10 @@ struct EpiCtaP : EpiBase {
       t0 = globaltimer();
     }
     __syncthreads();
-    const int o = threadIdx.x + 1;
-    if (o <= st->t) {
+    // one WARP per order: the orders run different code (hankel_T<o>), so lanes
+    // of one warp would run them one after another
+    const int o = (threadIdx.x >> 5) + 1;
+    if ((threadIdx.x & 31) == 0 && o <= st->t) {
       if (!hankel_min_norm(st->phi, o, st->rcond, st->alpha_o[o - 1])) atomicExch(&bad, 1);
     }
     __syncthreads();
@@ -376,7 +379,7 @@ struct EpiCtaCand : EpiBase {
   int64_t m;
   int t_c = 0;
   const double* al_s = nullptr;  // block copy of alpha_o (shared memory)
-  __device__ bool active() const { return running(st); }
+  __device__ bool active() const { return running(st) && slot_ok(st, slot); }
   __device__ void prepare(double* smem) {
     t_c = st->t;
     for (int k = threadIdx.x; k < kTMax * kTMax; k += kNT) smem[k] = (&st->alpha_o[0][0])[k];
@@ -493,7 +496,7 @@ struct EpiCtaUpd : EpiBase {
   int o_c = 0, blend_c = 0;
   double w_c = 0.0;
   const double* al_s = nullptr;
-  __device__ bool active() const { return running(st); }
+  __device__ bool active() const { return running(st) && slot_ok(st, slot); }
   __device__ void prepare(double* smem) {
     o_c = st->sel_order;
     blend_c = st->blend;
@@ -734,7 +737,10 @@ struct EpiCtaRecheck : EpiBase {
   static constexpr int K = 2;
   const double* b;
   double* r;
-  __device__ bool active() const { return st->status == TS_RUNNING; }
+  int need_maint = 0;  // in-graph recheck: runs only when that maintenance is due
+  __device__ bool active() const {
+    return st->status == TS_RUNNING && (!need_maint || st->maint == need_maint);
+  }
   __device__ void elem(int64_t i, double y, double (&acc)[K]) const {
     const double f = __dsub_rn(b[i], y);
     const double d = __dsub_rn(f, r[i]);

@@ -753,29 +753,29 @@ static int cta_probe_finish(const CtaOp& op, const Instance* I, cudaStream_t s) 
 // moments pairs for orders 1..npairs (predicated on state t); `solve_last`
 // makes the pair that equals the state's t run the Hankel solves
 static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, int solve_last,
-                     cudaStream_t s) {
+                     cudaStream_t s, int slot = -1) {
   const bool pair = gram && !op.normal && band_pair_ok(op.M);
   for (int i = 1; i <= npairs; ++i) {
     if (pair) {  // q_i = A^T p_{i-1} and p_i = A q_i in one kernel (square banded, L2-resident)
       EpiCtaQ eq;
-      eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i; eq.tclass = 1;
+      eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i; eq.tclass = 1; eq.slot = slot;
       EpiCtaP ep;
       ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
-      ep.with_solve = solve_last; ep.tclass = 0;
+      ep.with_solve = solve_last; ep.tclass = 0; ep.slot = slot;
       ++g_launches;
       TS_CHECK(launch_pair_band(op.M, I->kp.p[i - 1], eq, ep, I->wk, s));
     } else if (gram) {
       EpiCtaQ eq;
-      eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i;
+      eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i; eq.slot = slot;
       TS_CHECK(op.T(I->kp.p[i - 1], eq, s));
       EpiCtaP ep;
       ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
-      ep.with_solve = solve_last;
+      ep.with_solve = solve_last; ep.slot = slot;
       TS_CHECK(op.N(I->kp.q[i - 1], ep, s));
     } else {
       EpiCtaP ep;
       ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
-      ep.with_solve = solve_last;
+      ep.with_solve = solve_last; ep.slot = slot;
       TS_CHECK(op.N(I->kp.p[i - 1], ep, s));
     }
   }
@@ -786,17 +786,17 @@ static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, i
 // finisher), candidate norms / retry rule, fused r / x update (tail)
 static int cta_step_kernels(const CtaOp& op, const Instance* I, int npairs, int gram, cudaStream_t s,
                             cudaGraphConditionalHandle h, int use, int enhanced = 0,
-                            cudaGraphConditionalHandle hsw = 0, int ncases = 0) {
-  TS_CHECK(cta_pairs(op, I, npairs, gram, 1, s));
+                            cudaGraphConditionalHandle hsw = 0, int ncases = 0, int slot = -1) {
+  TS_CHECK(cta_pairs(op, I, npairs, gram, 1, s, slot));
   if (enhanced) TS_CHECK(cta_probe_kernels(op, I, npairs, gram, s));
   const int64_t mo = op.mo(), no = op.no();
   EpiCtaCand ecd;
-  ecd.st = I->ds; ecd.kp = I->kp; ecd.m = mo;
+  ecd.st = I->ds; ecd.kp = I->kp; ecd.m = mo; ecd.slot = slot;
   TS_CHECK(vecpass(op.M, mo, ecd, I->wk, s));
   EpiCtaUpd eu;
   eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = mo;
   eu.n = no; eu.gram = gram;
-  eu.sw = hsw; eu.use_sw = ncases > 0; eu.ncases = ncases;
+  eu.sw = hsw; eu.use_sw = ncases > 0; eu.ncases = ncases; eu.slot = slot;
   return vecpass(op.M, std::max(mo, no), eu, I->wk, s);
 }
 
@@ -852,13 +852,13 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   };
   // ||x||, then r = b - A x against the maintained residual
   auto recheck = [&](cudaStream_t s, cudaGraphConditionalHandle hw, int use, cudaGraphConditionalHandle hsw,
-                     int nocase) -> int {
+                     int nocase, int need_maint = 0) -> int {
     EpiNormTo en;
-    en.st = ds; en.v = I->x; en.len = no; en.what = 1;
+    en.st = ds; en.v = I->x; en.len = no; en.what = 1; en.need_maint = need_maint;
     TS_CHECK(vecpass(M, no, en, wk, s));
     EpiCtaRecheck er;
-    er.st = ds; er.b = I->b; er.r = I->kp.p[0];
-    er.cond = hw; er.use_cond = use; er.sw = hsw; er.use_sw = use; er.nocase = nocase;
+    er.st = ds; er.b = I->b; er.r = I->kp.p[0]; er.need_maint = need_maint;
+    er.cond = hw; er.use_cond = use; er.sw = hsw; er.use_sw = use && nocase > 0; er.nocase = nocase;
     return op.N(I->x, er, s);
   };
   // graph: [head: switch = t - 1] -> WHILE{ SWITCH{order 1 .. t_max} }: each case
@@ -868,7 +868,28 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
   // per iteration (tools/microbench/cond_handle.cu: a case kernel may set the
   // value the next trip's SWITCH reads; the first value may come from a
   // kernel node in the outer graph)
+  // Default (plain CTA): no SWITCH at all.  One WHILE trip is one PERIOD of
+  // the triangle-wave order schedule (2 t_max - 2 iterations); every
+  // iteration's kernels are baked in with their schedule slot and run when the
+  // state stands at that slot, so the conditional nodes cost one WHILE
+  // evaluation per period instead of a WHILE and a SWITCH evaluation per
+  // iteration (tools/microbench/lat_chain.cu: 3.5 + 3 us).  The recheck
+  // kernels open every trip and idle unless it is due.  A solve that stops,
+  // or re-enters, in mid-period idles through the rest of that trip.
+  static const bool force_switch = getenv("TS_CTA_SWITCH") != nullptr;
+  const int period = a.t_max == 1 ? 1 : 2 * a.t_max - 2;
+  GraphFn gperiod = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
+    return capture_into(cap, bodyg, [&](cudaStream_t s) -> int {
+      TS_CHECK(recheck(s, 0, 0, 0, 0, MAINT_RECHECK));
+      for (int slot = 0; slot < period; ++slot) {
+        const int t = a.t_max == 1 ? 1 : (slot < a.t_max ? slot + 1 : 2 * a.t_max - 1 - slot);
+        TS_CHECK(cta_step_kernels(op, I, t, a.gram, s, hw, 1, 0, 0, 0, slot));
+      }
+      return 0;
+    });
+  };
   GraphFn gbody = [&](cudaGraph_t bodyg, cudaGraphConditionalHandle hw, cudaStream_t cap) -> int {
+    if (!a.enhanced && !force_switch && period <= 16) return gperiod(bodyg, hw, cap);
     cudaGraphConditionalHandle hsw;
     TS_CUDA(cudaGraphConditionalHandleCreate(&hsw, bodyg, 0, 0));
     {

@@ -170,6 +170,22 @@ template <class Epi>
 __device__ __forceinline__ void finish_last(Epi& epi, const Work& wk, const double* facc, int nb,
                                             double* sm, int* sflag) {
   constexpr int K = Epi::K;
+  if (nb == 1 && !facc) {
+    // a single block (vector passes of small systems): no arrival counter, no
+    // fences, no reload — the value reduce_partials would return (identity
+    // combined with the block's sums, then zeros added across the block)
+    if (threadIdx.x == 0) {
+      double red[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        red[k] = red_combine(epi.op(k), red_identity(epi.op(k)), wk.bacc[blockIdx.x * kKMax + k]);
+      ktimer_end(epi.timer());
+      epi.finish(red);
+    }
+    __syncthreads();
+    epi.finish_block();
+    return;
+  }
   if (arrive_last(wk.done, (unsigned)nb, sflag)) {
     double red[K];
     reduce_partials<K>(wk.bacc, facc, nb, red, sm, epi);
@@ -454,13 +470,11 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_pair_band(CsrRows AT, CsrRo
   const int64_t m = A.m, P = gridDim.x, b = blockIdx.x;
   const int64_t R0 = m * b / P, R1 = m * (b + 1) / P;
   const int64_t lo = R0 - bw > 0 ? R0 - bw : 0, hi = R1 + bw < m ? R1 + bw : m;
-  // the first row's bounds do not depend on the state word
+  // p is complete and the matrix immutable: the thread's first q row is computed
+  // (loads and arithmetic only) while the state word is in flight
   int64_t j = R0 + threadIdx.x;
-  int kb = 0, ke = 0;
-  if (j < R1) {
-    kb = __ldg(AT.rp + j);
-    ke = __ldg(AT.rp + j + 1);
-  }
+  double qfirst = 0.0;
+  if (j < R1) qfirst = row_serial_any(AT, __ldg(AT.rp + j), __ldg(AT.rp + j + 1), pprev);
   if (!ep.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) ep.idle();
     return;
@@ -473,11 +487,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_pair_band(CsrRows AT, CsrRo
   double (&ap)[KP] = *reinterpret_cast<double (*)[KP]>(&acc[KQ]);
   // q on the block's own rows (k_rows_short's thread <-> row mapping), then the halo rows
   for (bool first = true; j < R1; j += kNT, first = false) {
-    if (!first) {
-      kb = __ldg(AT.rp + j);
-      ke = __ldg(AT.rp + j + 1);
-    }
-    const double qv = row_serial_any(AT, kb, ke, pprev);
+    const double qv = first ? qfirst : row_serial_any(AT, __ldg(AT.rp + j), __ldg(AT.rp + j + 1), pprev);
     qs[j - lo] = qv;
     eq.elem(j, qv, aq);
   }
@@ -1034,6 +1044,14 @@ __global__ void __launch_bounds__(kNT, 2) k_rows_wdense(DenseRows A, const doubl
   };
   int64_t r = r0 + wid;
   if (r < r1) load(r, 0);
+  // x is complete (the previous kernel wrote it): its loads go out before the state word too
+  const int npad = (int)((n + 63) & ~(int64_t)63);
+  double xr[kWdMaxN / kNT];
+#pragma unroll
+  for (int q = 0; q < kWdMaxN / kNT; ++q) {
+    const int k = threadIdx.x + q * kNT;
+    xr[q] = k < n ? __ldg(x + k) : 0.0;
+  }
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
@@ -1042,8 +1060,11 @@ __global__ void __launch_bounds__(kNT, 2) k_rows_wdense(DenseRows A, const doubl
   ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
-  const int npad = (int)((n + 63) & ~(int64_t)63);
-  for (int k = threadIdx.x; k < npad; k += kNT) xsl[k] = k < n ? xs(__ldg(x + k)) : 0.0;
+#pragma unroll
+  for (int q = 0; q < kWdMaxN / kNT; ++q) {
+    const int k = threadIdx.x + q * kNT;
+    if (k < npad) xsl[k] = k < n ? xs(xr[q]) : 0.0;
+  }
   __syncthreads();
   double acc[K];
 #pragma unroll

@@ -29,7 +29,7 @@ struct alignas(16) SolveState {
   int halvings_left, since_reval, has_lb, warm;
   int t, sched_pos, t_max, sel_order;
   int slow_steps, blend, known_solvable, accelerate;
-  int accel_patience, enhanced, seg_cap, pad0;
+  int accel_patience, enhanced, seg_cap, slot;  // slot: position in the order schedule's period
   long long iterations, max_iters, recheck_every;
   long long m_rows, n_cols;
   long long trace_count, trace_flushed, body_runs, launches;
@@ -204,6 +204,7 @@ struct EpiBase {
   int use_cond = 0;
   int use_sw = 0;
   int tclass = -1;  // live accounting class (set by the launch helper)
+  int slot = -1;    // CTA period graph: the schedule slot this kernel belongs to (-1: any)
   // vector passes: reduction slots that sum over n-space (column-sharded)
   static constexpr unsigned kShardMask = 0;
   // vector passes: true -> the epilogue provides elem2(i, acc) for elements
@@ -234,6 +235,12 @@ struct EpiBase {
 
 __device__ __forceinline__ bool running(const SolveState* s) {
   return s->status == TS_RUNNING && s->maint == MAINT_NONE;
+}
+// CTA period graph (one WHILE trip = one period of the order schedule, every
+// iteration's kernels baked in with their slot): a kernel runs when the state
+// stands at its slot and the trace ring has room for the iteration's row
+__device__ __forceinline__ bool slot_ok(const SolveState* s, int slot) {
+  return slot < 0 || (s->slot == slot && (s->trace_count - s->trace_flushed) < (long long)s->seg_cap);
 }
 
 // TA init without warm start: b' = 0, gap = b.  sums: gap.gap, gap.b, b.b
@@ -284,7 +291,10 @@ struct EpiNormTo : EpiBase {
   const double* v;
   int64_t len;
   int what;  // 0: ta x0 (rho / warm flag), 1: cta x norm (recheck)
-  __device__ bool active() const { return st->status == TS_RUNNING; }
+  int need_maint = 0;  // in-graph recheck: runs only when that maintenance is due
+  __device__ bool active() const {
+    return st->status == TS_RUNNING && (!need_maint || st->maint == need_maint);
+  }
   __device__ void elem(int64_t i, double (&acc)[K]) const {
     const double a = v[i];
     acc[0] = fma(a, a, acc[0]);

@@ -337,6 +337,72 @@ int main() {
         CK(cudaGraphExecDestroy(we));
         CK(cudaGraphDestroy(wg));
       }
+  // per-trip cost of the conditional nodes: WHILE{K passes} for several K, and
+  // WHILE{SWITCH{K passes}} (the case is re-selected by the last pass of a trip)
+  for (int sw = 0; sw < 2; ++sw)
+    for (int K2 : {1, 2, 4, 8, 16}) {
+      const int P = sms, REP2 = 400;
+      Args a = {};
+      a.lo = dlo; a.di = ddi; a.up = dup; a.bacc = bacc; a.ticket = ticket; a.state = state;
+      a.trips = trips; a.n = n; a.pdl = 0;
+      const double st0[2] = {1.0, 0.0};
+      CK(cudaMemcpy(state, st0, 16, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(x0, x.data(), n * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemset(ticket, 0, 16));
+      cudaGraph_t wg;
+      CK(cudaGraphCreate(&wg, 0));
+      cudaGraphConditionalHandle h;
+      CK(cudaGraphConditionalHandleCreate(&h, wg, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams np = {};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = h;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      CK(cudaGraphAddNode(&node, wg, nullptr, 0, &np));
+      cudaGraph_t body = np.conditional.phGraph_out[0];
+      cudaGraph_t target = body;
+      if (sw) {
+        cudaGraphConditionalHandle hs;
+        CK(cudaGraphConditionalHandleCreate(&hs, body, 0, cudaGraphCondAssignDefault));  // always case 0
+        cudaGraphNodeParams sp = {};
+        sp.type = cudaGraphNodeTypeConditional;
+        sp.conditional.handle = hs;
+        sp.conditional.type = cudaGraphCondTypeSwitch;
+        sp.conditional.size = 2;
+        cudaGraphNode_t sn;
+        CK(cudaGraphAddNode(&sn, body, nullptr, 0, &sp));
+        target = sp.conditional.phGraph_out[0];
+      }
+      CK(cudaStreamBeginCaptureToGraph(s, target, nullptr, nullptr, 0, cudaStreamCaptureModeGlobal));
+      for (int k = 0; k < K2; ++k) {
+        Args c = a;
+        c.x = (k & 1) ? x1 : x0;
+        c.y = (k & 1) ? x0 : x1;
+        c.use_cond = k == K2 - 1;
+        c.h = h;
+        c.stop = REP2;
+        launch(s, c, P, 0);
+      }
+      CK(cudaStreamEndCapture(s, &target));
+      cudaGraphExec_t we;
+      CK(cudaGraphInstantiate(&we, wg, 0));
+      float ms = 0;
+      for (int w = 0; w < 3; ++w) {
+        CK(cudaMemset(trips, 0, 8));
+        CK(cudaEventRecord(e0, s));
+        CK(cudaGraphLaunch(we, s));
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms, e0, e1);
+      }
+      unsigned long long tr;
+      CK(cudaMemcpy(&tr, trips, 8, cudaMemcpyDeviceToHost));
+      printf("WHILE%s K=%2d : %7.2f us/trip = %6.2f us/pass  (%llu trips)\n", sw ? "{SWITCH}" : "        ", K2,
+             ms * 1e3 / tr, ms * 1e3 / (tr * K2), tr);
+      CK(cudaGraphExecDestroy(we));
+      CK(cudaGraphDestroy(wg));
+    }
   // persistent
   for (int heavy = 0; heavy < 2; ++heavy) {
     const int P = sms;
