@@ -200,6 +200,11 @@ struct KTimer {
 __device__ __forceinline__ void ktimer_begin(KTimer* kt) {
   if (kt && threadIdx.x == 0) atomicMin(&kt->start, globaltimer());
 }
+// kernels that load ahead of the state word take their entry time first, so
+// the hoisted work is inside the accounted interval
+__device__ __forceinline__ void ktimer_begin_at(KTimer* kt, unsigned long long t_entry) {
+  if (kt && threadIdx.x == 0) atomicMin(&kt->start, t_entry);
+}
 __device__ __forceinline__ void ktimer_end(KTimer* kt) {
   if (kt) {
     const unsigned long long now = globaltimer();

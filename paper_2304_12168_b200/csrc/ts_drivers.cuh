@@ -33,8 +33,10 @@ static int capture_switch(cudaStream_t cap, cudaGraphConditionalHandle h, int nc
 }
 
 static int capture_into(cudaStream_t cap, cudaGraph_t g, const std::function<int(cudaStream_t)>& f) {
-  TS_CUDA(cudaStreamBeginCaptureToGraph(cap, g, nullptr, nullptr, 0,
-                                        cudaStreamCaptureModeThreadLocal));
+  // relaxed: the capture holds kernel launches on a private stream only, and
+  // nothing another solver thread does (allocations, module loads, its own
+  // captures) may invalidate it
+  TS_CUDA(cudaStreamBeginCaptureToGraph(cap, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   const int rc = f(cap);
   cudaGraph_t out = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(cap, &out);
@@ -267,6 +269,9 @@ struct Instance {
   }
 
   int build(const GraphFn& gbody) {
+    // graphs are built once per instance: concurrent solver threads take turns
+    static std::mutex build_mu;
+    std::lock_guard<std::mutex> lk(build_mu);
     TS_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle h;
     TS_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));

@@ -143,7 +143,8 @@ static void free_plan(RowPlan& p) {
       if (q) cudaFree(q);
   p.sell_borrowed = 0;
   p.slab_borrowed = 0;
-  p.slab_cb = p.slab_sp = p.slab_wr = p.slab_pos = nullptr;
+  p.slab_cb = p.slab_sp = p.slab_pos = nullptr;
+  p.slab_wr = nullptr;
   p.slab_col = nullptr;
   p.slab_val = nullptr;
   p.wrow = nullptr;
@@ -195,7 +196,7 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
       const size_t nsp = (size_t)nw.P * nw.slab_nsl + 1, npos = (size_t)nw.P * nw.slab_rows;
       cudaMemcpyAsync(old.slab_cb, nw.slab_cb, (nw.P + 1) * sizeof(int), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_sp, nw.slab_sp, nsp * sizeof(int), cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(old.slab_wr, nw.slab_wr, (size_t)nw.P * 33 * sizeof(int), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(old.slab_wr, nw.slab_wr, (size_t)nw.P * 33 * sizeof(int2), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_pos, nw.slab_pos, npos * sizeof(int), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_col, nw.slab_col, nw.slab_slots * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(old.slab_val, nw.slab_val, nw.slab_slots * sizeof(double), cudaMemcpyDeviceToDevice, st);
@@ -210,7 +211,8 @@ static bool adopt_plan(RowPlan& old, RowPlan& nw, int64_t rows, cudaStream_t st)
       nw.sell_borrowed = 0;
     }
     if (nw.slab_borrowed) {
-      old.slab_cb = old.slab_sp = old.slab_wr = old.slab_pos = nullptr;
+      old.slab_cb = old.slab_sp = old.slab_pos = nullptr;
+      old.slab_wr = nullptr;
       old.slab_col = nullptr;
       old.slab_val = nullptr;
       nw.slab_borrowed = 0;
@@ -700,6 +702,13 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
   }
   if (tot >= (int64_t)INT32_MAX) return 0;
   sp[(size_t)P * nsl] = (int)tot;
+  // every warp run with its slot offset: one load instead of the wr -> sp chain
+  std::vector<int2> wre((size_t)P * 33);
+  for (int s = 0; s < P; ++s)
+    for (int ww = 0; ww <= 32; ++ww) {
+      const int q = wr[(size_t)s * 33 + ww];
+      wre[(size_t)s * 33 + ww] = make_int2(q, sp[(size_t)s * nsl + q]);
+    }
   const size_t slots = (size_t)std::max<int64_t>(tot, 1);
   if (reuse && reuse->kind == PLAN_SLAB && reuse->slab_slots == tot && reuse->P == P && reuse->slab_nsl == nsl &&
       reuse->slab_rows == m) {
@@ -713,7 +722,7 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
     p.slab_borrowed = 1;
   } else if (dev_malloc(&p.slab_cb, (P + 1) * sizeof(int), dev) != cudaSuccess ||
              dev_malloc(&p.slab_sp, sp.size() * sizeof(int), dev) != cudaSuccess ||
-             dev_malloc(&p.slab_wr, wr.size() * sizeof(int), dev) != cudaSuccess ||
+             dev_malloc(&p.slab_wr, wre.size() * sizeof(int2), dev) != cudaSuccess ||
              dev_malloc(&p.slab_pos, Pm * sizeof(int), dev) != cudaSuccess ||
              dev_malloc(&p.slab_col, slots * sizeof(uint16_t), dev) != cudaSuccess ||
              dev_malloc(&p.slab_val, slots * sizeof(double), dev) != cudaSuccess) {
@@ -722,7 +731,7 @@ static int build_slab(RowPlan& p, const int* rp, const int* ci, const double* va
   }
   TS_CUDA(cudaMemcpyAsync(p.slab_cb, cb.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
   TS_CUDA(cudaMemcpyAsync(p.slab_sp, sp.data(), sp.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  TS_CUDA(cudaMemcpyAsync(p.slab_wr, wr.data(), wr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  TS_CUDA(cudaMemcpyAsync(p.slab_wr, wre.data(), wre.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
   TS_CUDA(cudaMemcpyAsync(p.slab_pos, pos, Pm * sizeof(int), cudaMemcpyDeviceToDevice, st));
   TS_CUDA(cudaMemsetAsync(p.slab_col, 0xFF, slots * sizeof(uint16_t), st));  // padding: kSlabPad
   TS_CUDA(cudaMemsetAsync(p.slab_val, 0, slots * sizeof(double), st));

@@ -54,7 +54,8 @@ struct RowPlan {
   // PLAN_SLAB: the column-slab copy (see k_slab_av); P = slabs
   int slab_nsl = 0, slab_maxw = 0;
   int64_t slab_slots = 0, slab_rows = 0;
-  int *slab_cb = nullptr, *slab_sp = nullptr, *slab_wr = nullptr, *slab_pos = nullptr;
+  int *slab_cb = nullptr, *slab_sp = nullptr, *slab_pos = nullptr;
+  int2* slab_wr = nullptr;  // [P * 33] (first slice, slot offset) of every warp run
   uint16_t* slab_col = nullptr;
   double* slab_val = nullptr;
   int slab_borrowed = 0;

@@ -717,7 +717,7 @@ struct SlabRows {
   int xcap;               // doubles reserved for the x slab
   const int* cb;          // [P + 1] slab column boundaries
   const int* sp;          // [P * nsl + 1] slot offset of every slice
-  const int* wr;          // [P * 33] first in-slab slice of each warp's run
+  const int2* wr;         // [P * 33] each warp's run: (first in-slab slice, its slot offset)
   const int* pos;         // [P * m] position (slice * 32 + lane) of every row in its slab's order
   const uint16_t* col;    // in-slab column, kSlabPad on padding
   const double* val;
@@ -737,15 +737,18 @@ __global__ void __launch_bounds__(kSlabT, 1) k_slab_av(SlabRows S, const double*
   double* accs = xsl + S.xcap;                                    // [slab_accn(nsl)]
   int* sps = reinterpret_cast<int*>(accs + slab_accn(S.nsl));     // [nsl + 1]
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) return;  // k_slab_combine owns idle()
-  xs.load();
-  ktimer_begin(epi.timer());
+  unsigned long long t_in = 0;  // entry time (thread 0): hoisted work stays inside the accounted interval
+  if (threadIdx.x == 0) t_in = globaltimer();
+  // The tables are immutable and x is complete: the table chain (slab bounds ->
+  // run bounds -> first k-steps) and the thread's part of the x slab are in
+  // flight before the state word decides whether the pass runs at all.
   constexpr int U = kSlabU;
+  constexpr int XR = 8;  // x entries per thread staged through registers (slabs of <= 8192 columns)
   const int s = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int cb0 = __ldg(S.cb + s), cw = __ldg(S.cb + s + 1) - cb0;
-  const int q0 = __ldg(S.wr + s * 33 + w), q1 = __ldg(S.wr + s * 33 + w + 1);
+  const int2 w0 = __ldg(S.wr + s * 33 + w), w1 = __ldg(S.wr + s * 33 + w + 1);
+  const int q0 = w0.x, q1 = w1.x, E0 = w0.y, E1 = w1.y;
   const int g0 = s * S.nsl;
-  const int E0 = __ldg(S.sp + g0 + q0), E1 = __ldg(S.sp + g0 + q1);
   const int KT = (E1 - E0) >> 5;  // k-steps (32 slots each) of this warp's run
   const double* vp = S.val + E0 + lane;
   const uint16_t* cp = S.col + E0 + lane;
@@ -760,8 +763,22 @@ __global__ void __launch_bounds__(kSlabT, 1) k_slab_av(SlabRows S, const double*
     }
   };
   load(va, ca, 0);  // in flight with the staging below
+  double xr[XR];
+#pragma unroll
+  for (int u = 0; u < XR; ++u) {
+    const int i = threadIdx.x + u * kSlabT;
+    xr[u] = i < cw ? __ldg(x + cb0 + i) : 0.0;
+  }
+  if (!epi.active()) return;  // k_slab_combine owns idle()
+  xs.load();
+  ktimer_begin_at(epi.timer(), t_in);
   for (int i = threadIdx.x; i <= S.nsl; i += kSlabT) sps[i] = __ldg(S.sp + g0 + i);
-  for (int i = threadIdx.x; i < cw; i += kSlabT) xsl[i] = xs(__ldg(x + cb0 + i));
+#pragma unroll
+  for (int u = 0; u < XR; ++u) {
+    const int i = threadIdx.x + u * kSlabT;
+    if (i < cw) xsl[i] = xs(xr[u]);
+  }
+  for (int i = threadIdx.x + XR * kSlabT; i < cw; i += kSlabT) xsl[i] = xs(__ldg(x + cb0 + i));
   __syncthreads();
   int q = q0;
   int kend = q0 < q1 ? (sps[q0 + 1] - E0) >> 5 : INT32_MAX;
@@ -806,22 +823,14 @@ __global__ void __launch_bounds__(kNT) k_slab_combine(int m, int P, const double
   __shared__ int sflag;
   __shared__ double epi_smem[kEpiSmem];
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
-  if (!epi.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
-    return;
-  }
-  epi.prepare(epi_smem);
-  __syncthreads();
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int qa = P * g / kWarps, qb = P * (g + 1) / kWarps;
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
   const int ngroups = (m + 31) >> 5;
-  for (int rg = blockIdx.x; rg < ngroups; rg += gridDim.x) {
-    const int r = rg * 32 + lane;
+  // slab sums of one row over this warp's slab range, every load of a batch in
+  // flight (a serial tail costs a round trip per slab)
+  auto range_sum = [&](int r) -> double {
     double sum = 0.0;
-    if (r < m) {  // every load of a batch in flight (a serial tail costs a round trip per slab)
+    if (r < m) {
       for (int q = qa; q < qb; q += 10) {
         double t[10];
 #pragma unroll
@@ -830,6 +839,24 @@ __global__ void __launch_bounds__(kNT) k_slab_combine(int m, int P, const double
         for (int u = 0; u < 10; ++u) sum += t[u];
       }
     }
+    return sum;
+  };
+  // the partials are complete (the slab kernel wrote them): the block's first
+  // row group is summed while the state word is in flight
+  double sum0 = 0.0;
+  if ((int)blockIdx.x < ngroups) sum0 = range_sum((int)blockIdx.x * 32 + lane);
+  if (!epi.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
+    return;
+  }
+  epi.prepare(epi_smem);
+  __syncthreads();
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
+  for (int rg = blockIdx.x; rg < ngroups; rg += gridDim.x) {
+    const int r = rg * 32 + lane;
+    const double sum = rg == (int)blockIdx.x ? sum0 : range_sum(r);
     red[g][lane] = sum;
     __syncthreads();
     if (g == 0 && r < m) {
@@ -1028,6 +1055,8 @@ __global__ void __launch_bounds__(kNT, 2) k_rows_wdense(DenseRows A, const doubl
   __shared__ __align__(16) double xsl[kWdMaxN + 64];
   __shared__ int sflag;
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  unsigned long long t_in = 0;  // entry time (thread 0): hoisted work stays inside the accounted interval
+  if (threadIdx.x == 0) t_in = globaltimer();
   const int64_t m = A.m, n = A.n, lda = A.lda, P = gridDim.x, b = blockIdx.x;
   const int64_t r0 = m * b / P, r1 = m * (b + 1) / P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1057,7 +1086,7 @@ __global__ void __launch_bounds__(kNT, 2) k_rows_wdense(DenseRows A, const doubl
     return;
   }
   xs.load();
-  ktimer_begin(epi.timer());
+  ktimer_begin_at(epi.timer(), t_in);
   __shared__ double epi_smem[kEpiSmem];
   epi.prepare(epi_smem);
 #pragma unroll
