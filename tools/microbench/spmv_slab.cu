@@ -50,6 +50,42 @@ __device__ __forceinline__ int ld_stream_i(const int* p) {
   return v;
 }
 
+// L2 eviction-priority hints (createpolicy): the matrix stream is evict_first,
+// so it does not push x, the position table and the partials out of L2
+__device__ __forceinline__ unsigned long long pol_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_stream_h(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_stream_u16_h(const unsigned short* p, unsigned long long pol) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_keep_i(const int* p, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 struct SlabStream {
   int m, n, P, nsl;      // rows, columns, slabs, slices per slab
   const int* cb;         // [P + 1] slab column boundaries
@@ -279,7 +315,7 @@ __device__ __forceinline__ double ld_dsmem(unsigned addr) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-template <int NW, int U, int PIPE, int CL = 1>
+template <int NW, int U, int PIPE, int CL = 1, int HINT = 0>
 __global__ void __launch_bounds__(NW * 32, 1) k_slab2(SlabStream S, const int* __restrict__ inv,
                                                       const double* __restrict__ x, double* __restrict__ part,
                                                       int xcap, unsigned long long* ts) {
@@ -301,17 +337,23 @@ __global__ void __launch_bounds__(NW * 32, 1) k_slab2(SlabStream S, const int* _
   const unsigned short* cp = S.col + E0 + lane;
   double va[U], vb[U];
   unsigned ca[U], cbf[U];
+  const unsigned long long pf = HINT ? pol_first() : 0ull, pl = HINT ? pol_last() : 0ull;
   auto load = [&](double (&v)[U], unsigned (&c)[U], int k0) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool ok = k0 + u < KT;
-      v[u] = ok ? ld_stream(vp + 32 * (k0 + u)) : 0.0;
-      c[u] = ok ? ld_stream_u16(cp + 32 * (k0 + u)) : 0xFFFFu;
+      if (HINT) {
+        v[u] = ok ? ld_stream_h(vp + 32 * (k0 + u), pf) : 0.0;
+        c[u] = ok ? ld_stream_u16_h(cp + 32 * (k0 + u), pf) : 0xFFFFu;
+      } else {
+        v[u] = ok ? ld_stream(vp + 32 * (k0 + u)) : 0.0;
+        c[u] = ok ? ld_stream_u16(cp + 32 * (k0 + u)) : 0xFFFFu;
+      }
     }
   };
   load(va, ca, 0);  // in flight with the staging below
-  for (int i = threadIdx.x; i <= S.nsl; i += NT_) sps[i] = __ldg(S.sp + g0 + i);
-  for (int i = threadIdx.x; i < cw; i += NT_) xs[i] = __ldg(x + cb0 + i);
+  for (int i = threadIdx.x; i <= S.nsl; i += NT_) sps[i] = HINT ? ld_keep_i(S.sp + g0 + i, pl) : __ldg(S.sp + g0 + i);
+  for (int i = threadIdx.x; i < cw; i += NT_) xs[i] = HINT ? ld_keep(x + cb0 + i, pl) : __ldg(x + cb0 + i);
   __syncthreads();
   if (ts && threadIdx.x == 0) ts[s * 4 + 1] = gtimer();
   int q = q0;
@@ -352,7 +394,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_slab2(SlabStream S, const int* _
   if (CL == 1) {
     double* out = part + (size_t)s * S.m;
     const int* iv = inv + (size_t)s * S.m;
-    for (int r = threadIdx.x; r < S.m; r += NT_) out[r] = accs[__ldg(iv + r)];
+    if (HINT) {
+      for (int r = threadIdx.x; r < S.m; r += NT_) st_keep(out + r, accs[ld_keep_i(iv + r, pl)], pl);
+    } else {
+      for (int r = threadIdx.x; r < S.m; r += NT_) out[r] = accs[__ldg(iv + r)];
+    }
   } else {
     // pair reduce over distributed shared memory: block `rank` of the pair owns
     // rows [rank m/2, (rank+1) m/2): slab 2c's sum + slab 2c+1's sum, in that order
@@ -775,10 +821,32 @@ int main() {
       printf("      slab kernel %.2f us, sum %.2f us; phases: start %.2f staged %.2f streamed %.2f flushed %.2f (max %.2f)\n", \
              t1 * 1e3, t2 * 1e3, a0 / P * 1e-3, a1 / P * 1e-3, a2 / P * 1e-3, a3 / P * 1e-3, mx * 1e-3); \
     }
-    SLAB2C(32, 4, 1, 8, 10)
-    SLAB2C(32, 4, 1, 16, 5)
-    SLAB2C(32, 4, 1, 4, 10)
-    SLAB2C(32, 8, 0, 8, 10)
+
+#define SLAB2H(NW, U, PIPE, HINT)                                                                        \
+    {                                                                                                    \
+      const int xcap = (maxw + 15) & ~15;                                                                \
+      const int sm_ = xcap * 8 + nsl * 32 * 8 + (nsl + 1) * 4 + 16;                                      \
+      CK(cudaFuncSetAttribute(k_slab2<NW, U, PIPE, 1, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_)); \
+      float t = timeit([&] {                                                                             \
+        k_slab2<NW, U, PIPE, 1, HINT><<<P, NW * 32, sm_>>>(S, dinv, x, part, xcap, nullptr);              \
+        k_sumA<8, 10><<<(m + 31) / 32, 256>>>(part, m, P, y);                                            \
+      }, 40, fl);                                                                                        \
+      report("slab2 NW" #NW " U" #U " PIPE" #PIPE " HINT" #HINT " + sumA8x10", t);                       \
+      if (fl) flush_l2();                                                                                \
+      k_slab2<NW, U, PIPE, 1, HINT><<<P, NW * 32, sm_>>>(S, dinv, x, part, xcap, nullptr);                \
+      k_slab2<NW, U, PIPE, 1, HINT><<<P, NW * 32, sm_>>>(S, dinv, x, part, xcap, dts);                    \
+      CK(cudaDeviceSynchronize());                                                                       \
+      std::vector<unsigned long long> hts(P * 4);                                                        \
+      CK(cudaMemcpy(hts.data(), dts, P * 32, cudaMemcpyDeviceToHost));                                   \
+      unsigned long long T0 = ~0ull; double a1 = 0, a2 = 0, a3 = 0, mx = 0;                               \
+      for (int b = 0; b < P; ++b) T0 = std::min(T0, hts[b * 4]);                                         \
+      for (int b = 0; b < P; ++b) { a1 += hts[b*4+1]-T0; a2 += hts[b*4+2]-T0; a3 += hts[b*4+3]-T0; mx = std::max(mx, (double)(hts[b*4+3]-T0)); } \
+      printf("      phases: staged %.2f streamed %.2f flushed %.2f (max %.2f)\n", a1 / P * 1e-3, a2 / P * 1e-3, a3 / P * 1e-3, mx * 1e-3); \
+    }
+    SLAB2H(32, 4, 1, 0)
+    SLAB2H(32, 4, 1, 1)
+    SLAB2H(32, 4, 1, 0)
+    SLAB2H(32, 4, 1, 1)
     {
       float a = timeit([&] { k_sumA<8, 10><<<(m + 31) / 32, 256>>>(part, m, P, y); }, 20, fl);
       float b = timeit([&] { k_sumA<16, 10><<<(m + 31) / 32, 512>>>(part, m, P, y); }, 20, fl);
@@ -787,7 +855,6 @@ int main() {
       float e = timeit([&] { k_sum32<32><<<1, 32>>>(part, 1, 1, y); }, 20, fl);
       printf("      full-P sums: sumA8x10 %.2f sumA16x10 %.2f sumA32x5 %.2f sumA8x19 %.2f; empty kernel %.2f us\n", a * 1e3, b * 1e3, c * 1e3, d * 1e3, e * 1e3);
     }
-    SLABT(32, 4, 128, 0)
   }
   return 0;
 }
