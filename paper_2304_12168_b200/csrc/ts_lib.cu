@@ -985,6 +985,21 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
           A->npart = npart_elems(m, n) + npart_elems(n, m);  // disjoint A v / A^T v layouts
         }
       }
+      // HBM-sized dense A: a transposed copy for A v on the column-tile kernel
+      // (TS_DENSE_AV=rows keeps the row-tile kernel and saves the copy)
+      const char* ae = getenv("TS_DENSE_AV");
+      if (!rc && !A->aT && m >= 1024 && n >= 1024 && 8 * m * n >= kNcolsBytes && A->planN.kind == PLAN_TILE &&
+          !A->planN.wdense && !(ae && !strcmp(ae, "rows"))) {
+        A->ldaT = (m + 15) / 16 * 16;
+        if (dev_malloc(&A->aT, (size_t)A->ldaT * n * sizeof(double), device) == cudaSuccess) {
+          if (A->ldaT != m) cudaMemsetAsync(A->aT, 0, (size_t)A->ldaT * n * sizeof(double), st);
+          A->planN.kind = PLAN_NCOLS;
+          A->planN.P = tile_grid(n, m, A->sms, kTileTBlocks, kTileMinRowsT);
+        } else {
+          cudaGetLastError();  // no room for the copy: the row-tile kernel stays
+          A->aT = nullptr;
+        }
+      }
     }
     if (!rc) rc = finish_create(A, st, ar);
   }

@@ -29,8 +29,9 @@ namespace ts {
 // PLAN_TRANS  small dense A^T v over a transposed copy (k_rows_tile_fused)
 // PLAN_SELL   short CSR rows, HBM-sized: sliced-ELL copy (k_rows_sell)
 // PLAN_SLAB   long CSR rows of a wide matrix: column slabs (k_slab_av + k_slab_combine)
+// PLAN_NCOLS  large dense A v as column tiles over a transposed copy (k_cols_tile)
 enum PlanKind : int { PLAN_FLAT = 0, PLAN_SHORT = 1, PLAN_TILE = 2, PLAN_WROW = 7, PLAN_TRANS = 9,
-                      PLAN_SELL = 10, PLAN_SLAB = 11 };
+                      PLAN_SELL = 10, PLAN_SLAB = 11, PLAN_NCOLS = 12 };
 
 
 // elements of Work::npart a dense matrix needs (0 for CSR / non-tiled plans):
@@ -157,6 +158,11 @@ inline int vec_grid(int64_t len, int sms, int per_sm = 0) {
 // 15.7 us with 8 (16 and 64 were worse); A v is best at 8 (7.2 vs 9.1 us).
 // dense matrices up to this size keep a transposed copy for A^T v (PLAN_TRANS)
 constexpr int64_t kTransBytes = 32ll << 20;
+// HBM-sized dense matrices keep a transposed copy too, for A v: the column-tile
+// kernel (each thread owns two columns, 12 rows in flight, no warp reductions,
+// no per-(tile, row) partials) streams at 0.96 of the copy peak, the row-tile
+// kernel at 0.86-0.90 (C2: 126 vs 135-142 us); 180 GB of HBM pay for the copy
+constexpr int64_t kNcolsBytes = 256ll << 20;
 constexpr int kTileMinRowsN = 8;
 constexpr int kTileMinRowsT = 32;
 inline int tile_grid(int64_t m, int64_t n, int sms, int per_sm = kMinBlocks, int min_rows = kTileMinRowsN) {
@@ -202,6 +208,8 @@ int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi,
     if (!trans) {
       if (M.planN.wdense)
         k_rows_wdense<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
+      else if (M.planN.kind == PLAN_NCOLS)
+        k_cols_tile<Epi, 2><<<M.planN.P, kNT, 0, st>>>(DenseRows{M.aT, M.ldaT, M.n, M.m}, x, xs, epi, wk);
       else if (M.planN.kind == PLAN_TILE)
         k_rows_tile_fused<Epi><<<M.planN.P, kNT, 0, st>>>(M.dense(), x, xs, epi, wk);
       else

@@ -144,7 +144,8 @@ class DeviceMatrix:
         return out
 
     PLAN_NAMES = {0: "flat", 1: "thread_rows", 2: "dense_tiles", 7: "warp_rows", 9: "dense_transposed",
-                  10: "sliced_ell", 11: "column_slabs"}
+                  10: "sliced_ell", 11: "column_slabs",
+                  12: "column_tiles_transposed_copy"}
 
     def plans(self) -> tuple[str, str]:
         """The kernels chosen for A v and A^T v."""
