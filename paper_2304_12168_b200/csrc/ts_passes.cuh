@@ -567,9 +567,21 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_rows_sell(SellRows A, const
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = red_identity(epi.op(k));
-  for (int64_t s = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); s < nsl; s += W) {
-    const int b0 = __ldg(A.sp + s);
-    const int wd = (__ldg(A.sp + s + 1) - b0) >> 5;
+  // the next slice's offsets are loaded a slice ahead: one dependent round trip
+  // (offsets -> entries -> gathers) less per slice
+  int64_t s = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  int nb0 = 0, nb1 = 0;
+  if (s < nsl) {
+    nb0 = __ldg(A.sp + s);
+    nb1 = __ldg(A.sp + s + 1);
+  }
+  for (; s < nsl; s += W) {
+    const int b0 = nb0;
+    const int wd = (nb1 - b0) >> 5;
+    if (s + W < nsl) {
+      nb0 = __ldg(A.sp + s + W);
+      nb1 = __ldg(A.sp + s + W + 1);
+    }
     const int* cp = A.ci + b0 + lane;
     const double* vp = A.val + b0 + lane;
     double sum = 0.0;
