@@ -190,6 +190,7 @@ struct Instance {
   cudaGraphNode_t wnode = nullptr;  // the WHILE node of `graph`
   cudaGraphExec_t exec = nullptr;
   cudaStream_t cap = nullptr;
+  cudaStream_t out = nullptr;  // result read-back, concurrent with the final residual passes
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   int64_t pad = 0;  // row-block shards: halo entries before and after every vector
@@ -263,9 +264,23 @@ struct Instance {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (cap) cudaStreamDestroy(cap);
+    if (out) cudaStreamDestroy(out);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (void* p : allocs) cudaFree(p);
+  }
+
+  // The loop has stopped and the host has read the state (a synchronisation
+  // point), so x is final: its device->host copy runs on a second stream while
+  // the final residual passes (which only read x) run on the solve's stream.
+  int read_back(void* dst, const void* src, size_t bytes) {
+    if (!out) TS_CUDA(cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking));
+    TS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, out));
+    return 0;
+  }
+  int read_back_done() {
+    if (out) TS_CUDA(cudaStreamSynchronize(out));
+    return 0;
   }
 
   int build(const GraphFn& gbody) {
@@ -615,9 +630,13 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
     set_error("degenerate pivot: v coincides with the iterate");
     return TS_EDEGENERATE;
   }
+  bool early = false;  // x (and b') on their way to the host during the final passes
   if (c.hs->trivial) {
     TS_CUDA(cudaMemsetAsync(I->x, 0, no * sizeof(double), st));
   } else {
+    early = true;
+    if (x_out) TS_CHECK(I->read_back(x_out, I->x, no * sizeof(double)));
+    if (bp_out) TS_CHECK(I->read_back(bp_out, I->bp, mo * sizeof(double)));
     EpiFinalR efr;
     efr.st = ds; efr.b = I->b; efr.fr = I->fr;
     TS_CHECK(K.op_apply(st, I->x, XS{}, efr, 0));
@@ -629,8 +648,12 @@ static int ta_solve(const Mat& M, const double* b_in, const TaArgs& a, double* x
     TS_CHECK(vecpass(M, no, en, wk, st));
   }
   TS_CHECK(c.read_state());
-  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, no * sizeof(double), cudaMemcpyDefault, st));
-  if (bp_out) TS_CUDA(cudaMemcpyAsync(bp_out, I->bp, mo * sizeof(double), cudaMemcpyDefault, st));
+  if (!early) {
+    if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, no * sizeof(double), cudaMemcpyDefault, st));
+    if (bp_out) TS_CUDA(cudaMemcpyAsync(bp_out, I->bp, mo * sizeof(double), cudaMemcpyDefault, st));
+  } else {
+    TS_CHECK(I->read_back_done());
+  }
   fill_result(*c.hs, res);
   TS_CHECK(c.finish_timing(res));
   TS_CUDA(cudaStreamSynchronize(st));
@@ -929,6 +952,8 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     return recheck(s, 0, 0, 0, 0);
   };
   TS_CHECK(c.run(body, gbody, maint));
+  const bool early = !c.hs->trivial;  // x on its way to the host during the final passes
+  if (early && x_out) TS_CHECK(I->read_back(x_out, I->x, no * sizeof(double)));
   if (!c.hs->trivial) {
     EpiFinalR efr;
     efr.st = ds; efr.b = I->b; efr.fr = I->fr;
@@ -938,7 +963,11 @@ static int cta_solve(const Mat& M, const double* b_in, const CtaArgs& a, double*
     TS_CHECK(op.T(I->fr, enr, st));
   }
   TS_CHECK(c.read_state());
-  if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, no * sizeof(double), cudaMemcpyDefault, st));
+  if (!early) {
+    if (x_out) TS_CUDA(cudaMemcpyAsync(x_out, I->x, no * sizeof(double), cudaMemcpyDefault, st));
+  } else {
+    TS_CHECK(I->read_back_done());
+  }
   fill_result(*c.hs, res);
   TS_CHECK(c.finish_timing(res));
   TS_CUDA(cudaStreamSynchronize(st));
