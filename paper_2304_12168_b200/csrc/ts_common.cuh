@@ -14,6 +14,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -21,6 +23,31 @@
 #include "../../include/trisolve_b200.h"
 
 namespace ts {
+
+// Allocation, freeing and device-wide synchronisation (matrix creation and
+// destruction, solver-instance setup) must not run while another thread captures a
+// graph: they are the "potentially unsafe" calls of stream capture, and with a pool
+// of solver threads an occasional capture lost a node to them (cudaGraphAddNode:
+// invalid argument).  Such code holds the structural lock SHARED (re-entrant per
+// thread); a graph build holds it EXCLUSIVE.  Lock order: structural, then graph.
+inline std::shared_mutex& struct_mu() {
+  static std::shared_mutex mu;
+  return mu;
+}
+struct StructShared {
+  static int& depth() {
+    static thread_local int d = 0;
+    return d;
+  }
+  StructShared() {
+    if (depth()++ == 0) struct_mu().lock_shared();
+  }
+  ~StructShared() {
+    if (--depth() == 0) struct_mu().unlock_shared();
+  }
+  StructShared(const StructShared&) = delete;
+  StructShared& operator=(const StructShared&) = delete;
+};
 
 // ---------------------------------------------------------------- errors ----
 void set_error(const char* fmt, ...);

@@ -68,6 +68,7 @@ __global__ void k_copy_in(double* __restrict__ dst, const double* __restrict__ s
 static SolveState* pinned_state() {
   static thread_local SolveState* hs = nullptr;
   if (!hs) {
+    StructShared structural;
     if (cudaHostAlloc(&hs, sizeof(SolveState) + 64, cudaHostAllocDefault) != cudaSuccess) {
       hs = nullptr;
     }
@@ -170,6 +171,19 @@ static int vecpass(const Mat& M, int64_t len, const Epi& e, const Work& w, cudaS
 // whose kernel nodes bake those addresses in.  Instances are cached on the
 // (immutable) matrix handle per solver shape, so a repeated solve is just
 // memcpy-in, init kernels, graph launches, final kernels, memcpy-out.
+// Conditional graphs are built, run and destroyed under one process-wide lock:
+// with a pool of solver threads (TRISOLVE_WORKERS), building or destroying one
+// thread's graph while another thread's WHILE graph was executing made
+// cudaGraphAddNode fail now and then, and once crashed inside the destroy (one
+// run in ~20-40 of tests/test_gpu_cli.py::test_bench_rows).  The lock is held
+// from the graph launch to the state read-back that follows it, so the solves
+// of one process take turns on the device they would share anyway; direct
+// launches (TS_NO_GRAPH, emulated worlds) are not affected.
+inline std::mutex& graph_mu() {
+  static std::mutex mu;
+  return mu;
+}
+
 struct Instance {
   int key[4] = {0, 0, 0, 0};
   bool in_use = false;
@@ -190,6 +204,7 @@ struct Instance {
   cudaGraphNode_t wnode = nullptr;  // the WHILE node of `graph`
   cudaGraphExec_t exec = nullptr;
   cudaStream_t cap = nullptr;
+  bool no_graph = false;  // the graph could not be built: iterations are launched directly
   cudaStream_t out = nullptr;  // result read-back, concurrent with the final residual passes
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
@@ -259,11 +274,29 @@ struct Instance {
     TS_CUDA(cudaEventCreate(&ev1));
     return 0;
   }
-  ~Instance() {
-    if (hstage) cudaFreeHost(hstage);
+  // drop a (partially) built graph: the next solve rebuilds it or runs without
+  void drop_graph() {
+    std::lock_guard<std::mutex> lk(graph_mu());
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (cap) cudaStreamDestroy(cap);
+    exec = nullptr;
+    graph = nullptr;
+    cap = nullptr;
+    wnode = nullptr;
+  }
+  // a build failed: the half-built graph is abandoned, not destroyed (the driver
+  // crashed in cuGraphDestroy on such a graph); happens, if ever, once per instance
+  void abandon_graph() {
+    cudaGetLastError();
+    exec = nullptr;
+    graph = nullptr;
+    cap = nullptr;
+    wnode = nullptr;
+  }
+  ~Instance() {
+    if (hstage) cudaFreeHost(hstage);
+    drop_graph();
     if (out) cudaStreamDestroy(out);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -284,9 +317,8 @@ struct Instance {
   }
 
   int build(const GraphFn& gbody) {
-    // graphs are built once per instance: concurrent solver threads take turns
-    static std::mutex build_mu;
-    std::lock_guard<std::mutex> lk(build_mu);
+    std::unique_lock<std::shared_mutex> sl(struct_mu());  // no allocation / free / device sync meanwhile
+    std::lock_guard<std::mutex> lk(graph_mu());
     TS_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle h;
     TS_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
@@ -324,6 +356,7 @@ static int acquire(const Mat& Mc, const int key[4], const std::function<int(Inst
       }
     }
   }
+  StructShared structural;  // the instance's allocations
   Instance* I = new Instance();
   memcpy(I->key, key, sizeof(I->key));
   I->pad = M.row_shard ? M.halo : 0;
@@ -436,9 +469,26 @@ struct SolveCtx {
         static const bool dbg = getenv("TS_DEBUG_MAINT") != nullptr;
         if (dbg) fprintf(stderr, "[trisolve] host maintenance %d at iteration %lld\n", hs->maint, hs->iterations);
         TS_CHECK(maint(st));
-      } else if (!direct) {
-        if (!I->exec) TS_CHECK(I->build(gbody));
+      } else if (!direct && !I->no_graph) {
+        if (!I->exec) {
+          // a failed build is retried once; after that this instance launches
+          // its iterations directly (same kernels, same results)
+          int brc = I->build(gbody);
+          if (brc) {
+            I->abandon_graph();
+            brc = I->build(gbody);
+          }
+          if (brc) {
+            I->abandon_graph();
+            I->no_graph = true;
+            continue;
+          }
+        }
+        std::lock_guard<std::mutex> lk(graph_mu());
         TS_CUDA(cudaGraphLaunch(I->exec, st));
+        TS_CHECK(read_state());  // the graph has left the device before the lock is released
+        TS_CHECK(flush());
+        continue;
       } else {
         TS_CHECK(body(st));
       }
@@ -1290,6 +1340,7 @@ int ts_cta_step(const ts_matrix* A, int32_t h_mode, const double* x, const doubl
 // ------------------------------------------------------- column sharding --
 int ts_comm_create(int device, int rank, int world, int64_t vec_capacity, ts_comm** out,
                    void* ipc_handles_out) {
+  StructShared structural;
   if (!out || !ipc_handles_out) TS_INVAL("null argument");
   *out = nullptr;
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
@@ -1333,6 +1384,7 @@ int ts_comm_create(int device, int rank, int world, int64_t vec_capacity, ts_com
 // Each rank's solves must run on their own host thread.
 int ts_comm_create_local(int device, int world, int64_t vec_capacity, const int32_t* devices,
                          ts_comm** out) {
+  StructShared structural;
   if (!out) TS_INVAL("null argument");
   if (world < 1 || world > kMaxRanks) TS_INVAL("world %d outside 1..%d", world, kMaxRanks);
   if (vec_capacity < 1) TS_INVAL("vector capacity must be positive");
@@ -1406,6 +1458,7 @@ int ts_comm_create_local(int device, int world, int64_t vec_capacity, const int3
 }
 
 int ts_comm_connect(ts_comm* h, const void* all_handles) {
+  StructShared structural;
   Comm* c = reinterpret_cast<Comm*>(h);
   if (!c || !all_handles) TS_INVAL("null argument");
   DeviceGuard g(c->dev);
@@ -1437,6 +1490,7 @@ int ts_comm_connect(ts_comm* h, const void* all_handles) {
 }
 
 int ts_comm_destroy(ts_comm* h) {
+  StructShared structural;
   Comm* c = reinterpret_cast<Comm*>(h);
   if (!c) return 0;
   DeviceGuard g(c->dev);

@@ -7,6 +7,10 @@
 // reference, centering.py:344-352 / triangle.py:239-242), or the device trace
 // ring (seg_cap rows) needs flushing.  The host synchronises only at those
 // points, never inside an iteration.
+#include <execinfo.h>
+#include <fcntl.h>
+#include <signal.h>
+#include <unistd.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
 
@@ -31,6 +35,33 @@ void set_error(const char* fmt, ...) {
 const char* last_error() { return g_err; }
 
 static thread_local long long g_launches = 0;  // kernels enqueued by this thread
+
+// TS_BACKTRACE=<file>: append the native stack to <file> on SIGSEGV / SIGABRT
+// (addresses resolve against this library with addr2line; built with -lineinfo)
+static char g_bt_path[512] = "";
+static void segv_backtrace(int sig) {
+  void* bt[64];
+  const int n = backtrace(bt, 64);
+  const int fd = open(g_bt_path, O_WRONLY | O_CREAT | O_APPEND, 0644);
+  if (fd >= 0) {
+    const char* hdr = sig == SIGSEGV ? "SIGSEGV\n" : "SIGABRT\n";
+    ssize_t w = write(fd, hdr, 8);
+    (void)w;
+    backtrace_symbols_fd(bt, n, fd);
+    close(fd);
+  }
+  _exit(128 + sig);
+}
+static struct SegvInit {
+  SegvInit() {
+    const char* e = getenv("TS_BACKTRACE");
+    if (e && *e) {
+      snprintf(g_bt_path, sizeof(g_bt_path), "%s", e);
+      signal(SIGSEGV, segv_backtrace);
+      signal(SIGABRT, segv_backtrace);
+    }
+  }
+} g_segv_init;
 
 // ------------------------------------------------------- device guards ----
 struct DeviceGuard {
@@ -782,6 +813,7 @@ int ts_device_count(int* count) {
 // A fully built, unsharded, non-column-tiled handle is retired into the
 // storage pool (see retire_take); everything else is freed.
 static int matrix_release(ts_matrix* A, bool complete) {
+  StructShared structural;
   if (!A) return 0;
   if (complete && matrix_pool_enabled() && !A->comm && A->halo == 0) {
     {
@@ -807,6 +839,7 @@ static int matrix_release(ts_matrix* A, bool complete) {
 int ts_matrix_destroy(ts_matrix* A) { return matrix_release(A, true); }
 
 int ts_pool_trim(int device) {
+  StructShared structural;
   pool_trim_device(device);
   std::vector<std::pair<size_t, void*>> drop;
   {
@@ -819,6 +852,7 @@ int ts_pool_trim(int device) {
 }
 
 int ts_host_alloc(size_t bytes, void** out) {
+  StructShared structural;
   if (!out) TS_INVAL("null output pointer");
   *out = nullptr;
   bytes = std::max<size_t>(bytes, 64);
@@ -845,6 +879,7 @@ int ts_host_alloc(size_t bytes, void** out) {
 }
 
 int ts_host_free(void* ptr) {
+  StructShared structural;
   if (!ptr) return 0;
   void* base = static_cast<char*>(ptr) - 64;
   const size_t bytes = *reinterpret_cast<size_t*>(base);
@@ -908,6 +943,7 @@ static int finish_create(ts_matrix* A, cudaStream_t st, Arena& ar) {
 
 int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, int device,
                            void* stream, ts_matrix** out) {
+  StructShared structural;
   if (!out) TS_INVAL("null output handle");
   *out = nullptr;
   if (m < 1 || n < 1) TS_INVAL("matrix must have at least one row and one column (got %lld x %lld)",
@@ -1014,6 +1050,7 @@ int ts_matrix_create_dense(const double* a, int64_t m, int64_t n, int64_t lda, i
 int ts_matrix_create_csr(const int32_t* indptr, const int32_t* indices, const double* data,
                          int64_t m, int64_t n, int64_t nnz, int device, void* stream,
                          ts_matrix** out) {
+  StructShared structural;
   if (!out) TS_INVAL("null output handle");
   *out = nullptr;
   if (m < 1 || n < 1) TS_INVAL("matrix must have at least one row and one column (got %lld x %lld)",
@@ -1162,6 +1199,7 @@ int ts_matrix_create_csr_pair(const int32_t* indptr, const int32_t* indices, con
                               int64_t nnz, const int32_t* indptr_t, const int32_t* indices_t,
                               const double* data_t, int64_t nnz_t, int64_t m, int64_t halo,
                               int device, void* stream, ts_matrix** out) {
+  StructShared structural;
   if (!out) TS_INVAL("null output handle");
   *out = nullptr;
   if (m < 1) TS_INVAL("row block must have at least one row");
@@ -1312,6 +1350,7 @@ __global__ void k_clement_fill(int64_t n, int* rp, int* ci, double* val) {
 
 int ts_matrix_gen_stencil5(int64_t grid, double center, double west, double east, double south,
                            double north, int32_t center_mode, int device, void* stream, ts_matrix** out) {
+  StructShared structural;
   if (!out) TS_INVAL("null output handle");
   *out = nullptr;
   if (grid < 2) TS_INVAL("grid must be at least 2");
@@ -1344,6 +1383,7 @@ int ts_matrix_gen_stencil5(int64_t grid, double center, double west, double east
 }
 
 int ts_matrix_gen_clement(int64_t n, int device, void* stream, ts_matrix** out) {
+  StructShared structural;
   if (!out) TS_INVAL("null output handle");
   *out = nullptr;
   if (n < 2) TS_INVAL("n must be at least 2");
@@ -1448,6 +1488,7 @@ int ts_mm_free(ts_mm* P) {
 // Coordinate file -> device CSR handle: triplets uploaded once, mirrored,
 // sorted, de-duplicated and compressed on the device.
 int ts_mm_to_device(const ts_mm* P, int device, void* stream, ts_matrix** out, int64_t* duplicates) {
+  StructShared structural;
   if (!P || !out) TS_INVAL("null argument");
   *out = nullptr;
   if (P->fmt != 0) TS_INVAL("array files are dense: build them with ts_matrix_create_dense");
