@@ -1,3 +1,8 @@
+"""Maintenance-step probe (not the bench contract): a C3 CTA solve of 1200
+iterations (4 residual rechecks) and a C1 TA solve of 1500 iterations (2
+revalidations).  With TS_DEBUG_MAINT=1 the library prints every HOST-driven
+maintenance step: none in graph mode, all of them with TS_NO_GRAPH=1; the
+printed results must be identical."""
 import sys; sys.path.insert(0, ".")
 import numpy as np
 import paper_2304_12168_b200 as ts
