@@ -833,8 +833,17 @@ static int cta_probe_finish(const CtaOp& op, const Instance* I, cudaStream_t s) 
 static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, int solve_last,
                      cudaStream_t s, int slot = -1) {
   const bool pair = gram && !op.normal && band_pair_ok(op.M);
+  const bool dpair = gram && !op.normal && dense_pair_ok(op.M);
   for (int i = 1; i <= npairs; ++i) {
-    if (pair) {  // q_i = A^T p_{i-1} and p_i = A q_i in one kernel (square banded, L2-resident)
+    if (dpair) {  // small dense: both passes in one cooperative kernel
+      EpiCtaQ eq;
+      eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i; eq.tclass = 1; eq.slot = slot;
+      EpiCtaP ep;
+      ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
+      ep.with_solve = solve_last; ep.tclass = 0; ep.slot = slot;
+      ++g_launches;
+      TS_CHECK(launch_pair_wdense(op.M, I->kp.p[i - 1], I->kp.q[i - 1], eq, ep, I->wk, s));
+    } else if (pair) {  // q_i = A^T p_{i-1} and p_i = A q_i in one kernel (square banded, L2-resident)
       EpiCtaQ eq;
       eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i; eq.tclass = 1; eq.slot = slot;
       EpiCtaP ep;

@@ -201,6 +201,43 @@ int launch_pair_band(const Mat& M, const double* pprev, const EpiQ& eq, const Ep
   return 0;
 }
 
+// A small L2-resident dense matrix (both orientations on the warp-per-row
+// kernel) runs a CTA moments pair as one cooperative kernel (k_pair_wdense);
+// TS_DENSE_PAIR=0 keeps the two passes
+inline bool dense_pair_ok(const Mat& M) {
+  static const bool off = [] {
+    const char* e = getenv("TS_DENSE_PAIR");
+    return e && e[0] == '0';
+  }();
+  return !off && M.kind == 0 && !M.comm && M.aT && M.planN.wdense && M.planT.wdense &&
+         M.planT.kind == PLAN_TRANS;
+}
+template <class EpiQ, class EpiP>
+int launch_pair_wdense(const Mat& M, const double* pprev, const double* q, const EpiQ& eq, const EpiP& ep,
+                       const Work& wk, cudaStream_t st) {
+  // one grid for both phases, co-resident (2 blocks/SM by the launch bounds)
+  const int PT = std::min(M.planT.P, 2 * M.sms), PN = std::min(M.planN.P, 2 * M.sms);
+  const int P = std::max(PT, PN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P);
+  cfg.blockDim = dim3(kNT);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const DenseRows dT{M.aT, M.ldaT, M.n, M.m};
+  const int64_t len = std::max(M.m, M.n);  // the longer of the two staged vectors
+  if (len <= 4 * kNT)
+    TS_CUDA(cudaLaunchKernelEx(&cfg, k_pair_wdense<EpiQ, EpiP, 4>, dT, M.dense(), pprev, q, eq, ep, wk, PT, PN));
+  else if (len <= 8 * kNT)
+    TS_CUDA(cudaLaunchKernelEx(&cfg, k_pair_wdense<EpiQ, EpiP, 8>, dT, M.dense(), pprev, q, eq, ep, wk, PT, PN));
+  else
+    TS_CUDA(cudaLaunchKernelEx(&cfg, k_pair_wdense<EpiQ, EpiP, 16>, dT, M.dense(), pprev, q, eq, ep, wk, PT, PN));
+  return 0;
+}
+
 template <class Epi>
 int launch_pass(const Mat& M, int trans, const double* x, XS xs, const Epi& epi, const Work& wk,
                 cudaStream_t st) {

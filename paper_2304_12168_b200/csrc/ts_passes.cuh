@@ -1142,6 +1142,162 @@ __global__ void __launch_bounds__(kNT, 2) k_rows_wdense(DenseRows A, const doubl
   finish_last(epi, wk, nullptr, (int)gridDim.x, sm, &sflag);
 }
 
+// ---------------------------------------------------------- k_pair_wdense ----
+// One CTA moments pair q = A^T p, p' = A q in ONE cooperative kernel for a small
+// L2-resident dense matrix (C1; both orientations on the warp-per-row scheme,
+// A^T from the transposed copy).  Phase 1 computes this block's rows of q and
+// runs the q epilogue on them; a grid barrier makes q complete; phase 2 stages
+// q in shared memory and computes the block's rows of p' with the p' epilogue.
+// Against two kernels this saves the first kernel's whole reduction chain
+// (block sums -> arrival -> last block -> finisher), a kernel boundary and the
+// second state read; A's first rows are in flight across the barrier.  One
+// reduction for both epilogues' sums, the last block finishes both.  Row
+// arithmetic and each phase's row -> (block, warp) mapping are k_rows_wdense's,
+// so q, p' and their block sums are the bits of the two passes.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g0;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *count = 0u;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g0 + 1u) : "memory");
+    } else {
+      unsigned g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+      } while (g == g0);
+    }
+  }
+  __syncthreads();
+}
+
+// XN: vector entries per thread staged through registers (vectors of <= XN * 256 entries)
+template <class EpiQ, class EpiP, int XN>
+__global__ void __launch_bounds__(kNT, 2) k_pair_wdense(const __grid_constant__ DenseRows AT,
+                                                       const __grid_constant__ DenseRows A, const double* pprev,
+                                                       const double* q, const __grid_constant__ EpiQ eq,
+                                                       const __grid_constant__ EpiP ep,
+                                                       const __grid_constant__ Work wk, int PT, int PN) {
+  constexpr int KQ = EpiQ::K, KP = EpiP::K, K = KQ + KP;
+  constexpr int C = kWdChunks;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ __align__(16) double xsl[kWdMaxN + 64];
+  __shared__ int sflag;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ep.count_launch();
+  unsigned long long t_in = 0;  // entry time (thread 0): hoisted work stays inside the accounted interval
+  if (threadIdx.x == 0) t_in = globaltimer();
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double2 v[C];
+  auto load = [&](const DenseRows& D, int64_t r, int64_t c0) {
+    const double* row = D.a + r * D.lda + 2 * lane;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int64_t c = c0 + 64 * k + 2 * lane;
+      v[k] = c < D.lda ? ld_stream2(row + c0 + 64 * k) : make_double2(0.0, 0.0);
+    }
+  };
+  // rows [r0, r1) of D times the vector staged in xsl; `first`: row r's leading chunks are loaded
+  auto rows = [&](const DenseRows& D, int64_t r, int64_t r1, auto&& sink) {
+    const int64_t n = D.n;
+    bool first = true;
+    for (; r < r1; r += kWarps) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int64_t c0 = 0; c0 < n; c0 += 64 * C) {
+        if (!(first && c0 == 0)) load(D, r, c0);
+#pragma unroll
+        for (int k = 0; k < C; k += 2) {
+          const int64_t ca = c0 + 64 * k + 2 * lane, cb = ca + 64;
+          if (ca < n) {
+            const double2 xa = *reinterpret_cast<const double2*>(xsl + ca);
+            a0 = fma(v[k].x, xa.x, a0);
+            if (ca + 1 < n) a0 = fma(v[k].y, xa.y, a0);
+          }
+          if (cb < n) {
+            const double2 xb = *reinterpret_cast<const double2*>(xsl + cb);
+            a1 = fma(v[k + 1].x, xb.x, a1);
+            if (cb + 1 < n) a1 = fma(v[k + 1].y, xb.y, a1);
+          }
+        }
+      }
+      first = false;
+      const double y = warp_reduce(a0 + a1, RED_SUM);
+      if (lane == 0) sink(r, y);
+    }
+  };
+  auto stage = [&](const double (&xr)[XN], int64_t n) {
+    const int npad = (int)((n + 63) & ~(int64_t)63);
+#pragma unroll
+    for (int u = 0; u < XN; ++u) {
+      const int k = threadIdx.x + u * kNT;
+      if (k < npad) xsl[k] = k < n ? xr[u] : 0.0;
+    }
+  };
+  // ---- phase 1: q = A^T p on rows [t0, t1) of the transposed copy
+  // (each phase keeps the row split of its stand-alone pass: blocks [0, PT) / [0, PN))
+  const int64_t t0 = b < PT ? AT.m * b / PT : 0, t1 = b < PT ? AT.m * (b + 1) / PT : 0;
+  int64_t r = t0 + wid;
+  if (r < t1) load(AT, r, 0);
+  double xr[XN];
+#pragma unroll
+  for (int u = 0; u < XN; ++u) {
+    const int k = threadIdx.x + u * kNT;
+    xr[u] = k < AT.n ? __ldg(pprev + k) : 0.0;  // p is complete: written by an earlier kernel
+  }
+  if (!ep.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ep.idle();
+    return;
+  }
+  ktimer_begin_at(ep.timer(), t_in);
+  stage(xr, AT.n);
+  __syncthreads();
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  double (&aq)[KQ] = *reinterpret_cast<double (*)[KQ]>(&acc[0]);
+  double (&ap)[KP] = *reinterpret_cast<double (*)[KP]>(&acc[KQ]);
+  rows(AT, r, t1, [&](int64_t row, double y) { eq.elem(row, y, aq); });
+  // ---- A's first rows in flight across the barrier (the matrix is immutable)
+  const int64_t r0 = b < PN ? A.m * b / PN : 0, r1 = b < PN ? A.m * (b + 1) / PN : 0;
+  r = r0 + wid;
+  if (r < r1) load(A, r, 0);
+  grid_barrier(wk.done + 2, wk.done + 3, (unsigned)P);
+  // ---- phase 2: p' = A q; q was written inside this kernel: L2-coherent loads
+#pragma unroll
+  for (int u = 0; u < XN; ++u) {
+    const int k = threadIdx.x + u * kNT;
+    xr[u] = k < A.n ? __ldcg(q + k) : 0.0;
+  }
+  stage(xr, A.n);
+  __syncthreads();
+  rows(A, r, r1, [&](int64_t row, double y) { ep.elem(row, y, ap); });
+  const OpsSum ops;
+  block_reduce<K>(acc, sm, ops);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    double red[K];
+    reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, ops);
+    if (threadIdx.x == 0) {
+      ktimer_end(ep.timer());
+      double rq[KQ], rp2[KP];
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) rq[k] = red[k];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) rp2[k] = red[KQ + k];
+      eq.finish(rq);
+      ep.finish(rp2);
+    }
+    __syncthreads();
+    ep.finish_block();
+  }
+}
+
 // ------------------------------------------------------ k_rows_tile_fused ----
 // Dense A v in ONE kernel.  The (tile, row) units are ordered group-major:
 // 256-row groups one after another, inside a group tile by tile, so a group's

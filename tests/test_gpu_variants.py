@@ -9,8 +9,9 @@ interpreter (``tests/_variant_probe.py`` prints digests of the iterates):
   that falls in mid-period (``recheck_every=3``) — the in-graph recheck against
   the host-driven one;
 * the in-graph 512-pivot revalidation of TA against the host-driven one;
-* one-kernel moment pairs on a square banded matrix (k_pair_band) against
-  the two passes (TS_BAND_PAIR=0);
+* one-kernel moment pairs on a square banded matrix (k_pair_band) and on a
+  small dense matrix (k_pair_wdense, cooperative, grid barrier between the two
+  products) against the two passes (TS_BAND_PAIR=0, TS_DENSE_PAIR=0);
 * the warp-per-row small dense kernel against the tile kernel
   (TS_DENSE_SMALL=tile): same statuses and iteration counts, iterates within
   north_star's 1e-9 (the dot products are summed in another order, and TA
@@ -36,7 +37,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _probe(**env):
     e = dict(os.environ)
-    for k in ("TS_CTA_SWITCH", "TS_NO_GRAPH", "TS_BAND_PAIR", "TS_DENSE_SMALL"):
+    for k in ("TS_CTA_SWITCH", "TS_NO_GRAPH", "TS_BAND_PAIR", "TS_DENSE_PAIR", "TS_DENSE_SMALL"):
         e.pop(k, None)
     e.update(env)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_variant_probe.py")], env=e, cwd=ROOT,
@@ -50,8 +51,9 @@ def default_run():
     return _probe()
 
 
-@pytest.mark.parametrize("env", [{"TS_CTA_SWITCH": "1"}, {"TS_NO_GRAPH": "1"}, {"TS_BAND_PAIR": "0"}],
-                         ids=["switch_graph", "direct_launches", "two_pass_pairs"])
+@pytest.mark.parametrize("env", [{"TS_CTA_SWITCH": "1"}, {"TS_NO_GRAPH": "1"}, {"TS_BAND_PAIR": "0"},
+                                 {"TS_DENSE_PAIR": "0"}],
+                         ids=["switch_graph", "direct_launches", "two_pass_band_pairs", "two_pass_dense_pairs"])
 def test_structure_variants_are_bitwise(default_run, env):
     got = _probe(**env)
     assert got.keys() == default_run.keys()
