@@ -771,4 +771,193 @@ struct EpiCtaRecheck : EpiBase {
   int nocase = 0;
 };
 
+// ---------------------------------------------------------- k_chain_wdense ----
+// ALL moment pairs of one CTA iteration in one cooperative kernel, for a small
+// L2-resident dense matrix (C1).  Between the pairs only vectors flow — the
+// sums phi_k and ||A^T r||^2 are first needed after the last pair (the Hankel
+// solve) — so the 2 t products run back to back with a grid barrier after
+// each, every pair's three block sums are parked per block as they complete,
+// and ONE arrival / last-block reduction at the end runs the t pairs' finishers
+// in order and then the Hankel solves.  Against t pair kernels this removes
+// t - 1 reduction chains, kernel boundaries and state reads.  Each product
+// keeps k_rows_wdense's row arithmetic and row -> (block, warp) split, every sum
+// its block / thread composition, the finishers are the epilogues' own: the
+// bits of the separate passes.  Up to 5 pairs (15 sums in the two partial rows).
+constexpr int kChainMaxT = 5;
+
+template <int XN>
+__global__ void __launch_bounds__(kNT, 2) k_chain_wdense(const __grid_constant__ DenseRows AT,
+                                                        const __grid_constant__ DenseRows A,
+                                                        const __grid_constant__ KrylovPtrs kp, SolveState* st,
+                                                        int npairs, int slot, const __grid_constant__ Work wk,
+                                                        int PT, int PN) {
+  constexpr int C = kWdChunks;
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ __align__(16) double xsl[kWdMaxN + 64];
+  __shared__ int sflag;
+  EpiCtaP ep0;  // activity, accounting and the launch counter are the first pair's
+  ep0.st = st; ep0.i = 1; ep0.slot = slot; ep0.tclass = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ep0.count_launch();
+  unsigned long long t_in = 0;  // entry time (thread 0): hoisted work stays inside the accounted interval
+  if (threadIdx.x == 0) t_in = globaltimer();
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double2 v[C];
+  auto load = [&](const DenseRows& D, int64_t r, int64_t c0) {
+    const double* row = D.a + r * D.lda + 2 * lane;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int64_t c = c0 + 64 * k + 2 * lane;
+      v[k] = c < D.lda ? ld_stream2(row + c0 + 64 * k) : make_double2(0.0, 0.0);
+    }
+  };
+  auto rows = [&](const DenseRows& D, int64_t r, int64_t r1, auto&& sink) {
+    const int64_t n = D.n;
+    bool first = true;
+    for (; r < r1; r += kWarps) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int64_t c0 = 0; c0 < n; c0 += 64 * C) {
+        if (!(first && c0 == 0)) load(D, r, c0);
+#pragma unroll
+        for (int k = 0; k < C; k += 2) {
+          const int64_t ca = c0 + 64 * k + 2 * lane, cb = ca + 64;
+          if (ca < n) {
+            const double2 xa = *reinterpret_cast<const double2*>(xsl + ca);
+            a0 = fma(v[k].x, xa.x, a0);
+            if (ca + 1 < n) a0 = fma(v[k].y, xa.y, a0);
+          }
+          if (cb < n) {
+            const double2 xb = *reinterpret_cast<const double2*>(xsl + cb);
+            a1 = fma(v[k + 1].x, xb.x, a1);
+            if (cb + 1 < n) a1 = fma(v[k + 1].y, xb.y, a1);
+          }
+        }
+      }
+      first = false;
+      const double y = warp_reduce(a0 + a1, RED_SUM);
+      if (lane == 0) sink(r, y);
+    }
+  };
+  // stage a vector of length n into xsl; kCoh: written inside this kernel (L2-coherent loads)
+  auto stage = [&](const double* x, int64_t n, bool coh) {
+    double xr[XN];
+#pragma unroll
+    for (int u = 0; u < XN; ++u) {
+      const int k = threadIdx.x + u * kNT;
+      xr[u] = k < n ? (coh ? __ldcg(x + k) : __ldg(x + k)) : 0.0;
+    }
+    const int npad = (int)((n + 63) & ~(int64_t)63);
+#pragma unroll
+    for (int u = 0; u < XN; ++u) {
+      const int k = threadIdx.x + u * kNT;
+      if (k < npad) xsl[k] = k < n ? xr[u] : 0.0;
+    }
+  };
+  const int64_t t0 = b < PT ? AT.m * b / PT : 0, t1 = b < PT ? AT.m * (b + 1) / PT : 0;
+  const int64_t r0 = b < PN ? A.m * b / PN : 0, r1 = b < PN ? A.m * (b + 1) / PN : 0;
+  int64_t r = t0 + wid;
+  if (r < t1) load(AT, r, 0);  // the matrix is immutable: in flight with the state word
+  if (!ep0.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ep0.idle();
+    return;
+  }
+  ktimer_begin_at(ep0.timer(), t_in);
+  const int t = st->t < npairs ? st->t : npairs;  // the state's order (the slot's, in graph mode)
+  const OpsSum ops;
+  unsigned nbar = 0;  // barriers passed so far
+  for (int i = 1; i <= t; ++i) {
+    EpiCtaQ eq;
+    eq.st = st; eq.q = kp.q[i - 1]; eq.i = i;
+    EpiCtaP ep;
+    ep.st = st; ep.pprev = kp.p[i - 1]; ep.p = kp.p[i]; ep.i = i;
+    double acc[3] = {0.0, 0.0, 0.0};
+    double (&aq)[1] = *reinterpret_cast<double (*)[1]>(&acc[0]);
+    double (&ap)[2] = *reinterpret_cast<double (*)[2]>(&acc[1]);
+    // q_i = A^T p_{i-1} (p_0 = r comes from an earlier kernel, later p's from this one)
+    stage(kp.p[i - 1], AT.n, i > 1);
+    __syncthreads();
+    rows(AT, r, t1, [&](int64_t row, double y) { eq.elem(row, y, aq); });
+    r = r0 + wid;
+    if (r < r1) load(A, r, 0);  // A's first rows in flight across the barrier
+    grid_barrier(wk.done + 2, ++nbar * (unsigned)P);
+    // p_i = A q_i
+    stage(kp.q[i - 1], A.n, true);
+    __syncthreads();
+    rows(A, r, r1, [&](int64_t row, double y) { ep.elem(row, y, ap); });
+    block_reduce<3>(acc, sm, ops);
+    if (threadIdx.x == 0) {  // pair i's block sums: slots 3 (i - 1) .. 3 (i - 1) + 2 of the two partial rows
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int sl = 3 * (i - 1) + k;
+        (sl < kKMax ? wk.bacc : wk.facc)[b * kKMax + (sl < kKMax ? sl : sl - kKMax)] = acc[k];
+      }
+    }
+    if (i < t) {
+      r = t0 + wid;
+      if (r < t1) load(AT, r, 0);
+      grid_barrier(wk.done + 2, ++nbar * (unsigned)P);
+    }
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    if (threadIdx.x == 0) wk.done[2] = 0u;  // the barrier counter, for the next launch
+    // the separate passes' reduction, slot by slot: 256 threads stride the blocks, then the block tree
+    for (int i = 1; i <= t; ++i) {
+      double red[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) red[k] = 0.0;
+      for (int bb = threadIdx.x; bb < (int)P; bb += kNT) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int sl = 3 * (i - 1) + k;
+          red[k] += __ldcg((sl < kKMax ? wk.bacc : wk.facc) + (size_t)bb * kKMax + (sl < kKMax ? sl : sl - kKMax));
+        }
+      }
+      block_reduce<3>(red, sm, ops);
+      if (threadIdx.x == 0) {
+        EpiCtaQ eq;
+        eq.st = st; eq.i = i;
+        double rq[1] = {red[0]};
+        eq.finish(rq);
+        EpiCtaP ep;
+        ep.st = st; ep.i = i; ep.with_solve = 1;
+        double rp[2] = {red[1], red[2]};
+        if (i == t) ktimer_end(ep0.timer());
+        ep.finish(rp);
+      }
+      __syncthreads();
+    }
+    EpiCtaP ep;
+    ep.st = st; ep.i = t; ep.with_solve = 1;
+    ep.finish_block();
+  }
+}
+
+inline bool dense_chain_ok(const Mat& M, int npairs) {
+  static const bool off = [] {
+    const char* e = getenv("TS_DENSE_CHAIN");
+    return e && e[0] == '0';
+  }();
+  return !off && npairs >= 1 && npairs <= kChainMaxT && dense_pair_ok(M);
+}
+inline int launch_chain_wdense(const Mat& M, const KrylovPtrs& kp, SolveState* st, int npairs, int slot,
+                               const Work& wk, cudaStream_t s) {
+  const int PT = std::min(M.planT.P, 2 * M.sms), PN = std::min(M.planN.P, 2 * M.sms);
+  const int P = std::max(PT, PN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P);
+  cfg.blockDim = dim3(kNT);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const DenseRows dT{M.aT, M.ldaT, M.n, M.m};
+  const int64_t len = std::max(M.m, M.n);
+  if (len <= 4 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<4>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
+  else if (len <= 8 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<8>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
+  else TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<16>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
+  return 0;
+}
+
 }  // namespace ts

@@ -834,6 +834,10 @@ static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, i
                      cudaStream_t s, int slot = -1) {
   const bool pair = gram && !op.normal && band_pair_ok(op.M);
   const bool dpair = gram && !op.normal && dense_pair_ok(op.M);
+  if (dpair && solve_last && dense_chain_ok(op.M, npairs)) {  // every pair of the iteration in one kernel
+    ++g_launches;
+    return launch_chain_wdense(op.M, I->kp, I->ds, npairs, slot, I->wk, s);
+  }
   for (int i = 1; i <= npairs; ++i) {
     if (dpair) {  // small dense: both passes in one cooperative kernel
       EpiCtaQ eq;

@@ -1154,22 +1154,19 @@ __global__ void __launch_bounds__(kNT, 2) k_rows_wdense(DenseRows A, const doubl
 // reduction for both epilogues' sums, the last block finishes both.  Row
 // arithmetic and each phase's row -> (block, warp) mapping are k_rows_wdense's,
 // so q, p' and their block sums are the bits of the two passes.
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+// Grid barrier of a cooperative launch (every block resident).  The counter only
+// grows inside a kernel: barrier number k waits for k * nblocks arrivals, one
+// atomic and one polled load per block; the kernel's last block (its final
+// arrival) puts the counter back to zero for the next launch.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned g0;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
     __threadfence();
-    if (atomicAdd(count, 1u) == nblocks - 1) {
-      *count = 0u;
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g0 + 1u) : "memory");
-    } else {
-      unsigned g;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
-      } while (g == g0);
-    }
+    atomicAdd(count, 1u);
+    unsigned c;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(count) : "memory");
+    } while (c < target);
   }
   __syncthreads();
 }
@@ -1264,7 +1261,7 @@ __global__ void __launch_bounds__(kNT, 2) k_pair_wdense(const __grid_constant__ 
   const int64_t r0 = b < PN ? A.m * b / PN : 0, r1 = b < PN ? A.m * (b + 1) / PN : 0;
   r = r0 + wid;
   if (r < r1) load(A, r, 0);
-  grid_barrier(wk.done + 2, wk.done + 3, (unsigned)P);
+  grid_barrier(wk.done + 2, (unsigned)P);
   // ---- phase 2: p' = A q; q was written inside this kernel: L2-coherent loads
 #pragma unroll
   for (int u = 0; u < XN; ++u) {
@@ -1281,6 +1278,7 @@ __global__ void __launch_bounds__(kNT, 2) k_pair_wdense(const __grid_constant__ 
     for (int k = 0; k < K; ++k) wk.bacc[b * kKMax + k] = acc[k];
   }
   if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    if (threadIdx.x == 0) wk.done[2] = 0u;  // the barrier counter, for the next launch
     double red[K];
     reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, ops);
     if (threadIdx.x == 0) {
