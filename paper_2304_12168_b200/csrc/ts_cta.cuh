@@ -960,4 +960,147 @@ inline int launch_chain_wdense(const Mat& M, const KrylovPtrs& kp, SolveState* s
   return 0;
 }
 
+// ------------------------------------------------------------ k_chain_csr ----
+// The same chain for an L2-resident short-row CSR matrix that is not banded: thread per row in
+// scipy's order (k_rows_short's arithmetic and row -> thread mapping), q and p'
+// exchanged through L2 between the phases, so no bandwidth condition and no
+// halo recomputation (k_pair_band needs a banded square matrix).
+__device__ __forceinline__ double row_serial_cg(const CsrRows& A, int k0, int k1, const double* xq) {
+  double s = 0.0;
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    double v[4], xv[4];
+    int j[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = ld_stream(A.val + k + u);
+      j[u] = ld_stream_i(A.ci + k + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = __ldcg(xq + j[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+  }
+  const int rem = k1 - k;
+  double v[3], xv[3];
+  int j[3];
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (u < rem) {
+      v[u] = ld_stream(A.val + k + u);
+      j[u] = ld_stream_i(A.ci + k + u);
+    }
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (u < rem) xv[u] = __ldcg(xq + j[u]);
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (u < rem) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+  return s;
+}
+
+__global__ void __launch_bounds__(kNT, kMinBlocks) k_chain_csr(const __grid_constant__ CsrRows AT,
+                                                             const __grid_constant__ CsrRows A,
+                                                             const __grid_constant__ KrylovPtrs kp, SolveState* st,
+                                                             int npairs, int slot, const __grid_constant__ Work wk,
+                                                             int PT, int PN) {
+  __shared__ double sm[kWarps * kKMax];
+  __shared__ int sflag;
+  EpiCtaP ep0;
+  ep0.st = st; ep0.i = 1; ep0.slot = slot; ep0.tclass = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ep0.count_launch();
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int64_t t0 = b < PT ? AT.m * b / PT : 0, t1 = b < PT ? AT.m * (b + 1) / PT : 0;
+  const int64_t r0 = b < PN ? A.m * b / PN : 0, r1 = b < PN ? A.m * (b + 1) / PN : 0;
+  if (!ep0.active()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ep0.idle();
+    return;
+  }
+  ktimer_begin(ep0.timer());
+  const int t = st->t < npairs ? st->t : npairs;
+  const OpsSum ops;
+  unsigned nbar = 0;
+  for (int i = 1; i <= t; ++i) {
+    EpiCtaQ eq;
+    eq.st = st; eq.q = kp.q[i - 1]; eq.i = i;
+    EpiCtaP ep;
+    ep.st = st; ep.pprev = kp.p[i - 1]; ep.p = kp.p[i]; ep.i = i;
+    double acc[3] = {0.0, 0.0, 0.0};
+    double (&aq)[1] = *reinterpret_cast<double (*)[1]>(&acc[0]);
+    double (&ap)[2] = *reinterpret_cast<double (*)[2]>(&acc[1]);
+    for (int64_t j = t0 + threadIdx.x; j < t1; j += kNT)
+      eq.elem(j, row_serial_cg(AT, __ldg(AT.rp + j), __ldg(AT.rp + j + 1), kp.p[i - 1]), aq);
+    grid_barrier(wk.done + 2, ++nbar * (unsigned)P);
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += kNT)
+      ep.elem(r, row_serial_cg(A, __ldg(A.rp + r), __ldg(A.rp + r + 1), kp.q[i - 1]), ap);
+    block_reduce<3>(acc, sm, ops);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int sl = 3 * (i - 1) + k;
+        (sl < kKMax ? wk.bacc : wk.facc)[b * kKMax + (sl < kKMax ? sl : sl - kKMax)] = acc[k];
+      }
+    }
+    if (i < t) grid_barrier(wk.done + 2, ++nbar * (unsigned)P);
+  }
+  if (arrive_last(wk.done, (unsigned)P, &sflag)) {
+    if (threadIdx.x == 0) wk.done[2] = 0u;  // the barrier counter, for the next launch
+    for (int i = 1; i <= t; ++i) {
+      double red[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) red[k] = 0.0;
+      for (int bb = threadIdx.x; bb < (int)P; bb += kNT) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int sl = 3 * (i - 1) + k;
+          red[k] += __ldcg((sl < kKMax ? wk.bacc : wk.facc) + (size_t)bb * kKMax + (sl < kKMax ? sl : sl - kKMax));
+        }
+      }
+      block_reduce<3>(red, sm, ops);
+      if (threadIdx.x == 0) {
+        EpiCtaQ eq;
+        eq.st = st; eq.i = i;
+        double rq[1] = {red[0]};
+        eq.finish(rq);
+        EpiCtaP ep;
+        ep.st = st; ep.i = i; ep.with_solve = 1;
+        double rp[2] = {red[1], red[2]};
+        if (i == t) ktimer_end(ep0.timer());
+        ep.finish(rp);
+      }
+      __syncthreads();
+    }
+    EpiCtaP ep;
+    ep.st = st; ep.i = t; ep.with_solve = 1;
+    ep.finish_block();
+  }
+}
+
+inline bool csr_chain_ok(const Mat& M, int npairs) {
+  static const bool off = [] {
+    const char* e = getenv("TS_CSR_CHAIN");
+    return e && e[0] == '0';
+  }();
+  // a banded square matrix keeps one kernel per pair (k_pair_band, halo recomputation
+  // instead of barriers): on C3, 391 blocks, 7.4 us per pair against the chain's 8.3
+  return !off && npairs >= 1 && npairs <= kChainMaxT && M.kind == 1 && !M.comm && !band_pair_ok(M) &&
+         M.planN.kind == PLAN_SHORT && M.planT.kind == PLAN_SHORT &&
+         std::max(M.planN.P, M.planT.P) <= M.sms * kMinBlocks;
+}
+inline int launch_chain_csr(const Mat& M, const KrylovPtrs& kp, SolveState* st, int npairs, int slot,
+                            const Work& wk, cudaStream_t s) {
+  const int PT = M.planT.P, PN = M.planN.P;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::max(PT, PN));
+  cfg.blockDim = dim3(kNT);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_csr, M.csrT(), M.csr(), kp, st, npairs, slot, wk, PT, PN));
+  return 0;
+}
+
 }  // namespace ts

@@ -838,6 +838,10 @@ static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, i
     ++g_launches;
     return launch_chain_wdense(op.M, I->kp, I->ds, npairs, slot, I->wk, s);
   }
+  if (gram && !op.normal && solve_last && csr_chain_ok(op.M, npairs)) {  // L2-resident short-row CSR: the same
+    ++g_launches;
+    return launch_chain_csr(op.M, I->kp, I->ds, npairs, slot, I->wk, s);
+  }
   for (int i = 1; i <= npairs; ++i) {
     if (dpair) {  // small dense: both passes in one cooperative kernel
       EpiCtaQ eq;

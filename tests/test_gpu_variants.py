@@ -13,7 +13,8 @@ interpreter (``tests/_variant_probe.py`` prints digests of the iterates):
   small dense matrix (k_pair_wdense, cooperative, grid barrier between the two
   products) against the two passes (TS_BAND_PAIR=0, TS_DENSE_PAIR=0), and all
   pairs of an iteration chained in one kernel (k_chain_wdense, the default for
-  small dense matrices) against one kernel per pair (TS_DENSE_CHAIN=0);
+  small dense matrices; k_chain_csr for L2-resident short-row CSR) against one
+  kernel per pair (TS_DENSE_CHAIN=0, TS_CSR_CHAIN=0);
 * the warp-per-row small dense kernel against the tile kernel
   (TS_DENSE_SMALL=tile): same statuses and iteration counts, iterates within
   north_star's 1e-9 (the dot products are summed in another order, and TA
@@ -39,7 +40,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _probe(**env):
     e = dict(os.environ)
-    for k in ("TS_CTA_SWITCH", "TS_NO_GRAPH", "TS_BAND_PAIR", "TS_DENSE_PAIR", "TS_DENSE_CHAIN", "TS_DENSE_SMALL"):
+    for k in ("TS_CTA_SWITCH", "TS_NO_GRAPH", "TS_BAND_PAIR", "TS_DENSE_PAIR", "TS_DENSE_CHAIN", "TS_CSR_CHAIN", "TS_DENSE_SMALL"):
         e.pop(k, None)
     e.update(env)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_variant_probe.py")], env=e, cwd=ROOT,
@@ -54,9 +55,10 @@ def default_run():
 
 
 @pytest.mark.parametrize("env", [{"TS_CTA_SWITCH": "1"}, {"TS_NO_GRAPH": "1"}, {"TS_BAND_PAIR": "0"},
-                                 {"TS_DENSE_PAIR": "0"}, {"TS_DENSE_CHAIN": "0"}],
+                                 {"TS_DENSE_PAIR": "0"}, {"TS_DENSE_CHAIN": "0"}, {"TS_CSR_CHAIN": "0"},
+                                 {"TS_CSR_CHAIN": "0", "TS_BAND_PAIR": "0"}],
                          ids=["switch_graph", "direct_launches", "two_pass_band_pairs", "two_pass_dense_pairs",
-                              "dense_pair_kernels"])
+                              "dense_pair_kernels", "csr_pair_passes", "csr_two_passes"])
 def test_structure_variants_are_bitwise(default_run, env):
     got = _probe(**env)
     assert got.keys() == default_run.keys()
