@@ -402,6 +402,9 @@ def ours_arm(args, cfg):
                                   "share_of_step": float(kms[2] / ms)}
     breakdown["hankel solves (in-finisher)"] = {"launches": int(kcnt[3]), "ms_total": float(kms[3]),
                                    "share_of_step": float(kms[3] / ms)}
+    breakdown["note"] = ("per class: matrix products timed on the device (kernel entry or state-word read to the "
+                         "finisher); 'launches' counts products — the one-kernel moment pairs / chains of the "
+                         "latency-bound configs perform 2 / 2t products per launch and are booked under 'A v'")
     dom = max((k for k in classes if kcnt[k]), key=lambda k: kms[k])
     dom_name = classes[dom][0]
     achieved = breakdown[dom_name]["gbs"]

@@ -232,11 +232,13 @@ __device__ __forceinline__ void ktimer_begin(KTimer* kt) {
 __device__ __forceinline__ void ktimer_begin_at(KTimer* kt, unsigned long long t_entry) {
   if (kt && threadIdx.x == 0) atomicMin(&kt->start, t_entry);
 }
-__device__ __forceinline__ void ktimer_end(KTimer* kt) {
+// `products`: matrix products the launch performed (pair / chain kernels: 2 / 2 t), so
+// the class average stays a time per product
+__device__ __forceinline__ void ktimer_end(KTimer* kt, int products = 1) {
   if (kt) {
     const unsigned long long now = globaltimer();
     kt->total_ns += now - kt->start;
-    kt->count += 1;
+    kt->count += products;
     kt->start = ~0ull;
   }
 }

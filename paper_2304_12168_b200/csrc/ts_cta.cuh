@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(kNT, 2) k_chain_wdense(const __grid_constant__
         EpiCtaP ep;
         ep.st = st; ep.i = i; ep.with_solve = 1;
         double rp[2] = {red[1], red[2]};
-        if (i == t) ktimer_end(ep0.timer());
+        if (i == t) ktimer_end(ep0.timer(), 2 * t);
         ep.finish(rp);
       }
       __syncthreads();
@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_chain_csr(const __grid_cons
         EpiCtaP ep;
         ep.st = st; ep.i = i; ep.with_solve = 1;
         double rp[2] = {red[1], red[2]};
-        if (i == t) ktimer_end(ep0.timer());
+        if (i == t) ktimer_end(ep0.timer(), 2 * t);
         ep.finish(rp);
       }
       __syncthreads();

@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) k_pair_band(CsrRows AT, CsrRo
     double red[K];
     reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, ops);
     if (threadIdx.x == 0) {
-      ktimer_end(ep.timer());
+      ktimer_end(ep.timer(), 2);
       double rq[KQ], rp2[KP];
 #pragma unroll
       for (int k = 0; k < KQ; ++k) rq[k] = red[k];
@@ -1282,7 +1282,7 @@ __global__ void __launch_bounds__(kNT, 2) k_pair_wdense(const __grid_constant__ 
     double red[K];
     reduce_partials<K>(wk.bacc, nullptr, (int)P, red, sm, ops);
     if (threadIdx.x == 0) {
-      ktimer_end(ep.timer());
+      ktimer_end(ep.timer(), 2);
       double rq[KQ], rp2[KP];
 #pragma unroll
       for (int k = 0; k < KQ; ++k) rq[k] = red[k];
