@@ -954,6 +954,7 @@ inline int launch_chain_wdense(const Mat& M, const KrylovPtrs& kp, SolveState* s
   cfg.numAttrs = 1;
   const DenseRows dT{M.aT, M.ldaT, M.n, M.m};
   const int64_t len = std::max(M.m, M.n);
+  if (!coop_fits(k_chain_wdense<16>, P, M)) return kNoCoop;
   if (len <= 4 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<4>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
   else if (len <= 8 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<8>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
   else TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<16>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
@@ -1099,6 +1100,7 @@ inline int launch_chain_csr(const Mat& M, const KrylovPtrs& kp, SolveState* st, 
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (!coop_fits(k_chain_csr, std::max(PT, PN), M)) return kNoCoop;
   TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_csr, M.csrT(), M.csr(), kp, st, npairs, slot, wk, PT, PN));
   return 0;
 }

@@ -833,14 +833,23 @@ static int cta_probe_finish(const CtaOp& op, const Instance* I, cudaStream_t s) 
 static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, int solve_last,
                      cudaStream_t s, int slot = -1) {
   const bool pair = gram && !op.normal && band_pair_ok(op.M);
-  const bool dpair = gram && !op.normal && dense_pair_ok(op.M);
+  bool dpair = gram && !op.normal && dense_pair_ok(op.M);
+  // (kNoCoop from a launch helper: the cooperative grid would not be co-resident
+  // on this device; the barrier-free kernels below take over)
   if (dpair && solve_last && dense_chain_ok(op.M, npairs)) {  // every pair of the iteration in one kernel
-    ++g_launches;
-    return launch_chain_wdense(op.M, I->kp, I->ds, npairs, slot, I->wk, s);
+    const int rc = launch_chain_wdense(op.M, I->kp, I->ds, npairs, slot, I->wk, s);
+    if (rc != kNoCoop) {
+      ++g_launches;
+      return rc;
+    }
+    dpair = false;
   }
   if (gram && !op.normal && solve_last && csr_chain_ok(op.M, npairs)) {  // L2-resident short-row CSR: the same
-    ++g_launches;
-    return launch_chain_csr(op.M, I->kp, I->ds, npairs, slot, I->wk, s);
+    const int rc = launch_chain_csr(op.M, I->kp, I->ds, npairs, slot, I->wk, s);
+    if (rc != kNoCoop) {
+      ++g_launches;
+      return rc;
+    }
   }
   for (int i = 1; i <= npairs; ++i) {
     if (dpair) {  // small dense: both passes in one cooperative kernel
@@ -849,8 +858,14 @@ static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, i
       EpiCtaP ep;
       ep.st = I->ds; ep.pprev = I->kp.p[i - 1]; ep.p = I->kp.p[i]; ep.i = i;
       ep.with_solve = solve_last; ep.tclass = 0; ep.slot = slot;
+      const int rc = launch_pair_wdense(op.M, I->kp.p[i - 1], I->kp.q[i - 1], eq, ep, I->wk, s);
+      if (rc == kNoCoop) {
+        dpair = false;
+        --i;  // this pair again, as two passes
+        continue;
+      }
       ++g_launches;
-      TS_CHECK(launch_pair_wdense(op.M, I->kp.p[i - 1], I->kp.q[i - 1], eq, ep, I->wk, s));
+      TS_CHECK(rc);
     } else if (pair) {  // q_i = A^T p_{i-1} and p_i = A q_i in one kernel (square banded, L2-resident)
       EpiCtaQ eq;
       eq.st = I->ds; eq.q = I->kp.q[i - 1]; eq.i = i; eq.tclass = 1; eq.slot = slot;

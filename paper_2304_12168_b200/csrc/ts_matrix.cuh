@@ -201,6 +201,27 @@ int launch_pair_band(const Mat& M, const double* pprev, const EpiQ& eq, const Ep
   return 0;
 }
 
+// Cooperative kernels (grid barriers) need their whole grid resident: the device
+// must support cooperative launches and `grid` blocks of the kernel must fit
+// (occupancy x multiprocessors; asked once per kernel and device).  false: the
+// caller keeps the barrier-free kernels.
+template <class Kern>
+inline bool coop_fits(Kern kernel, int grid, const Mat& M) {
+  static int per_sm[64] = {0};  // 0: not asked yet, -1: no
+  const int d = (M.dev >= 0 && M.dev < 64) ? M.dev : 0;
+  if (per_sm[d] == 0) {
+    int coop = 0, nb = 0;
+    if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, M.dev) != cudaSuccess || !coop ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kNT, 0) != cudaSuccess || nb < 1) {
+      cudaGetLastError();
+      nb = -1;
+    }
+    per_sm[d] = nb;
+  }
+  return per_sm[d] > 0 && grid <= per_sm[d] * M.sms;
+}
+constexpr int kNoCoop = -7001;  // launch helper: the grid would not be co-resident
+
 // A small L2-resident dense matrix (both orientations on the warp-per-row
 // kernel) runs a CTA moments pair as one cooperative kernel (k_pair_wdense);
 // TS_DENSE_PAIR=0 keeps the two passes
@@ -229,6 +250,7 @@ int launch_pair_wdense(const Mat& M, const double* pprev, const double* q, const
   cfg.numAttrs = 1;
   const DenseRows dT{M.aT, M.ldaT, M.n, M.m};
   const int64_t len = std::max(M.m, M.n);  // the longer of the two staged vectors
+  if (!coop_fits(k_pair_wdense<EpiQ, EpiP, 16>, P, M)) return kNoCoop;
   if (len <= 4 * kNT)
     TS_CUDA(cudaLaunchKernelEx(&cfg, k_pair_wdense<EpiQ, EpiP, 4>, dT, M.dense(), pprev, q, eq, ep, wk, PT, PN));
   else if (len <= 8 * kNT)
