@@ -902,11 +902,25 @@ static int cta_step_kernels(const CtaOp& op, const Instance* I, int npairs, int 
   const int64_t mo = op.mo(), no = op.no();
   EpiCtaCand ecd;
   ecd.st = I->ds; ecd.kp = I->kp; ecd.m = mo; ecd.slot = slot;
-  TS_CHECK(vecpass(op.M, mo, ecd, I->wk, s));
+  // both vector passes single-block (<= 1024 unknowns, unsharded): one kernel for the two
+  static const bool vec_fuse_off = [] {
+    const char* e = getenv("TS_VEC_FUSE");
+    return e && e[0] == '0';
+  }();
+  const bool fuse = !vec_fuse_off && !op.M.comm && vec_grid(std::max(mo, no), op.M.sms) == 1;
+  if (!fuse) TS_CHECK(vecpass(op.M, mo, ecd, I->wk, s));
   EpiCtaUpd eu;
   eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = mo;
   eu.n = no; eu.gram = gram;
   eu.sw = hsw; eu.use_sw = ncases > 0; eu.ncases = ncases; eu.slot = slot;
+  if (fuse) {
+    ++g_launches;
+    ecd.tclass = 2;
+    eu.tclass = 2;
+    k_vec2<EpiCtaCand, EpiCtaUpd><<<1, kNT, 0, s>>>(mo, ecd, std::max(mo, no), eu, I->wk);
+    TS_CUDA(cudaGetLastError());
+    return 0;
+  }
   return vecpass(op.M, std::max(mo, no), eu, I->wk, s);
 }
 

@@ -1496,4 +1496,26 @@ __global__ void __launch_bounds__(kNT, kVecBlocksOf<Epi>) k_vec(int64_t len, Epi
   body_vec<Epi, false>(len, epi, wk, blockIdx.x, gridDim.x);
 }
 
+// Two single-block vector passes in one kernel (systems of <= 1024 unknowns: the
+// CTA candidate and update passes of C1): the second pass starts after the first
+// one's finisher has written the state, in the same block — one launch, one
+// kernel boundary less.  Each pass keeps its own activity test, accounting,
+// thread <-> element mapping and finisher.
+template <class EA, class EB>
+__global__ void __launch_bounds__(kNT, (kVecBlocksOf<EA> < kVecBlocksOf<EB> ? kVecBlocksOf<EA> : kVecBlocksOf<EB>))
+    k_vec2(int64_t len_a, EA ea, int64_t len_b, EB eb, Work wk) {
+  if (threadIdx.x == 0) ea.count_launch();
+  if (!ea.active()) {
+    if (threadIdx.x == 0) ea.idle();
+  } else {
+    body_vec<EA, false>(len_a, ea, wk, 0, 1);
+  }
+  __syncthreads();  // the first finisher's state, visible to the whole block
+  if (!eb.active()) {
+    if (threadIdx.x == 0) eb.idle();
+    return;
+  }
+  body_vec<EB, false>(len_b, eb, wk, 0, 1);
+}
+
 }  // namespace ts
