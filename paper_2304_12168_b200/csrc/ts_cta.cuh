@@ -785,12 +785,22 @@ struct EpiCtaRecheck : EpiBase {
 // bits of the separate passes.  Up to 5 pairs (15 sums in the two partial rows).
 constexpr int kChainMaxT = 5;
 
-template <int XN>
+// kTail: systems of <= 1024 unknowns — the last block, once it has run the pairs'
+// finishers and the Hankel solves, goes straight on with the candidate and the
+// update pass (single-block passes: no other block is needed), so a whole CTA
+// iteration is ONE kernel.
+struct ChainTail {
+  EpiCtaCand cand;
+  EpiCtaUpd upd;
+  int64_t len_cand, len_upd;
+};
+
+template <int XN, bool kTail>
 __global__ void __launch_bounds__(kNT, 2) k_chain_wdense(const __grid_constant__ DenseRows AT,
                                                         const __grid_constant__ DenseRows A,
                                                         const __grid_constant__ KrylovPtrs kp, SolveState* st,
                                                         int npairs, int slot, const __grid_constant__ Work wk,
-                                                        int PT, int PN) {
+                                                        int PT, int PN, const __grid_constant__ ChainTail tail) {
   constexpr int C = kWdChunks;
   __shared__ double sm[kWarps * kKMax];
   __shared__ __align__(16) double xsl[kWdMaxN + 64];
@@ -858,7 +868,13 @@ __global__ void __launch_bounds__(kNT, 2) k_chain_wdense(const __grid_constant__
   int64_t r = t0 + wid;
   if (r < t1) load(AT, r, 0);  // the matrix is immutable: in flight with the state word
   if (!ep0.active()) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) ep0.idle();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ep0.idle();
+      if constexpr (kTail) {  // the passes that would have followed: inactive too, the update owns the loop condition
+        tail.cand.idle();
+        tail.upd.idle();
+      }
+    }
     return;
   }
   ktimer_begin_at(ep0.timer(), t_in);
@@ -929,6 +945,22 @@ __global__ void __launch_bounds__(kNT, 2) k_chain_wdense(const __grid_constant__
     EpiCtaP ep;
     ep.st = st; ep.i = t; ep.with_solve = 1;
     ep.finish_block();
+    if constexpr (kTail) {
+      __syncthreads();  // the finishers' state, visible to the whole block
+      EpiCtaCand ec = tail.cand;
+      EpiCtaUpd eu = tail.upd;
+      if (!ec.active()) {
+        if (threadIdx.x == 0) ec.idle();
+      } else {
+        body_vec<EpiCtaCand, false>(tail.len_cand, ec, wk, 0, 1);
+      }
+      __syncthreads();
+      if (!eu.active()) {
+        if (threadIdx.x == 0) eu.idle();
+      } else {
+        body_vec<EpiCtaUpd, false>(tail.len_upd, eu, wk, 0, 1);
+      }
+    }
   }
 }
 
@@ -940,7 +972,7 @@ inline bool dense_chain_ok(const Mat& M, int npairs) {
   return !off && npairs >= 1 && npairs <= kChainMaxT && dense_pair_ok(M);
 }
 inline int launch_chain_wdense(const Mat& M, const KrylovPtrs& kp, SolveState* st, int npairs, int slot,
-                               const Work& wk, cudaStream_t s) {
+                               const Work& wk, cudaStream_t s, const ChainTail* tail = nullptr) {
   const int PT = std::min(M.planT.P, 2 * M.sms), PN = std::min(M.planN.P, 2 * M.sms);
   const int P = std::max(PT, PN);
   cudaLaunchConfig_t cfg = {};
@@ -954,10 +986,16 @@ inline int launch_chain_wdense(const Mat& M, const KrylovPtrs& kp, SolveState* s
   cfg.numAttrs = 1;
   const DenseRows dT{M.aT, M.ldaT, M.n, M.m};
   const int64_t len = std::max(M.m, M.n);
-  if (!coop_fits(k_chain_wdense<16>, P, M)) return kNoCoop;
-  if (len <= 4 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<4>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
-  else if (len <= 8 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<8>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
-  else TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<16>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN));
+  if (!coop_fits(k_chain_wdense<16, false>, P, M)) return kNoCoop;
+  if (tail) {  // (<= 1024 unknowns: the 4-entry staging variant)
+    if (!coop_fits(k_chain_wdense<4, true>, P, M)) return kNoCoop;
+    TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<4, true>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN, *tail));
+    return 0;
+  }
+  const ChainTail none{};
+  if (len <= 4 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<4, false>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN, none));
+  else if (len <= 8 * kNT) TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<8, false>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN, none));
+  else TS_CUDA(cudaLaunchKernelEx(&cfg, k_chain_wdense<16, false>, dT, M.dense(), kp, st, npairs, slot, wk, PT, PN, none));
   return 0;
 }
 

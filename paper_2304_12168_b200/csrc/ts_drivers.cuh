@@ -897,22 +897,38 @@ static int cta_pairs(const CtaOp& op, const Instance* I, int npairs, int gram, i
 static int cta_step_kernels(const CtaOp& op, const Instance* I, int npairs, int gram, cudaStream_t s,
                             cudaGraphConditionalHandle h, int use, int enhanced = 0,
                             cudaGraphConditionalHandle hsw = 0, int ncases = 0, int slot = -1) {
-  TS_CHECK(cta_pairs(op, I, npairs, gram, 1, s, slot));
-  if (enhanced) TS_CHECK(cta_probe_kernels(op, I, npairs, gram, s));
   const int64_t mo = op.mo(), no = op.no();
   EpiCtaCand ecd;
   ecd.st = I->ds; ecd.kp = I->kp; ecd.m = mo; ecd.slot = slot;
+  EpiCtaUpd eu;
+  eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = mo;
+  eu.n = no; eu.gram = gram;
+  eu.sw = hsw; eu.use_sw = ncases > 0; eu.ncases = ncases; eu.slot = slot;
   // both vector passes single-block (<= 1024 unknowns, unsharded): one kernel for the two
   static const bool vec_fuse_off = [] {
     const char* e = getenv("TS_VEC_FUSE");
     return e && e[0] == '0';
   }();
   const bool fuse = !vec_fuse_off && !op.M.comm && vec_grid(std::max(mo, no), op.M.sms) == 1;
+  // ... and behind a chained small dense matrix, the whole iteration is one kernel
+  static const bool tail_off = [] {
+    const char* e = getenv("TS_CHAIN_TAIL");
+    return e && e[0] == '0';
+  }();
+  if (fuse && !tail_off && !enhanced && gram && !op.normal && dense_pair_ok(op.M) && dense_chain_ok(op.M, npairs)) {
+    ChainTail tl;
+    tl.cand = ecd; tl.cand.tclass = 2;
+    tl.upd = eu; tl.upd.tclass = 2;
+    tl.len_cand = mo; tl.len_upd = std::max(mo, no);
+    const int rc = launch_chain_wdense(op.M, I->kp, I->ds, npairs, slot, I->wk, s, &tl);
+    if (rc != kNoCoop) {
+      ++g_launches;
+      return rc;
+    }
+  }
+  TS_CHECK(cta_pairs(op, I, npairs, gram, 1, s, slot));
+  if (enhanced) TS_CHECK(cta_probe_kernels(op, I, npairs, gram, s));
   if (!fuse) TS_CHECK(vecpass(op.M, mo, ecd, I->wk, s));
-  EpiCtaUpd eu;
-  eu.st = I->ds; eu.cond = h; eu.use_cond = use; eu.kp = I->kp; eu.x = I->x; eu.m = mo;
-  eu.n = no; eu.gram = gram;
-  eu.sw = hsw; eu.use_sw = ncases > 0; eu.ncases = ncases; eu.slot = slot;
   if (fuse) {
     ++g_launches;
     ecd.tclass = 2;

@@ -178,7 +178,7 @@ __device__ __forceinline__ void finish_last(Epi& epi, const Work& wk, const doub
       double red[K];
 #pragma unroll
       for (int k = 0; k < K; ++k)
-        red[k] = red_combine(epi.op(k), red_identity(epi.op(k)), wk.bacc[blockIdx.x * kKMax + k]);
+        red[k] = red_combine(epi.op(k), red_identity(epi.op(k)), wk.bacc[k]);  // block slot 0: the only one
       ktimer_end(epi.timer());
       epi.finish(red);
     }

@@ -16,7 +16,9 @@ interpreter (``tests/_variant_probe.py`` prints digests of the iterates):
   small dense matrices; k_chain_csr for L2-resident short-row CSR) against one
   kernel per pair (TS_DENSE_CHAIN=0, TS_CSR_CHAIN=0);
 * the candidate and update passes of small systems in one single-block kernel
-  (k_vec2) against two kernels (TS_VEC_FUSE=0);
+  (k_vec2) against two kernels (TS_VEC_FUSE=0), and run by the chain kernel's
+  last block (a whole iteration in one kernel) against a kernel of their own
+  (TS_CHAIN_TAIL=0);
 * the warp-per-row small dense kernel against the tile kernel
   (TS_DENSE_SMALL=tile): same statuses and iteration counts, iterates within
   north_star's 1e-9 (the dot products are summed in another order, and TA
@@ -42,7 +44,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _probe(**env):
     e = dict(os.environ)
-    for k in ("TS_CTA_SWITCH", "TS_NO_GRAPH", "TS_BAND_PAIR", "TS_DENSE_PAIR", "TS_DENSE_CHAIN", "TS_CSR_CHAIN", "TS_VEC_FUSE", "TS_DENSE_SMALL"):
+    for k in ("TS_CTA_SWITCH", "TS_NO_GRAPH", "TS_BAND_PAIR", "TS_DENSE_PAIR", "TS_DENSE_CHAIN", "TS_CSR_CHAIN", "TS_VEC_FUSE", "TS_CHAIN_TAIL", "TS_DENSE_SMALL"):
         e.pop(k, None)
     e.update(env)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_variant_probe.py")], env=e, cwd=ROOT,
@@ -58,9 +60,11 @@ def default_run():
 
 @pytest.mark.parametrize("env", [{"TS_CTA_SWITCH": "1"}, {"TS_NO_GRAPH": "1"}, {"TS_BAND_PAIR": "0"},
                                  {"TS_DENSE_PAIR": "0"}, {"TS_DENSE_CHAIN": "0"}, {"TS_CSR_CHAIN": "0"},
-                                 {"TS_CSR_CHAIN": "0", "TS_BAND_PAIR": "0"}, {"TS_VEC_FUSE": "0"}],
+                                 {"TS_CSR_CHAIN": "0", "TS_BAND_PAIR": "0"}, {"TS_VEC_FUSE": "0"},
+                                 {"TS_CHAIN_TAIL": "0"}],
                          ids=["switch_graph", "direct_launches", "two_pass_band_pairs", "two_pass_dense_pairs",
-                              "dense_pair_kernels", "csr_pair_passes", "csr_two_passes", "separate_vector_kernels"])
+                              "dense_pair_kernels", "csr_pair_passes", "csr_two_passes", "separate_vector_kernels",
+                              "vector_kernel_after_chain"])
 def test_structure_variants_are_bitwise(default_run, env):
     got = _probe(**env)
     assert got.keys() == default_run.keys()
