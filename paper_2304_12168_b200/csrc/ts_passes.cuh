@@ -1457,14 +1457,17 @@ __global__ void __launch_bounds__(kNT, kTileNBlocks) k_rows_tile_fused(DenseRows
 }
 
 // ----------------------------------------------------------------- k_vec ----
+// `prepared`: the caller has run epi.prepare() already (k_vec: ahead of the
+// activity test, so the two state reads overlap)
 template <class Epi, bool kP>
-__device__ __forceinline__ void body_vec(int64_t len, Epi& epi, const Work& wk, int64_t b, int64_t P) {
+__device__ __forceinline__ void body_vec(int64_t len, Epi& epi, const Work& wk, int64_t b, int64_t P,
+                                         bool prepared = false) {
   constexpr int K = Epi::K;
   __shared__ double sm[kWarps * kKMax];
   __shared__ int sflag;
   ktimer_begin(epi.timer());
   __shared__ double epi_smem[kEpiSmem];
-  epi.prepare(epi_smem);
+  if (!prepared) epi.prepare(epi_smem);
   __syncthreads();
   double acc[K];
 #pragma unroll
@@ -1489,11 +1492,15 @@ __device__ __forceinline__ void body_vec(int64_t len, Epi& epi, const Work& wk, 
 template <class Epi>
 __global__ void __launch_bounds__(kNT, kVecBlocksOf<Epi>) k_vec(int64_t len, Epi epi, Work wk) {
   if (blockIdx.x == 0 && threadIdx.x == 0) epi.count_launch();
+  // the epilogue's scalars (shared memory only: no side effect) are fetched
+  // together with the words the activity test reads: one round trip, not two
+  __shared__ double pre_smem[kEpiSmem];
+  epi.prepare(pre_smem);
   if (!epi.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.idle();
     return;
   }
-  body_vec<Epi, false>(len, epi, wk, blockIdx.x, gridDim.x);
+  body_vec<Epi, false>(len, epi, wk, blockIdx.x, gridDim.x, true);
 }
 
 // Two single-block vector passes in one kernel (systems of <= 1024 unknowns: the
